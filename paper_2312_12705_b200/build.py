@@ -1,0 +1,71 @@
+"""Builds the in-tree native library ``lib/libtrainplan_b200.so`` with nvcc for sm_100a.
+
+The library holds every CUDA kernel (K1-K12), the C++ host runtime (train step, 1F1B
+executor, NCCL communicators) and the C-ABI declared in ``include/trainplan/capi.h``.
+Incremental: an object is rebuilt when its source or any header under ``csrc``/``include``
+is newer than it.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+BUILD = PKG / "build"
+LIB = PKG / "lib" / "libtrainplan_b200.so"
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
+          f"-I{ROOT / 'include'}", f"-I{CSRC}", "-I/usr/local/cuda/include"]
+LINK = ["-shared", "-lcudart", "-lnccl", "-lgomp", "-L/usr/lib/x86_64-linux-gnu",
+        "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+
+
+def _sources() -> list[Path]:
+    return sorted(p for p in CSRC.rglob("*") if p.suffix in (".cu", ".cpp"))
+
+
+def _headers_mtime() -> float:
+    hs = [p for d in (CSRC, ROOT / "include") for p in d.rglob("*") if p.suffix in (".h", ".cuh", ".hpp")]
+    return max((h.stat().st_mtime for h in hs), default=0.0)
+
+
+def _compile(src: Path, hdr_mtime: float) -> Path:
+    obj = BUILD / (src.relative_to(CSRC).as_posix().replace("/", "__") + ".o")
+    if obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_mtime):
+        return obj
+    cmd = [NVCC, *ARCH, *COMMON, "-c", str(src), "-o", str(obj)]
+    if src.suffix == ".cpp":
+        cmd[1:1] = ["-x", "cu"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    return obj
+
+
+def build(verbose: bool = False) -> Path:
+    BUILD.mkdir(exist_ok=True)
+    LIB.parent.mkdir(exist_ok=True)
+    hdr = _headers_mtime()
+    srcs = _sources()
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        objs = list(ex.map(lambda s: _compile(s, hdr), srcs))
+    newest = max(o.stat().st_mtime for o in objs)
+    if not LIB.exists() or LIB.stat().st_mtime < newest:
+        cmd = [NVCC, *ARCH, *[str(o) for o in objs], "-o", str(LIB), *LINK]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    if verbose:
+        print(f"built {LIB}")
+    return LIB
+
+
+if __name__ == "__main__":
+    build(verbose=True)
+    sys.exit(0)

@@ -1,0 +1,39 @@
+// Host-facing declaration of the sm_100a GEMM (see gemm_sm100.cu for the kernel).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace gptb200 {
+
+enum GemmEpilogue {
+  EPI_BF16 = 0,       // C(bf16) = acc (+ bias[n])
+  EPI_BIAS_GELU = 1,  // C(bf16) = acc + bias[n];  C2(bf16) = gelu_tanh(C)
+  EPI_F32 = 2,        // C(fp32) = acc, or C += acc when accumulate != 0
+  EPI_DGELU = 3,      // C(bf16) = acc * gelu_tanh'(aux[m,n])
+};
+
+enum GemmStatus { kGemmOk = 0, kGemmErrShape = 1, kGemmErrTmap = 2, kGemmErrCuda = 3 };
+
+struct GemmParams {
+  int M = 0, N = 0, K = 0;
+  const __nv_bfloat16* A = nullptr;
+  int lda = 0;
+  bool a_mn = false;  // A stored [K][M] (M contiguous) instead of [M][K]
+  const __nv_bfloat16* B = nullptr;
+  int ldb = 0;
+  bool b_mn = false;  // B stored [K][N] instead of [N][K]
+  void* C = nullptr;  // bf16 or fp32 depending on epi
+  int ldc = 0;
+  int epi = EPI_BF16;
+  const __nv_bfloat16* bias = nullptr;  // [N]
+  __nv_bfloat16* C2 = nullptr;          // second output (EPI_BIAS_GELU), ld = ldc
+  const __nv_bfloat16* aux = nullptr;   // EPI_DGELU pre-activation
+  int ldaux = 0;
+  int accumulate = 0;
+};
+
+// Requires M % 128 == 0, K % 64 == 0, N % 64 == 0, 16-byte aligned rows.
+int gemm_bf16(const GemmParams& p, cudaStream_t stream);
+
+}  // namespace gptb200

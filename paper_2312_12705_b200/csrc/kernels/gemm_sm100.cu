@@ -1,0 +1,385 @@
+// K1-K4: Megatron column/row-parallel GEMMs (forward, dgrad, wgrad) on sm_100a.
+//
+// One persistent, warp-specialised kernel computes C[m,n] = sum_k A(m,k) * B(n,k) with
+//   A(m,k) = A[m*lda + k]  (K-major)  or  A[k*lda + m]  (MN-major)
+//   B(n,k) = B[n*ldb + k]  (K-major)  or  B[k*ldb + n]  (MN-major)
+// which covers every GEMM of the GPT block (row-major tensors throughout):
+//   forward  Y  = X  . W^T   A=X  K-major, B=W  K-major
+//   dgrad    dX = dY . W     A=dY K-major, B=W  MN-major
+//   wgrad    dW = dY^T . X   A=dY MN-major, B=X MN-major  (fp32 accumulate into main grad)
+//
+// Roles per CTA (192 threads): warp 0 = TMA producer, warp 1 = TMEM owner + tcgen05.mma
+// issuer, warps 2..5 = epilogue (TMEM -> registers -> fused epilogue -> HBM). Operand tiles
+// land in 128B-swizzled shared memory through TMA; the fp32 accumulator lives in TMEM and
+// is double-buffered so the epilogue of tile i overlaps the MMAs of tile i+1.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "gemm.h"
+#include "sm100_ptx.cuh"
+
+namespace gptb200 {
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+constexpr int kThreads = 192;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (BN == 256) ? 4 : 6;
+  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+};
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  float t = tanhf(k0 * (x + k1 * x * x * x));
+  return 0.5f * x * (1.f + t);
+}
+
+__device__ __forceinline__ float gelu_tanh_grad(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  float t = tanhf(k0 * (x + k1 * x * x * x));
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
+}
+
+// Tile order: groups of 8 M-blocks sweep all N-blocks so concurrently running CTAs share
+// both operand panels in L2.
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
+  constexpr int kGroup = 8;
+  int group = tile / (kGroup * num_n);
+  int first_m = group * kGroup;
+  int gsize = min(kGroup, num_m - first_m);
+  int in_group = tile - group * kGroup * num_n;
+  mb = first_m + in_group % gsize;
+  nb = in_group / gsize;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
+                      const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int kStages = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmA);
+    ptx::tma_prefetch_desc(&tmB);
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 4);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_m = p.M / kBM;
+  const int num_n = p.N / BN;
+  const int num_tiles = num_m * num_n;
+  const int kblocks = p.K / kBK;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, mb, nb);
+        const int m0 = mb * kBM, n0 = nb * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * Cfg::kStageBytes;
+          uint8_t* sb = sa + Cfg::kABytes;
+          ptx::mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+          const int k0 = kb * kBK;
+          if constexpr (A_MN) {
+#pragma unroll
+            for (int c = 0; c < kBM / 64; ++c)
+              ptx::tma_load_2d(sa + c * kBK * 128, &tmA, &full[stage], m0 + 64 * c, k0);
+          } else {
+            ptx::tma_load_2d(sa, &tmA, &full[stage], k0, m0);
+          }
+          if constexpr (B_MN) {
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c)
+              ptx::tma_load_2d(sb + c * kBK * 128, &tmB, &full[stage], n0 + 64 * c, k0);
+          } else {
+            ptx::tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kBM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        ptx::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(smem + stage * Cfg::kStageBytes);
+          const uint32_t sb = sa + Cfg::kABytes;
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            uint64_t adesc, bdesc;
+            if constexpr (A_MN)
+              adesc = ptx::smem_desc_sw128(sa + k * 2048, kBK * 128, 1024);
+            else
+              adesc = ptx::smem_desc_sw128(sa + k * 32, 16, 1024);
+            if constexpr (B_MN)
+              bdesc = ptx::smem_desc_sw128(sb + k * 2048, kBK * 128, 1024);
+            else
+              bdesc = ptx::smem_desc_sw128(sb + k * 32, 16, 1024);
+            ptx::mma_bf16_ss(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          ptx::mma_commit(&empty[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::mma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, mb, nb);
+      const int acc = it & 1;
+      ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      ptx::tc_fence_after();
+      const int row = mb * kBM + 32 * q + lane;
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
+        ptx::tmem_ld_wait();
+        const int n = nb * BN + c * 32;
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        if constexpr (EPI == EPI_F32) {
+          float* dst = reinterpret_cast<float*>(p.C) + static_cast<size_t>(row) * p.ldc + n;
+          float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4 o = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            if (p.accumulate) {
+              float4 old = d4[j];
+              o.x += old.x;
+              o.y += old.y;
+              o.z += old.z;
+              o.w += old.w;
+            }
+            d4[j] = o;
+          }
+        } else {
+          if constexpr (EPI == EPI_BF16 || EPI == EPI_BIAS_GELU) {
+            if (p.bias != nullptr) {
+              const uint4* b4 = reinterpret_cast<const uint4*>(p.bias + n);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                uint4 bb = b4[j];
+                uint32_t w[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  float2 f = ptx::unpack_bf16(w[e]);
+                  v[8 * j + 2 * e] += f.x;
+                  v[8 * j + 2 * e + 1] += f.y;
+                }
+              }
+            }
+          }
+          if constexpr (EPI == EPI_DGELU) {
+            const uint4* h4 = reinterpret_cast<const uint4*>(
+                p.aux + static_cast<size_t>(row) * p.ldaux + n);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint4 hh = h4[j];
+              uint32_t w[4] = {hh.x, hh.y, hh.z, hh.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                float2 f = ptx::unpack_bf16(w[e]);
+                v[8 * j + 2 * e] *= gelu_tanh_grad(f.x);
+                v[8 * j + 2 * e + 1] *= gelu_tanh_grad(f.y);
+              }
+            }
+          }
+          uint32_t packed[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) packed[j] = ptx::pack_bf16(v[2 * j], v[2 * j + 1]);
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.C) +
+                                                static_cast<size_t>(row) * p.ldc + n);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            dst[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2],
+                                packed[4 * j + 3]);
+          if constexpr (EPI == EPI_BIAS_GELU) {
+            uint32_t g[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              float2 f = ptx::unpack_bf16(packed[j]);
+              g[j] = ptx::pack_bf16(gelu_tanh(f.x), gelu_tanh(f.y));
+            }
+            uint4* dst2 = reinterpret_cast<uint4*>(p.C2 + static_cast<size_t>(row) * p.ldc + n);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              dst2[j] = make_uint4(g[4 * j], g[4 * j + 1], g[4 * j + 2], g[4 * j + 3]);
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// 2D bf16 tensor map over a row-major [outer][inner] matrix with leading dimension ld
+// (elements), box {64, box_outer}, 128B swizzle.
+bool make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+               uint32_t box_outer) {
+  auto enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {64, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+int launch(const GemmParams& p, cudaStream_t stream) {
+  using Cfg = GemmCfg<BN>;
+  auto kern = gemm_sm100_kernel<BN, A_MN, B_MN, EPI>;
+  static bool attr_set = false;  // per instantiation; set once per process (single device)
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg::kSmemBytes) != cudaSuccess)
+      return kGemmErrCuda;
+    attr_set = true;
+  }
+  CUtensorMap ta, tb;
+  bool ok = A_MN ? make_tmap(&ta, p.A, p.M, p.K, p.lda, 64)
+                 : make_tmap(&ta, p.A, p.K, p.M, p.lda, kBM);
+  ok = ok && (B_MN ? make_tmap(&tb, p.B, p.N, p.K, p.ldb, 64)
+                   : make_tmap(&tb, p.B, p.K, p.N, p.ldb, BN));
+  if (!ok) return kGemmErrTmap;
+  const int tiles = (p.M / kBM) * (p.N / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, p);
+  return cudaGetLastError() == cudaSuccess ? kGemmOk : kGemmErrCuda;
+}
+
+template <int BN, int EPI>
+int dispatch_major(const GemmParams& p, cudaStream_t s) {
+  if (!p.a_mn && !p.b_mn) return launch<BN, false, false, EPI>(p, s);
+  if (!p.a_mn && p.b_mn) return launch<BN, false, true, EPI>(p, s);
+  if (p.a_mn && p.b_mn) return launch<BN, true, true, EPI>(p, s);
+  return launch<BN, true, false, EPI>(p, s);
+}
+
+template <int BN>
+int dispatch_epi(const GemmParams& p, cudaStream_t s) {
+  switch (p.epi) {
+    case EPI_BF16: return dispatch_major<BN, EPI_BF16>(p, s);
+    case EPI_BIAS_GELU: return dispatch_major<BN, EPI_BIAS_GELU>(p, s);
+    case EPI_F32: return dispatch_major<BN, EPI_F32>(p, s);
+    case EPI_DGELU: return dispatch_major<BN, EPI_DGELU>(p, s);
+    default: return kGemmErrShape;
+  }
+}
+
+}  // namespace
+
+int gemm_bf16(const GemmParams& p, cudaStream_t stream) {
+  if (p.M <= 0 || p.N <= 0 || p.K <= 0) return kGemmErrShape;
+  if (p.M % kBM != 0 || p.K % kBK != 0 || p.N % 64 != 0) return kGemmErrShape;
+  if (p.epi == EPI_BIAS_GELU && p.C2 == nullptr) return kGemmErrShape;
+  if (p.epi == EPI_DGELU && p.aux == nullptr) return kGemmErrShape;
+  // Prefer the widest N tile that divides N and still yields at least one full wave.
+  const bool n256 = (p.N % 256 == 0) && (p.M / kBM) * (p.N / 256) >= num_sms();
+  if (n256) return dispatch_epi<256>(p, stream);
+  if (p.N % 128 == 0) return dispatch_epi<128>(p, stream);
+  return dispatch_epi<64>(p, stream);
+}
+
+}  // namespace gptb200

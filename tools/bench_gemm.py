@@ -1,0 +1,126 @@
+"""GEMM kernel check + microbenchmark on one B200 (tcgen05 kernel vs torch/cuBLAS).
+
+python tools/bench_gemm.py [--quick]
+Prints one line per case: layout, shape, max rel err vs fp32 reference, TFLOP/s ours and cuBLAS.
+"""
+from __future__ import annotations
+
+import argparse
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2312_12705_b200 import _lib  # noqa: E402
+
+
+def run_case(M, N, K, a_mn, b_mn, epi=0, iters=20, check=True):
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(0)
+    A = (torch.randn(K, M, device=dev, generator=g) if a_mn else torch.randn(M, K, device=dev, generator=g)).bfloat16()
+    B = (torch.randn(K, N, device=dev, generator=g) if b_mn else torch.randn(N, K, device=dev, generator=g)).bfloat16()
+    Am = A.t() if a_mn else A  # [M,K]
+    Bm = B.t() if b_mn else B  # [N,K]
+    lda = M if a_mn else K
+    ldb = N if b_mn else K
+    bias = (torch.randn(N, device=dev, generator=g) * 0.1).bfloat16()
+    aux = torch.randn(M, N, device=dev, generator=g).bfloat16()
+    if epi == 2:
+        C = torch.randn(M, N, device=dev, generator=g)
+        C0 = C.clone()
+    else:
+        C = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    C2 = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+
+    def call():
+        _lib.gemm_bf16(M, N, K, A.data_ptr(), lda, a_mn, B.data_ptr(), ldb, b_mn, C.data_ptr(), N, epi,
+                       bias.data_ptr() if epi in (0, 1) else None, C2.data_ptr() if epi == 1 else None,
+                       aux.data_ptr() if epi == 3 else None, N, 1 if epi == 2 else 0,
+                       torch.cuda.current_stream().cuda_stream)
+
+    call()
+    torch.cuda.synchronize()
+    err = float("nan")
+    if check:
+        ref = Am.float() @ Bm.float().t()
+        if epi == 0:
+            ref = ref + bias.float()
+            out = C.float()
+        elif epi == 1:
+            pre = (ref + bias.float()).bfloat16().float()
+            out = C.float()
+            ref2 = torch.nn.functional.gelu(pre, approximate="tanh")
+            e2 = ((C2.float() - ref2).norm() / ref2.norm()).item()
+            ref = pre
+        elif epi == 2:
+            ref = ref + C0
+            out = C
+        else:
+            x = aux.float()
+            k0, k1 = 0.7978845608028654, 0.044715
+            t = torch.tanh(k0 * (x + k1 * x ** 3))
+            d = 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * k0 * (1 + 3 * k1 * x * x)
+            ref = ref * d
+            out = C.float()
+        err = ((out - ref).norm() / ref.norm()).item()
+        if epi == 1:
+            err = max(err, e2)
+    # timing
+    if epi == 2:
+        C.copy_(C0)
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(3):
+        call()
+    torch.cuda.synchronize()
+    st.record()
+    for _ in range(iters):
+        call()
+    en.record()
+    torch.cuda.synchronize()
+    ms = st.elapsed_time(en) / iters
+    tf = 2 * M * N * K / ms / 1e9
+    # cuBLAS reference timing on the same logical op
+    for _ in range(3):
+        torch.matmul(Am, Bm.t())
+    torch.cuda.synchronize()
+    st.record()
+    for _ in range(iters):
+        torch.matmul(Am, Bm.t())
+    en.record()
+    torch.cuda.synchronize()
+    ms_ref = st.elapsed_time(en) / iters
+    tf_ref = 2 * M * N * K / ms_ref / 1e9
+    print(f"a_mn={int(a_mn)} b_mn={int(b_mn)} epi={epi} M={M} N={N} K={K}: relerr={err:.2e} "
+          f"ours={ms*1e3:.1f}us {tf:.0f} TF/s  cublas={ms_ref*1e3:.1f}us {tf_ref:.0f} TF/s", flush=True)
+    return err, tf, tf_ref
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true")
+    args = ap.parse_args()
+    bad = 0
+    small = [(256, 256, 128), (128, 64, 64), (384, 640, 192)]
+    for (M, N, K) in small:
+        for (a_mn, b_mn) in [(0, 0), (0, 1), (1, 1), (1, 0)]:
+            for epi in (0, 1, 2, 3):
+                e, _, _ = run_case(M, N, K, a_mn, b_mn, epi, iters=2)
+                bad += not (e < 2e-2)
+    if not args.quick:
+        # GPT 1.4B shapes (mbs 8, seq 2048 -> M = 16384)
+        for (M, N, K, a, b, epi) in [
+            (16384, 6144, 2048, 0, 0, 0), (16384, 2048, 2048, 0, 0, 0), (16384, 8192, 2048, 0, 0, 1),
+            (16384, 2048, 8192, 0, 0, 0), (16384, 51200, 2048, 0, 0, 0),
+            (16384, 2048, 6144, 0, 1, 0), (16384, 2048, 8192, 0, 1, 0), (16384, 8192, 2048, 0, 1, 3),
+            (6144, 2048, 16384, 1, 1, 2), (8192, 2048, 16384, 1, 1, 2), (2048, 8192, 16384, 1, 1, 2),
+            (8192, 8192, 8192, 0, 0, 0),
+        ]:
+            e, _, _ = run_case(M, N, K, a, b, epi, iters=10)
+            bad += not (e < 2e-2)
+    print("FAIL" if bad else "PASS", bad)
+    sys.exit(1 if bad else 0)
+
+
+if __name__ == "__main__":
+    main()
