@@ -40,6 +40,41 @@ const char* tp_last_error(void);
 /* ABI version of this library. */
 int tp_abi_version(void);
 
+/* ------------------------------------------------------------------ plan (structural)
+ * Mirrors of trainplan::ModelSpec (arch.hpp:10-20) and ParallelConfig (memory.hpp:17-32). */
+typedef struct tp_model_spec {
+  int num_layers, hidden_size, num_heads, vocab_size, seq_length;
+} tp_model_spec;
+
+typedef struct tp_parallel_config {
+  int tp, pp, dp, mbs, gbs, zero_stage, interleave_v;
+  int precision;        /* 0 FP16, 1 BF16, 2 FP32 (trainplan::Precision) */
+  int grad_accum_fp32;  /* trainplan::GradAccumDtype::FP32 */
+  int checkpoint_activations, flash_attention;
+} tp_parallel_config;
+
+typedef struct tp_validation {
+  int ok, dp, num_microbatches, num_violations;
+  char fields[16][24];
+  int hard[16];
+  char first_message[256];
+} tp_validation;
+
+/* trainplan::param_count (arch.cpp:48-62): out = {attention, ffn, embedding, total_exact,
+ * total_approx, executed_total}. */
+int tp_param_count(const tp_model_spec* m, uint64_t out[6]);
+/* trainplan::model_flops_per_iteration (arch.cpp:64-92). */
+int tp_model_flops(const tp_model_spec* m, int64_t batch, int ckpt, int factor, double* out);
+/* trainplan::validate (search.cpp:23-84) on a cluster of num_nodes x gpus_per_node; with
+ * kernel_checks != 0 the B200 kernel constraints are appended (validate_kernels). */
+int tp_validate(const tp_model_spec* m, const tp_parallel_config* c, int num_nodes,
+                int gpus_per_node, int kernel_checks, tp_validation* out);
+/* Per-device pipeline order (pipesim.cpp:31-91): kind 0 GPipe, 1 1F1B, 2 interleaved. Writes
+ * up to cap ops as (backward, microbatch, chunk) triples; *n = op count. */
+int tp_pipeline_order(int kind, int p, int m, int v, int device, int* ops, int cap, int* n);
+/* Rank layout (perf.cpp:15-20): rank = t + tp*(p + pp*d). out = {t, p, d}. */
+int tp_rank_coords(int rank, int tp, int pp, int dp, int out[3]);
+
 /* ------------------------------------------------------------------ K1-K4 GEMM
  * C[m,n] = sum_k A(m,k) B(n,k); A(m,k) = A[m*lda+k] (a_mn=0) or A[k*lda+m] (a_mn=1);
  * B(n,k) = B[n*ldb+k] (b_mn=0) or B[k*ldb+n] (b_mn=1). bf16 operands, fp32 accumulation.

@@ -20,7 +20,7 @@ BUILD = PKG / "build"
 LIB = PKG / "lib" / "libtrainplan_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
+COMMON = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
           f"-I{ROOT / 'include'}", f"-I{CSRC}", "-I/usr/local/cuda/include"]
 LINK = ["-shared", "-lcudart", "-lnccl", "-lgomp", "-L/usr/lib/x86_64-linux-gnu",
         "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
