@@ -85,6 +85,79 @@ int tp_gemm_bf16(int M, int N, int K, const void* A, int lda, int a_mn, const vo
                  int b_mn, void* C, int ldc, int epi, const void* bias, void* C2, const void* aux,
                  int ldaux, int accumulate, void* stream);
 
+/* ------------------------------------------------------------------ K5/K6 flash attention
+ * Causal; qkv[b*s, 3*heads*hd] (q | k | v heads, bf16) -> out[b*s, heads*hd], lse[b, heads, s]
+ * (fp32, log2 units). Backward writes dqkv; workspaces D[b*heads*s], dq_acc[b*s*heads*hd] fp32. */
+int tp_flash_attn_fwd(int batch, int seq, int heads, int head_dim, const void* qkv, void* out,
+                      void* lse, void* stream);
+int tp_flash_attn_bwd(int batch, int seq, int heads, int head_dim, const void* qkv,
+                      const void* out, const void* dout, const void* lse, void* D, void* dq_acc,
+                      void* dqkv, void* stream);
+
+/* ------------------------------------------------------------------ K7/K9 LayerNorm + residual
+ * h = resid + dropout(y + bias) (y may be NULL: h = resid); ln_out = LN(h)*gamma + beta (eps 1e-5)
+ * with fp32 mean/rstd. Dropout keyed by (seed, step, layer, site, elem_base + row*d + col). */
+int tp_resid_layernorm_fwd(int rows, int d, const void* y, const void* bias, const void* resid,
+                           void* h_out, const void* gamma, const void* beta, void* ln_out,
+                           void* mean, void* rstd, uint64_t seed, int step, int layer, int site,
+                           float p, int64_t elem_base, void* stream);
+/* dx = resid_grad + LN'(x; dy); dxd = dropout'(dx); dgamma, dbeta, dbias (+= fp32). */
+int tp_layernorm_bwd(int rows, int d, const void* x, const void* dy, const void* resid_grad,
+                     const void* gamma, const void* mean, const void* rstd, void* dx, void* dxd,
+                     void* dgamma, void* dbeta, void* dbias, uint64_t seed, int step, int layer,
+                     int site, float p, int64_t elem_base, void* workspace, void* stream);
+size_t tp_layernorm_bwd_workspace_bytes(int rows, int d);
+
+/* ------------------------------------------------------------------ K10 cross entropy (tp=1)
+ * In place: logits[rows, V] (bf16) -> scale*(softmax - onehot); row_loss[rows] (fp32).
+ * stats workspace: 3*rows floats. */
+int tp_cross_entropy(int rows, int vocab, void* logits, const int32_t* labels, float scale,
+                     void* row_loss, void* stats, void* stream);
+
+/* ------------------------------------------------------------------ K11 Adam (one shard) */
+int tp_adam_step(int64_t n, void* master, void* m, void* v, const void* grad, void* param_bf16,
+                 float lr, float beta1, float beta2, float eps, float weight_decay, int step,
+                 void* stream);
+
+/* ------------------------------------------------------------------ train-step session
+ * One rank of the distributed GPT train step (what trainplan::estimate models, perf.cpp:36-122).
+ * Launch one process per GPU; rank 0 calls tp_nccl_unique_id and shares the 128 bytes with the
+ * other ranks out of band (file, TCP store). world == 1 needs no id (nccl_id may be NULL). */
+typedef struct tp_session tp_session;
+
+typedef struct tp_train_options {
+  uint64_t seed;      /* parameter init + dropout key (counter-based; see oracle/gpt_oracle.h) */
+  float dropout;      /* hidden dropout p */
+  float lr, beta1, beta2, eps, weight_decay; /* Adam with fp32 master weights */
+} tp_train_options;
+
+int tp_nccl_unique_id(unsigned char out[128]);
+/* Validates (trainplan::validate + kernel constraints) and allocates everything; TP_ERR_INVALID
+ * on a bad config, TP_ERR_OOM when it does not fit. */
+int tp_session_create(const tp_model_spec* model, const tp_parallel_config* cfg,
+                      const tp_train_options* opts, int rank, int world, int device,
+                      const unsigned char* nccl_id, tp_session** out);
+int tp_session_destroy(tp_session* s);
+int tp_session_init_params(tp_session* s);
+/* Global batch tokens [gbs][s+1] int32 (host or device pointer). */
+int tp_session_upload_tokens(tp_session* s, const int32_t* tokens, int64_t n, int on_device);
+/* One iteration on the uploaded tokens (asynchronous; loss stays on device). */
+int tp_session_step(tp_session* s);
+/* End-to-end iteration: H2D copy of host tokens, step, D2H read of the mean loss. */
+int tp_session_train_step(tp_session* s, const int32_t* host_tokens, int64_t n, float* loss_out);
+int tp_session_read_loss(tp_session* s, float* loss_out);
+/* Forward-only mean loss of the uploaded batch with the current parameters. */
+int tp_session_eval_loss(tp_session* s, float* loss_out);
+int tp_session_sync(tp_session* s);
+int tp_session_barrier(tp_session* s);
+/* info = {present, rows, cols, offset, rseg, rstride, roff, coff, gcols}: the local shard of
+ * global tensor `tensor_id` (oracle numbering) and its local->global index map. */
+int tp_session_tensor_info(tp_session* s, int tensor_id, int64_t info[9]);
+/* which: 0 bf16 working param, 1 fp32 grad of the last step, 2 fp32 master, 3 Adam m, 4 Adam v. */
+int tp_session_read_tensor(tp_session* s, int which, int tensor_id, float* host_out);
+/* out = {flat_params, shard_params, device_bytes, microbatches, launches_last_step, rank, world, 0} */
+int tp_session_info(tp_session* s, int64_t out[8]);
+
 #ifdef __cplusplus
 }
 #endif

@@ -41,6 +41,18 @@ class Validation(C.Structure):
     def violations(self):
         return [(self.fields[i].value.decode(), self.hard[i]) for i in range(min(self.num_violations, 16))]
 
+class TrainOptions(C.Structure):
+    """tp_train_options."""
+    _fields_ = [("seed", _u64), ("dropout", _f), ("lr", _f), ("beta1", _f), ("beta2", _f), ("eps", _f),
+                ("weight_decay", _f)]
+
+    def __init__(self, seed=1234, dropout=0.0, lr=1e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0):
+        super().__init__(seed, dropout, lr, beta1, beta2, eps, weight_decay)
+
+
+_i64, _sz = C.c_int64, C.c_size_t
+_ptr = C.c_void_p
+
 # name -> (restype, argtypes)
 SIGNATURES: dict[str, tuple] = {
     "tp_last_error": (C.c_char_p, []),
@@ -51,6 +63,29 @@ SIGNATURES: dict[str, tuple] = {
     "tp_pipeline_order": (_i, [_i, _i, _i, _i, _i, C.POINTER(_i), _i, C.POINTER(_i)]),
     "tp_rank_coords": (_i, [_i, _i, _i, _i, C.POINTER(_i)]),
     "tp_gemm_bf16": (_i, [_i, _i, _i, _vp, _i, _i, _vp, _i, _i, _vp, _i, _i, _vp, _vp, _vp, _i, _i, _vp]),
+    "tp_flash_attn_fwd": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
+    "tp_flash_attn_bwd": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "tp_resid_layernorm_fwd": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _u64, _i, _i, _i, _f, _i64, _vp]),
+    "tp_layernorm_bwd": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _u64, _i, _i, _i, _f,
+                              _i64, _vp, _vp]),
+    "tp_layernorm_bwd_workspace_bytes": (_sz, [_i, _i]),
+    "tp_cross_entropy": (_i, [_i, _i, _vp, _vp, _f, _vp, _vp, _vp]),
+    "tp_adam_step": (_i, [_i64, _vp, _vp, _vp, _vp, _vp, _f, _f, _f, _f, _f, _i, _vp]),
+    "tp_nccl_unique_id": (_i, [C.c_char_p]),
+    "tp_session_create": (_i, [C.POINTER(ModelSpec), C.POINTER(ParallelConfig), C.POINTER(TrainOptions), _i, _i, _i,
+                               C.c_char_p, C.POINTER(_vp)]),
+    "tp_session_destroy": (_i, [_vp]),
+    "tp_session_init_params": (_i, [_vp]),
+    "tp_session_upload_tokens": (_i, [_vp, _vp, _i64, _i]),
+    "tp_session_step": (_i, [_vp]),
+    "tp_session_train_step": (_i, [_vp, _vp, _i64, C.POINTER(_f)]),
+    "tp_session_read_loss": (_i, [_vp, C.POINTER(_f)]),
+    "tp_session_eval_loss": (_i, [_vp, C.POINTER(_f)]),
+    "tp_session_sync": (_i, [_vp]),
+    "tp_session_barrier": (_i, [_vp]),
+    "tp_session_tensor_info": (_i, [_vp, _i, C.POINTER(_i64)]),
+    "tp_session_read_tensor": (_i, [_vp, _i, _i, _vp]),
+    "tp_session_info": (_i, [_vp, C.POINTER(_i64)]),
 }
 
 _lib = None
@@ -127,3 +162,109 @@ def rank_coords(rank: int, tp: int, pp: int, dp: int) -> tuple[int, int, int]:
     out = (_i * 3)()
     check(load().tp_rank_coords(rank, tp, pp, dp, out))
     return out[0], out[1], out[2]
+
+
+# ---------------------------------------------------------------- train-step session
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(load().tp_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Session:
+    """One rank of the GPT train step (tp_session_* in capi.h)."""
+
+    READ_PARAM, READ_GRAD, READ_MASTER, READ_ADAM_M, READ_ADAM_V = range(5)
+
+    def __init__(self, spec: ModelSpec, cfg: ParallelConfig, opts: TrainOptions | None = None, rank: int = 0,
+                 world: int = 1, device: int = 0, nccl_id: bytes | None = None):
+        self._lib = load()
+        self.spec, self.cfg = spec, cfg
+        self.opts = opts or TrainOptions()
+        h = _vp()
+        check(self._lib.tp_session_create(C.byref(spec), C.byref(cfg), C.byref(self.opts), rank, world, device,
+                                          nccl_id, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            check(self._lib.tp_session_destroy(self.h))
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def init_params(self):
+        check(self._lib.tp_session_init_params(self.h))
+
+    def upload_tokens(self, tokens, on_device: bool = False):
+        """tokens: numpy int32 [gbs, s+1] (host) or a device address (int) with on_device."""
+        if on_device:
+            ptr, n = tokens
+        else:
+            import numpy as np
+            arr = np.ascontiguousarray(tokens, dtype=np.int32)
+            self._keep = arr
+            ptr, n = arr.ctypes.data, arr.size
+        check(self._lib.tp_session_upload_tokens(self.h, ptr, n, int(on_device)))
+
+    def step(self):
+        check(self._lib.tp_session_step(self.h))
+
+    def train_step(self, tokens) -> float:
+        import numpy as np
+        arr = np.ascontiguousarray(tokens, dtype=np.int32)
+        out = _f()
+        check(self._lib.tp_session_train_step(self.h, arr.ctypes.data, arr.size, C.byref(out)))
+        return out.value
+
+    def read_loss(self) -> float:
+        out = _f()
+        check(self._lib.tp_session_read_loss(self.h, C.byref(out)))
+        return out.value
+
+    def eval_loss(self) -> float:
+        out = _f()
+        check(self._lib.tp_session_eval_loss(self.h, C.byref(out)))
+        return out.value
+
+    def sync(self):
+        check(self._lib.tp_session_sync(self.h))
+
+    def barrier(self):
+        check(self._lib.tp_session_barrier(self.h))
+
+    def tensor_info(self, tid: int) -> dict | None:
+        info = (_i64 * 9)()
+        check(self._lib.tp_session_tensor_info(self.h, tid, info))
+        if not info[0]:
+            return None
+        keys = ["rows", "cols", "offset", "rseg", "rstride", "roff", "coff", "gcols"]
+        return dict(zip(keys, list(info)[1:]))
+
+    def read_tensor(self, which: int, tid: int):
+        import numpy as np
+        info = self.tensor_info(tid)
+        if info is None:
+            return None
+        out = np.empty(info["rows"] * info["cols"], dtype=np.float32)
+        check(self._lib.tp_session_read_tensor(self.h, which, tid, out.ctypes.data))
+        return out.reshape(info["rows"], info["cols"]) if info["cols"] > 1 else out
+
+    def info(self) -> dict:
+        out = (_i64 * 8)()
+        check(self._lib.tp_session_info(self.h, out))
+        keys = ["flat_params", "shard_params", "device_bytes", "microbatches", "launches", "rank", "world"]
+        return dict(zip(keys, list(out)[:7]))
+
+
+def global_index_map(info: dict):
+    """(global_rows, global_cols) index arrays of a local shard (mirrors the init kernel's map)."""
+    import numpy as np
+    r = np.arange(info["rows"])
+    grow = (r // info["rseg"]) * info["rstride"] + info["roff"] + r % info["rseg"]
+    gcol = info["coff"] + np.arange(info["cols"])
+    return grow, gcol

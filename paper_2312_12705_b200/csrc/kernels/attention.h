@@ -1,0 +1,25 @@
+// Causal flash attention (K5 forward, K6 backward). See attention.cu for layouts.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace gptb200 {
+
+struct AttnShape {
+  int batch = 0;     // sequences in the microbatch
+  int seq = 0;       // s (multiple of 128)
+  int heads = 0;     // heads on this TP rank
+  int head_dim = 0;  // 64, 128 or 160
+};
+
+// qkv[M, 3*heads*hd] -> out[M, heads*hd], lse[batch, heads, seq] (log2 units).
+int flash_attn_fwd(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse,
+                   cudaStream_t st);
+
+// Writes dqkv[M, 3*heads*hd]. Workspaces: D[batch*heads*seq] fp32, dq_acc[M*heads*hd] fp32.
+int flash_attn_bwd(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* out,
+                   const __nv_bfloat16* dout, const float* lse, float* D, float* dq_acc,
+                   __nv_bfloat16* dqkv, cudaStream_t st);
+
+}  // namespace gptb200

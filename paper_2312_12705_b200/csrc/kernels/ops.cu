@@ -1,0 +1,624 @@
+// K7-K12: HBM-bound kernels of the GPT block. Every kernel moves 16-byte vectors with
+// coalesced row-contiguous access; row reductions are warp-shuffle + one smem pass; column
+// reductions (LN/bias grads) go through per-block fp32 partials and a second deterministic pass.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "ops.h"
+
+namespace gptb200 {
+
+namespace {
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+struct DropDev {
+  uint64_t key;
+  uint32_t thr;
+  float scale;
+  int64_t base;
+  bool on;
+};
+
+DropDev make_drop(const DropKey& k) {
+  DropDev d{};
+  d.on = k.p > 0.f;
+  if (!d.on) return d;
+  // identical to orc_dropout_keep's key schedule (host-side mix64 restated)
+  auto mix = [](uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+  };
+  d.key = mix(k.seed ^ 0xD6E8FEB86659FD93ULL ^ (static_cast<uint64_t>(static_cast<uint32_t>(k.step)) << 40) ^
+              (static_cast<uint64_t>(static_cast<uint32_t>(k.layer & 0xFFFF)) << 16) ^
+              static_cast<uint64_t>(static_cast<uint32_t>(k.site)));
+  d.thr = static_cast<uint32_t>(static_cast<double>(k.p) * 16777216.0);
+  d.scale = static_cast<float>(1.0 / (1.0 - static_cast<double>(k.p)));
+  d.base = k.elem_base;
+  return d;
+}
+
+__device__ __forceinline__ bool keep(const DropDev& d, int64_t elem) {
+  return static_cast<uint32_t>(mix64(d.key + static_cast<uint64_t>(d.base + elem)) >> 40) >= d.thr;
+}
+
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 v;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return v;
+}
+
+__device__ __forceinline__ float round_bf16(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+
+// Sum of `N` values across the block (blockDim.x multiple of 32, <= 1024).
+template <int N>
+__device__ __forceinline__ void block_sum(float (&v)[N], float* red /* >= 32*N */) {
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    for (int off = 16; off; off >>= 1) v[i] += __shfl_xor_sync(0xffffffff, v[i], off);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < N; ++i) red[i * 32 + warp] = v[i];
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    float t = lane < nw ? red[i * 32 + lane] : 0.f;
+    for (int off = 16; off; off >>= 1) t += __shfl_xor_sync(0xffffffff, t, off);
+    v[i] = t;
+  }
+}
+
+// vectors-per-thread choice: threads = (d/8)/vpt, a multiple of 32 and <= 1024
+int pick_vpt(int d) {
+  const int nvec = d / 8;
+  for (int vpt = 1; vpt <= 8; ++vpt)
+    if (nvec % vpt == 0 && (nvec / vpt) % 32 == 0 && nvec / vpt <= 1024) return vpt;
+  return 0;
+}
+
+// ---------------------------------------------------------------- residual + dropout + LN
+template <int VPT>
+__global__ void resid_ln_kernel(ResidLnArgs a, DropDev dr) {
+  __shared__ float red[64];
+  const int row = blockIdx.x;
+  const int d = a.d;
+  float h[VPT][8];
+  const size_t roff = static_cast<size_t>(row) * d;
+  const bf16* rsrc = a.resid_pos_table ? a.resid + static_cast<size_t>(row % a.seq) * d : a.resid + roff;
+#pragma unroll
+  for (int v = 0; v < VPT; ++v) {
+    const int c0 = (v * blockDim.x + threadIdx.x) * 8;
+    float r[8];
+    unpack8(*reinterpret_cast<const uint4*>(rsrc + c0), r);
+    if (a.y) {
+      float y[8];
+      unpack8(*reinterpret_cast<const uint4*>(a.y + roff + c0), y);
+      if (a.bias) {
+        float b[8];
+        unpack8(*reinterpret_cast<const uint4*>(a.bias + c0), b);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[i] += b[i];
+      }
+      if (dr.on) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[i] = keep(dr, static_cast<int64_t>(roff) + c0 + i) ? y[i] * dr.scale : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) h[v][i] = round_bf16(r[i] + y[i]);
+      if (a.h_out) *reinterpret_cast<uint4*>(a.h_out + roff + c0) = pack8(h[v]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) h[v][i] = r[i];
+    }
+  }
+  if (!a.gamma) return;
+  float s[1] = {0.f};
+#pragma unroll
+  for (int v = 0; v < VPT; ++v)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s[0] += h[v][i];
+  block_sum<1>(s, red);
+  const float mean = s[0] / d;
+  float q[1] = {0.f};
+#pragma unroll
+  for (int v = 0; v < VPT; ++v)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float t = h[v][i] - mean;
+      q[0] += t * t;
+    }
+  block_sum<1>(q, red);
+  const float rstd = rsqrtf(q[0] / d + 1e-5f);
+  if (threadIdx.x == 0) {
+    a.mean[row] = mean;
+    a.rstd[row] = rstd;
+  }
+#pragma unroll
+  for (int v = 0; v < VPT; ++v) {
+    const int c0 = (v * blockDim.x + threadIdx.x) * 8;
+    float g[8], b[8], o[8];
+    unpack8(*reinterpret_cast<const uint4*>(a.gamma + c0), g);
+    unpack8(*reinterpret_cast<const uint4*>(a.beta + c0), b);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = (h[v][i] - mean) * rstd * g[i] + b[i];
+    *reinterpret_cast<uint4*>(a.ln_out + roff + c0) = pack8(o);
+  }
+}
+
+// ---------------------------------------------------------------- LN backward (+residual, dropout')
+constexpr int kLnBwdRows = 64;
+
+template <int VPT>
+__global__ void ln_bwd_kernel(LnBwdArgs a, DropDev dr) {
+  __shared__ float red[64];
+  const int d = a.d;
+  const int r0 = blockIdx.x * kLnBwdRows;
+  const int r1 = min(r0 + kLnBwdRows, a.rows);
+  float pg[VPT][8], pb[VPT][8], pbias[VPT][8], gam[VPT][8];
+#pragma unroll
+  for (int v = 0; v < VPT; ++v)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) pg[v][i] = pb[v][i] = pbias[v][i] = 0.f;
+  if (a.dy) {
+#pragma unroll
+    for (int v = 0; v < VPT; ++v)
+      unpack8(*reinterpret_cast<const uint4*>(a.gamma + (v * blockDim.x + threadIdx.x) * 8), gam[v]);
+  }
+  for (int row = r0; row < r1; ++row) {
+    const size_t roff = static_cast<size_t>(row) * d;
+    float dx[VPT][8];
+    if (a.dy) {
+      const float mu = a.mean[row], rs = a.rstd[row];
+      float xh[VPT][8], gy[VPT][8];
+      float s[2] = {0.f, 0.f};
+#pragma unroll
+      for (int v = 0; v < VPT; ++v) {
+        const int c0 = (v * blockDim.x + threadIdx.x) * 8;
+        float x[8], dy[8];
+        unpack8(*reinterpret_cast<const uint4*>(a.x + roff + c0), x);
+        unpack8(*reinterpret_cast<const uint4*>(a.dy + roff + c0), dy);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          xh[v][i] = (x[i] - mu) * rs;
+          gy[v][i] = dy[i] * gam[v][i];
+          s[0] += gy[v][i];
+          s[1] += gy[v][i] * xh[v][i];
+          pg[v][i] += dy[i] * xh[v][i];
+          pb[v][i] += dy[i];
+        }
+      }
+      block_sum<2>(s, red);
+      const float m1 = s[0] / d, m2 = s[1] / d;
+#pragma unroll
+      for (int v = 0; v < VPT; ++v)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dx[v][i] = rs * (gy[v][i] - m1 - xh[v][i] * m2);
+    } else {
+#pragma unroll
+      for (int v = 0; v < VPT; ++v)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dx[v][i] = 0.f;
+    }
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+      const int c0 = (v * blockDim.x + threadIdx.x) * 8;
+      if (a.resid_grad) {
+        float r[8];
+        unpack8(*reinterpret_cast<const uint4*>(a.resid_grad + roff + c0), r);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dx[v][i] += r[i];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dx[v][i] = round_bf16(dx[v][i]);
+      if (a.dx) *reinterpret_cast<uint4*>(a.dx + roff + c0) = pack8(dx[v]);
+      if (a.dxd || a.dbias) {
+        float o[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          o[i] = dx[v][i];
+          if (dr.on) o[i] = keep(dr, static_cast<int64_t>(roff) + c0 + i) ? o[i] * dr.scale : 0.f;
+          o[i] = round_bf16(o[i]);
+          pbias[v][i] += o[i];
+        }
+        if (a.dxd && (dr.on || a.dxd != a.dx)) *reinterpret_cast<uint4*>(a.dxd + roff + c0) = pack8(o);
+      }
+    }
+  }
+  // per-block column partials: workspace[block][3][d]
+  float* w = a.workspace + static_cast<size_t>(blockIdx.x) * 3 * d;
+#pragma unroll
+  for (int v = 0; v < VPT; ++v) {
+    const int c0 = (v * blockDim.x + threadIdx.x) * 8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      w[c0 + i] = pg[v][i];
+      w[d + c0 + i] = pb[v][i];
+      w[2 * d + c0 + i] = pbias[v][i];
+    }
+  }
+}
+
+__global__ void reduce_partials_kernel(const float* __restrict__ ws, int nblocks, int stride, int n,
+                                       float* out0, float* out1, float* out2) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+  for (int b = 0; b < nblocks; ++b) {
+    const float* w = ws + static_cast<size_t>(b) * stride;
+    s0 += w[c];
+    if (out1) s1 += w[n + c];
+    if (out2) s2 += w[2 * n + c];
+  }
+  if (out0) out0[c] += s0;
+  if (out1) out1[c] += s1;
+  if (out2) out2[c] += s2;
+}
+
+// ---------------------------------------------------------------- column sums
+constexpr int kColsumRows = 128;
+
+__global__ void colsum_kernel(const bf16* __restrict__ X, int rows, int n, float* __restrict__ ws) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (c >= n) return;
+  const int r0 = blockIdx.y * kColsumRows, r1 = min(r0 + kColsumRows, rows);
+  float s0 = 0.f, s1 = 0.f;
+  for (int r = r0; r < r1; ++r) {
+    float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(X + static_cast<size_t>(r) * n + c));
+    s0 += v.x;
+    s1 += v.y;
+  }
+  ws[static_cast<size_t>(blockIdx.y) * n + c] = s0;
+  ws[static_cast<size_t>(blockIdx.y) * n + c + 1] = s1;
+}
+
+// ---------------------------------------------------------------- embedding
+__global__ void embed_lookup_kernel(const int32_t* __restrict__ tok, int rows, const bf16* __restrict__ wte,
+                                    int vstart, int vrows, int d, bf16* __restrict__ out) {
+  const int vpr = d / 8;
+  const size_t n = static_cast<size_t>(rows) * vpr;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / vpr), c = static_cast<int>(i % vpr) * 8;
+    const int t = tok[r] - vstart;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (t >= 0 && t < vrows) v = *reinterpret_cast<const uint4*>(wte + static_cast<size_t>(t) * d + c);
+    *reinterpret_cast<uint4*>(out + static_cast<size_t>(r) * d + c) = v;
+  }
+}
+
+__global__ void embed_bwd_wte_kernel(const int32_t* __restrict__ tok, int rows, const bf16* __restrict__ g,
+                                     int vstart, int vrows, int d, float* __restrict__ dwte) {
+  const int r = blockIdx.x;
+  const int t = tok[r] - vstart;
+  if (t < 0 || t >= vrows) return;
+  for (int c = threadIdx.x * 2; c < d; c += blockDim.x * 2) {
+    float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(g + static_cast<size_t>(r) * d + c));
+    atomicAdd(dwte + static_cast<size_t>(t) * d + c, v.x);
+    atomicAdd(dwte + static_cast<size_t>(t) * d + c + 1, v.y);
+  }
+}
+
+__global__ void embed_bwd_wpe_kernel(const bf16* __restrict__ g, int rows, int d, int seq, float* __restrict__ dwpe) {
+  const size_t n = static_cast<size_t>(seq) * d;
+  const int nseq = rows / seq;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t pos = i / d, c = i % d;
+    float s = 0.f;
+    for (int b = 0; b < nseq; ++b) s += __bfloat162float(g[(static_cast<size_t>(b) * seq + pos) * d + c]);
+    dwpe[i] += s;
+  }
+}
+
+// ---------------------------------------------------------------- cross entropy
+constexpr float kLog2eF = 1.4426950408889634f;
+
+__global__ void xent_stats_kernel(const bf16* __restrict__ logits, int vcols, const int32_t* __restrict__ labels,
+                                  int vstart, float* __restrict__ stats) {
+  __shared__ float redm[32], reds[32];
+  const int row = blockIdx.x;
+  const bf16* x = logits + static_cast<size_t>(row) * vcols;
+  float m = -INFINITY, s = 0.f;
+  for (int c = threadIdx.x * 8; c < vcols; c += blockDim.x * 8) {
+    float f[8];
+    unpack8(*reinterpret_cast<const uint4*>(x + c), f);
+    float lm = f[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) lm = fmaxf(lm, f[i]);
+    const float nm = fmaxf(m, lm);
+    float acc = s * exp2f((m - nm) * kLog2eF);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc += exp2f((f[i] - nm) * kLog2eF);
+    s = acc;
+    m = nm;
+  }
+  for (int off = 16; off; off >>= 1) {
+    const float om = __shfl_xor_sync(0xffffffff, m, off), os = __shfl_xor_sync(0xffffffff, s, off);
+    const float nm = fmaxf(m, om);
+    s = (m == -INFINITY ? 0.f : s * exp2f((m - nm) * kLog2eF)) + (om == -INFINITY ? 0.f : os * exp2f((om - nm) * kLog2eF));
+    m = nm;
+  }
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  if (lane == 0) {
+    redm[warp] = m;
+    reds[warp] = s;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    m = lane < nw ? redm[lane] : -INFINITY;
+    s = lane < nw ? reds[lane] : 0.f;
+    for (int off = 16; off; off >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffff, m, off), os = __shfl_xor_sync(0xffffffff, s, off);
+      const float nm = fmaxf(m, om);
+      s = (m == -INFINITY ? 0.f : s * exp2f((m - nm) * kLog2eF)) + (om == -INFINITY ? 0.f : os * exp2f((om - nm) * kLog2eF));
+      m = nm;
+    }
+    if (lane == 0) {
+      const int t = labels[row] - vstart;
+      stats[static_cast<size_t>(row) * 3 + 0] = m;
+      stats[static_cast<size_t>(row) * 3 + 1] = s;
+      stats[static_cast<size_t>(row) * 3 + 2] = (t >= 0 && t < vcols) ? __bfloat162float(x[t]) : 0.f;
+    }
+  }
+}
+
+__global__ void xent_finish_kernel(bf16* __restrict__ logits, int rows, int vcols, const int32_t* __restrict__ labels,
+                                   int vstart, const float* __restrict__ all_stats, int tp, float scale,
+                                   float* __restrict__ row_loss) {
+  const int row = blockIdx.x;
+  float gm = -INFINITY;
+  for (int i = 0; i < tp; ++i) gm = fmaxf(gm, all_stats[(static_cast<size_t>(i) * rows + row) * 3]);
+  float gs = 0.f, tgt = 0.f;
+  for (int i = 0; i < tp; ++i) {
+    const float* st = all_stats + (static_cast<size_t>(i) * rows + row) * 3;
+    gs += st[1] * exp2f((st[0] - gm) * kLog2eF);
+    tgt += st[2];
+  }
+  if (threadIdx.x == 0 && row_loss) row_loss[row] = logf(gs) + gm - tgt;
+  const float inv = 1.f / gs;
+  const int t = labels[row] - vstart;
+  bf16* x = logits + static_cast<size_t>(row) * vcols;
+  for (int c = threadIdx.x * 8; c < vcols; c += blockDim.x * 8) {
+    float f[8];
+    unpack8(*reinterpret_cast<const uint4*>(x + c), f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float p = exp2f((f[i] - gm) * kLog2eF) * inv;
+      if (c + i == t) p -= 1.f;
+      f[i] = p * scale;
+    }
+    *reinterpret_cast<uint4*>(x + c) = pack8(f);
+  }
+}
+
+// ---------------------------------------------------------------- Adam / init / casts
+__global__ void adam_kernel(AdamArgs a) {
+  const int64_t n4 = a.n / 4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 p = reinterpret_cast<float4*>(a.master)[i];
+    float4 m = reinterpret_cast<float4*>(a.m)[i];
+    float4 v = reinterpret_cast<float4*>(a.v)[i];
+    const float4 g = reinterpret_cast<const float4*>(a.grad)[i];
+    float pp[4] = {p.x, p.y, p.z, p.w}, mm[4] = {m.x, m.y, m.z, m.w}, vv[4] = {v.x, v.y, v.z, v.w};
+    const float gg[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      mm[k] = a.beta1 * mm[k] + (1.f - a.beta1) * gg[k];
+      vv[k] = a.beta2 * vv[k] + (1.f - a.beta2) * gg[k] * gg[k];
+      const float mh = mm[k] / a.bc1, vh = vv[k] / a.bc2;
+      pp[k] -= a.lr * (mh / (sqrtf(vh) + a.eps) + a.weight_decay * pp[k]);
+    }
+    reinterpret_cast<float4*>(a.master)[i] = make_float4(pp[0], pp[1], pp[2], pp[3]);
+    reinterpret_cast<float4*>(a.m)[i] = make_float4(mm[0], mm[1], mm[2], mm[3]);
+    reinterpret_cast<float4*>(a.v)[i] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+    uint2 o;
+    __nv_bfloat162 lo = __floats2bfloat162_rn(pp[0], pp[1]), hi = __floats2bfloat162_rn(pp[2], pp[3]);
+    o.x = *reinterpret_cast<uint32_t*>(&lo);
+    o.y = *reinterpret_cast<uint32_t*>(&hi);
+    reinterpret_cast<uint2*>(a.param)[i] = o;
+  }
+}
+
+__global__ void init_kernel(InitArgs a) {
+  const int64_t n = a.rows * a.cols;
+  const uint64_t key = mix64(a.seed ^ (static_cast<uint64_t>(static_cast<uint32_t>(a.tensor_id)) << 48));
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (a.scale == 0.f) {
+      a.dst[i] = a.constant;
+      continue;
+    }
+    const int64_t r = i / a.cols, c = i % a.cols;
+    const int64_t gr = (r / a.rseg) * a.rstride + a.roff + r % a.rseg;
+    const uint64_t gidx = static_cast<uint64_t>(gr * a.gcols + a.coff + c);
+    int64_t s = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s += static_cast<int64_t>(mix64(key + gidx * 4u + static_cast<uint64_t>(k)) >> 40);
+    const int32_t ci = static_cast<int32_t>(s - (static_cast<int64_t>(2) << 24));
+    a.dst[i] = __fmul_rn(__int2float_rn(ci), a.scale);
+  }
+}
+
+__global__ void cast_f32_bf16_kernel(const float* __restrict__ s, bf16* __restrict__ d, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    d[i] = __float2bfloat16_rn(s[i]);
+}
+
+__global__ void cast_bf16_f32_kernel(const bf16* __restrict__ s, float* __restrict__ d, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    d[i] = __bfloat162float(s[i]);
+}
+
+__global__ void split_tokens_kernel(const int32_t* __restrict__ tok, int n, int s, int32_t* __restrict__ in,
+                                    int32_t* __restrict__ lab) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int b = r / s, i = r % s;
+    in[r] = tok[b * (s + 1) + i];
+    lab[r] = tok[b * (s + 1) + i + 1];
+  }
+}
+
+__global__ void accumulate_sum_kernel(const float* __restrict__ x, int n, float* acc) {
+  __shared__ float red[32];
+  float s = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+  float v[1] = {s};
+  block_sum<1>(v, red);
+  if (threadIdx.x == 0) *acc += v[0];
+}
+
+int grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > 148 * 16) g = 148 * 16;
+  return static_cast<int>(g < 1 ? 1 : g);
+}
+
+int status() { return cudaGetLastError() == cudaSuccess ? 0 : 3; }
+
+}  // namespace
+
+int resid_ln_fwd(const ResidLnArgs& a, cudaStream_t st) {
+  const int vpt = pick_vpt(a.d);
+  if (vpt == 0 || a.rows <= 0) return 1;
+  if (a.gamma && (!a.ln_out || !a.mean || !a.rstd)) return 1;
+  const int threads = a.d / 8 / vpt;
+  const DropDev dr = make_drop(a.drop);
+  switch (vpt) {
+#define CASE(V) case V: resid_ln_kernel<V><<<a.rows, threads, 0, st>>>(a, dr); break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    default: return 1;
+  }
+  return status();
+}
+
+size_t ln_bwd_workspace_floats(int rows, int d) {
+  return static_cast<size_t>((rows + kLnBwdRows - 1) / kLnBwdRows) * 3 * d;
+}
+
+int ln_bwd(const LnBwdArgs& a, cudaStream_t st) {
+  const int vpt = pick_vpt(a.d);
+  if (vpt == 0 || a.rows <= 0 || !a.workspace) return 1;
+  if (a.drop.p > 0.f && a.dxd != nullptr && a.dxd == a.dx) return 1;  // would clobber dx
+  if (a.dy && (!a.gamma || !a.mean || !a.rstd || !a.x)) return 1;
+  const int threads = a.d / 8 / vpt;
+  const int blocks = (a.rows + kLnBwdRows - 1) / kLnBwdRows;
+  const DropDev dr = make_drop(a.drop);
+  switch (vpt) {
+#define CASE(V) case V: ln_bwd_kernel<V><<<blocks, threads, 0, st>>>(a, dr); break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    default: return 1;
+  }
+  const bool any = a.dgamma || a.dbeta || a.dbias;
+  if (any) {
+    // order of outputs in the workspace: dgamma, dbeta, dbias
+    reduce_partials_kernel<<<(a.d + 255) / 256, 256, 0, st>>>(a.workspace, blocks, 3 * a.d, a.d,
+                                                                a.dy ? a.dgamma : nullptr,
+                                                                a.dy ? a.dbeta : nullptr, a.dbias);
+  }
+  return status();
+}
+
+size_t colsum_workspace_floats(int rows, int n) {
+  return static_cast<size_t>((rows + kColsumRows - 1) / kColsumRows) * n;
+}
+
+int colsum_bf16(const bf16* X, int rows, int n, float* out, float* ws, cudaStream_t st) {
+  if (n % 2 != 0 || rows <= 0) return 1;
+  const int splits = (rows + kColsumRows - 1) / kColsumRows;
+  dim3 grid((n / 2 + 255) / 256, splits);
+  colsum_kernel<<<grid, 256, 0, st>>>(X, rows, n, ws);
+  reduce_partials_kernel<<<(n + 255) / 256, 256, 0, st>>>(ws, splits, n, n, out, nullptr, nullptr);
+  return status();
+}
+
+int embed_lookup(const int32_t* tokens, int rows, const bf16* wte, int vstart, int vrows, int d,
+                 bf16* out, cudaStream_t st) {
+  if (d % 8) return 1;
+  embed_lookup_kernel<<<grid_for(static_cast<int64_t>(rows) * d / 8, 256), 256, 0, st>>>(tokens, rows, wte, vstart,
+                                                                                       vrows, d, out);
+  return status();
+}
+
+int embed_bwd(const int32_t* tokens, int rows, const bf16* g, int vstart, int vrows, int d, int seq,
+              float* dwte, float* dwpe, cudaStream_t st) {
+  embed_bwd_wte_kernel<<<rows, 256, 0, st>>>(tokens, rows, g, vstart, vrows, d, dwte);
+  if (dwpe)
+    embed_bwd_wpe_kernel<<<grid_for(static_cast<int64_t>(seq) * d, 256), 256, 0, st>>>(g, rows, d, seq, dwpe);
+  return status();
+}
+
+int xent_stats(const bf16* logits, int rows, int vcols, const int32_t* labels, int vstart, float* stats,
+               cudaStream_t st) {
+  if (vcols % 8) return 1;
+  xent_stats_kernel<<<rows, 512, 0, st>>>(logits, vcols, labels, vstart, stats);
+  return status();
+}
+
+int xent_finish(bf16* logits, int rows, int vcols, const int32_t* labels, int vstart, const float* all_stats,
+                int tp, float scale, float* row_loss, cudaStream_t st) {
+  xent_finish_kernel<<<rows, 512, 0, st>>>(logits, rows, vcols, labels, vstart, all_stats, tp, scale, row_loss);
+  return status();
+}
+
+int adam_step(const AdamArgs& a, cudaStream_t st) {
+  if (a.n % 4) return 1;
+  adam_kernel<<<grid_for(a.n / 4, 256), 256, 0, st>>>(a);
+  return status();
+}
+
+int init_tensor(const InitArgs& a, cudaStream_t st) {
+  init_kernel<<<grid_for(a.rows * a.cols, 256), 256, 0, st>>>(a);
+  return status();
+}
+
+int split_tokens(const int32_t* tok, int nseq, int s, int32_t* inputs, int32_t* labels, cudaStream_t st) {
+  const int n = nseq * s;
+  split_tokens_kernel<<<grid_for(n, 256), 256, 0, st>>>(tok, n, s, inputs, labels);
+  return status();
+}
+
+int accumulate_sum(const float* x, int n, float* acc, cudaStream_t st) {
+  accumulate_sum_kernel<<<1, 1024, 0, st>>>(x, n, acc);
+  return status();
+}
+
+int cast_f32_bf16(const float* s, bf16* d, int64_t n, cudaStream_t st) {
+  cast_f32_bf16_kernel<<<grid_for(n, 256), 256, 0, st>>>(s, d, n);
+  return status();
+}
+
+int cast_bf16_f32(const bf16* s, float* d, int64_t n, cudaStream_t st) {
+  cast_bf16_f32_kernel<<<grid_for(n, 256), 256, 0, st>>>(s, d, n);
+  return status();
+}
+
+}  // namespace gptb200

@@ -1,0 +1,643 @@
+// The per-rank train step. See stage.h; data flow per decoder layer (TP-local sizes,
+// M = mbs*s tokens, dt = d/tp):
+//   fwd: a=LN1(h) -> qkv=a.Wqkv^T+b -> o=flash(qkv) -> y=o.Wo^T -> TP allreduce ->
+//        hmid=h+drop(y+bo), m2=LN2(hmid) -> u=m2.W1^T+b1, g=gelu(u) -> y2=g.W2^T -> TP allreduce
+//        -> hout=hmid+drop(y2+b2), next LN fused into the same kernel.
+//   bwd: the mirror image; every dgrad GEMM of a column-parallel layer is followed by the TP
+//        allreduce of its input gradient (Megatron f/g operators).
+#include "runtime/stage.h"
+
+#include <cmath>
+#include <cstring>
+
+#include "kernels/attention.h"
+#include "kernels/gemm.h"
+#include "trainplan/capi.h"
+
+namespace gptb200 {
+
+using trainplan::PipeOp;
+using trainplan::ScheduleKind;
+
+namespace {
+constexpr int kPerLayer = 16;  // tensor ids per layer (oracle numbering)
+enum LayerTensor { LN1G = 0, LN1B, WQKV, BQKV, WO, BO, LN2G, LN2B, W1, B1, W2, B2 };
+constexpr int kEmbedLayer = 0xFFFF;
+
+int64_t align64(int64_t x) { return (x + 63) / 64 * 64; }
+}  // namespace
+
+void Stage::ck(int status, const char* what) {
+  ++launches_;
+  if (status != 0) {
+    cudaError_t e = cudaGetLastError();
+    throw StepError{e == cudaErrorMemoryAllocation ? TP_ERR_OOM : (status == 1 ? TP_ERR_INVALID : TP_ERR_CUDA),
+                    std::string(what) + " failed (status " + std::to_string(status) + ", " +
+                        cudaGetErrorString(e) + ")"};
+  }
+}
+
+Stage::Stage(const trainplan::ModelSpec& model, const trainplan::ParallelConfig& cfg, const TrainOptions& opts,
+             int rank, int world, int device, const void* nccl_id)
+    : model_(model), cfg_(cfg), opts_(opts), device_(device) {
+  if (cudaSetDevice(device) != cudaSuccess) throw StepError{TP_ERR_CUDA, "cudaSetDevice failed"};
+  if (cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking) != cudaSuccess)
+    throw StepError{TP_ERR_CUDA, "cudaStreamCreate failed"};
+  try {
+    comms_.init(cfg, rank, world, static_cast<const ncclUniqueId*>(nccl_id));
+  } catch (const CommError& e) {
+    throw StepError{e.code, e.msg};
+  }
+  L_ = model.num_layers;
+  d_ = model.hidden_size;
+  V_ = model.vocab_size;
+  s_ = model.seq_length;
+  Ll_ = L_ / cfg.pp;
+  layer0_ = comms_.me.p * Ll_;
+  dt_ = d_ / cfg.tp;
+  ht_ = model.num_heads / cfg.tp;
+  hd_ = d_ / model.num_heads;
+  Vt_ = V_ / cfg.tp;
+  mbs_ = cfg.mbs;
+  M_ = mbs_ * s_;
+  m_ = cfg.num_microbatches();
+  first_ = comms_.me.p == 0;
+  last_ = comms_.me.p == cfg.pp - 1;
+  ckpt_ = cfg.checkpoint_activations;
+  nslots_ = std::min(m_, cfg.pp - comms_.me.p);
+  build_layout();
+  allocate();
+}
+
+Stage::~Stage() {
+  if (st_) cudaStreamSynchronize(st_);
+  for (void* p : allocations_) cudaFree(p);
+  if (st_) cudaStreamDestroy(st_);
+}
+
+void* Stage::alloc(size_t bytes) {
+  void* p = nullptr;
+  bytes = (bytes + 255) / 256 * 256;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw StepError{e == cudaErrorMemoryAllocation ? TP_ERR_OOM : TP_ERR_CUDA,
+                    "cudaMalloc(" + std::to_string(bytes) + ") failed: " + cudaGetErrorString(e)};
+  }
+  allocations_.push_back(p);
+  dev_bytes_ += bytes;
+  return p;
+}
+
+// Flat stage-local parameter layout; every tensor starts on a 64-element boundary (TMA and
+// 16-byte vector alignment). The local->global index map reproduces Megatron's TP split:
+// QKV rows by head within each of q/k/v, fc1 rows, W_o / fc2 columns, vocab rows of wte.
+void Stage::build_layout() {
+  const int t = comms_.me.t;
+  const float std_base = 0.02f;
+  const float std_out = static_cast<float>(0.02 / std::sqrt(2.0 * L_));
+  int64_t off = 0;
+  auto add = [&](int tid, int64_t rows, int64_t cols, int64_t rseg, int64_t rstride, int64_t roff, int64_t coff,
+                 int64_t gcols, float sd, float cst) {
+    ParamSlot s;
+    s.tensor_id = tid;
+    s.rows = rows;
+    s.cols = cols;
+    s.offset = off;
+    s.rseg = rseg;
+    s.rstride = rstride;
+    s.roff = roff;
+    s.coff = coff;
+    s.gcols = gcols;
+    s.stddev = sd;
+    s.constant = cst;
+    slots_.push_back(s);
+    off = align64(off + rows * cols);
+  };
+  const int64_t d = d_, dt = dt_, Vt = Vt_;
+  if (first_ || last_) add(0, Vt, d, Vt, 0, t * Vt, 0, d, std_base, 0.f);
+  if (first_) add(1, s_, d, s_, 0, 0, 0, d, std_base, 0.f);
+  for (int l = 0; l < Ll_; ++l) {
+    const int b = 2 + kPerLayer * (layer0_ + l);
+    add(b + LN1G, d, 1, d, 0, 0, 0, 1, 0.f, 1.f);
+    add(b + LN1B, d, 1, d, 0, 0, 0, 1, 0.f, 0.f);
+    add(b + WQKV, 3 * dt, d, dt, d, t * dt, 0, d, std_base, 0.f);
+    add(b + BQKV, 3 * dt, 1, dt, d, t * dt, 0, 1, 0.f, 0.f);
+    add(b + WO, d, dt, d, 0, 0, t * dt, d, std_out, 0.f);
+    add(b + BO, d, 1, d, 0, 0, 0, 1, 0.f, 0.f);
+    add(b + LN2G, d, 1, d, 0, 0, 0, 1, 0.f, 1.f);
+    add(b + LN2B, d, 1, d, 0, 0, 0, 1, 0.f, 0.f);
+    add(b + W1, 4 * dt, d, 4 * dt, 0, t * 4 * dt, 0, d, std_base, 0.f);
+    add(b + B1, 4 * dt, 1, 4 * dt, 0, t * 4 * dt, 0, 1, 0.f, 0.f);
+    add(b + W2, d, 4 * dt, d, 0, 0, t * 4 * dt, 4 * d, std_out, 0.f);
+    add(b + B2, d, 1, d, 0, 0, 0, 1, 0.f, 0.f);
+  }
+  if (last_) {
+    add(2 + kPerLayer * L_, d, 1, d, 0, 0, 0, 1, 0.f, 1.f);
+    add(2 + kPerLayer * L_ + 1, d, 1, d, 0, 0, 0, 1, 0.f, 0.f);
+  }
+  const int64_t q = static_cast<int64_t>(cfg_.dp) * 64;
+  P_ = (off + q - 1) / q * q;
+  shard_ = P_ / cfg_.dp;
+  slot_index_.assign(2 + kPerLayer * L_ + 2, -1);
+  for (size_t i = 0; i < slots_.size(); ++i) slot_index_[slots_[i].tensor_id] = static_cast<int>(i);
+}
+
+void Stage::allocate() {
+  const size_t M = M_, d = d_, dt = dt_;
+  params_ = static_cast<bf16*>(alloc(P_ * sizeof(bf16)));
+  grads_ = static_cast<float*>(alloc(P_ * sizeof(float)));
+  master_ = static_cast<float*>(alloc(shard_ * sizeof(float)));
+  adam_m_ = static_cast<float*>(alloc(shard_ * sizeof(float)));
+  adam_v_ = static_cast<float*>(alloc(shard_ * sizeof(float)));
+  tokens_ = static_cast<int32_t*>(alloc(static_cast<size_t>(cfg_.gbs) * (s_ + 1) * sizeof(int32_t)));
+  auto layer_acts = [&](LayerActs& A) {
+    A.a = static_cast<bf16*>(alloc(M * d * 2));
+    A.qkv = static_cast<bf16*>(alloc(M * 3 * dt * 2));
+    A.o = static_cast<bf16*>(alloc(M * dt * 2));
+    A.hmid = static_cast<bf16*>(alloc(M * d * 2));
+    A.m2 = static_cast<bf16*>(alloc(M * d * 2));
+    A.u = static_cast<bf16*>(alloc(M * 4 * dt * 2));
+    A.g = static_cast<bf16*>(alloc(M * 4 * dt * 2));
+    A.mu1 = static_cast<float*>(alloc(M * 4));
+    A.rs1 = static_cast<float*>(alloc(M * 4));
+    A.mu2 = static_cast<float*>(alloc(M * 4));
+    A.rs2 = static_cast<float*>(alloc(M * 4));
+    A.lse = static_cast<float*>(alloc(static_cast<size_t>(mbs_) * ht_ * s_ * 4));
+  };
+  slots_act_.resize(nslots_);
+  for (auto& S : slots_act_) {
+    S.h.resize(Ll_ + 1);
+    for (auto& h : S.h) h = static_cast<bf16*>(alloc(M * d * 2));
+    if (!ckpt_) {
+      S.acts.resize(Ll_);
+      for (auto& A : S.acts) layer_acts(A);
+    }
+    S.inputs = static_cast<int32_t*>(alloc(M * 4));
+    S.labels = static_cast<int32_t*>(alloc(M * 4));
+  }
+  if (ckpt_) layer_acts(scratch_);
+  tmp_md_ = static_cast<bf16*>(alloc(M * d * 2));
+  dh_[0] = static_cast<bf16*>(alloc(M * d * 2));
+  dh_[1] = static_cast<bf16*>(alloc(M * d * 2));
+  dy_ = static_cast<bf16*>(alloc(M * d * 2));
+  du_ = static_cast<bf16*>(alloc(M * 4 * dt * 2));
+  dm_ = static_cast<bf16*>(alloc(M * d * 2));
+  do_ = static_cast<bf16*>(alloc(M * dt * 2));
+  dqkv_ = static_cast<bf16*>(alloc(M * 3 * dt * 2));
+  attn_D_ = static_cast<float*>(alloc(static_cast<size_t>(mbs_) * ht_ * s_ * 4));
+  dq_acc_ = static_cast<float*>(alloc(M * dt * 4));
+  size_t ws = std::max({colsum_workspace_floats(M_, 4 * dt_), colsum_workspace_floats(M_, 3 * dt_),
+                        ln_bwd_workspace_floats(M_, d_)});
+  ws_ = static_cast<float*>(alloc(ws * 4));
+  if (last_) {
+    hf_ = static_cast<bf16*>(alloc(M * d * 2));
+    muf_ = static_cast<float*>(alloc(M * 4));
+    rsf_ = static_cast<float*>(alloc(M * 4));
+    logits_ = static_cast<bf16*>(alloc(M * static_cast<size_t>(Vt_) * 2));
+    xstats_ = static_cast<float*>(alloc(M * 3 * 4));
+    xall_ = static_cast<float*>(alloc(M * 3 * 4 * cfg_.tp));
+    row_loss_ = static_cast<float*>(alloc(M * 4));
+  }
+  loss_acc_ = static_cast<float*>(alloc(4));
+}
+
+const ParamSlot* Stage::slot(int tid) const {
+  if (tid < 0 || tid >= static_cast<int>(slot_index_.size()) || slot_index_[tid] < 0) return nullptr;
+  return &slots_[slot_index_[tid]];
+}
+
+Stage::LayerW Stage::w(int l) const {
+  const int b = 2 + kPerLayer * (layer0_ + l);
+  auto p = [&](int j) { return params_ + slot(b + j)->offset; };
+  return {p(LN1G), p(LN1B), p(WQKV), p(BQKV), p(WO), p(BO), p(LN2G), p(LN2B), p(W1), p(B1), p(W2), p(B2)};
+}
+
+Stage::LayerG Stage::gr(int l) const {
+  const int b = 2 + kPerLayer * (layer0_ + l);
+  auto p = [&](int j) { return grads_ + slot(b + j)->offset; };
+  return {p(LN1G), p(LN1B), p(WQKV), p(BQKV), p(WO), p(BO), p(LN2G), p(LN2B), p(W1), p(B1), p(W2), p(B2)};
+}
+
+LayerActs& Stage::acts_for(int slot, int l) { return ckpt_ ? scratch_ : slots_act_[slot].acts[l]; }
+
+void Stage::init_params() {
+  cudaMemsetAsync(grads_, 0, P_ * sizeof(float), st_);
+  for (const auto& s : slots_) {
+    InitArgs a;
+    a.dst = grads_ + s.offset;
+    a.rows = s.rows;
+    a.cols = s.cols;
+    a.rseg = s.rseg;
+    a.rstride = s.rstride;
+    a.roff = s.roff;
+    a.coff = s.coff;
+    a.gcols = s.gcols;
+    a.seed = opts_.seed;
+    a.tensor_id = s.tensor_id;
+    // same expression as orc_init_value's scale (bit-identical values)
+    a.scale = s.stddev > 0.f ? static_cast<float>(static_cast<double>(s.stddev) * std::sqrt(3.0) / 16777216.0) : 0.f;
+    a.constant = s.constant;
+    ck(init_tensor(a, st_), "init_tensor");
+  }
+  ck(cast_f32_bf16(grads_, params_, P_, st_), "cast params");
+  cudaMemcpyAsync(master_, grads_ + comms_.me.d * shard_, shard_ * sizeof(float), cudaMemcpyDeviceToDevice, st_);
+  cudaMemsetAsync(adam_m_, 0, shard_ * sizeof(float), st_);
+  cudaMemsetAsync(adam_v_, 0, shard_ * sizeof(float), st_);
+  cudaMemsetAsync(grads_, 0, P_ * sizeof(float), st_);
+  step_no_ = 0;
+  sync();
+}
+
+void Stage::upload_tokens(const int32_t* src, int64_t n, bool on_device) {
+  const int64_t need = static_cast<int64_t>(cfg_.gbs) * (s_ + 1);
+  if (n != need) throw StepError{TP_ERR_INVALID, "token count " + std::to_string(n) + " != gbs*(s+1) = " + std::to_string(need)};
+  cudaError_t e = cudaMemcpyAsync(tokens_, src, n * sizeof(int32_t),
+                                  on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st_);
+  if (e != cudaSuccess) throw StepError{TP_ERR_CUDA, std::string("token upload: ") + cudaGetErrorString(e)};
+}
+
+// ------------------------------------------------------------------------------ GEMM helpers
+void Stage::gemm_fwd(const bf16* X, const bf16* W, const bf16* bias, bf16* Y, int M, int N, int K, int epi, bf16* C2) {
+  GemmParams p;
+  p.M = M, p.N = N, p.K = K;
+  p.A = X, p.lda = K, p.a_mn = false;
+  p.B = W, p.ldb = K, p.b_mn = false;
+  p.C = Y, p.ldc = N, p.epi = epi, p.bias = bias, p.C2 = C2;
+  ck(gemm_bf16(p, st_), "gemm fwd");
+}
+
+// dX[M,K] = dY[M,N] . W[N,K]
+void Stage::gemm_dgrad(const bf16* dY, const bf16* W, bf16* dX, int M, int N, int K, int epi, const bf16* aux) {
+  GemmParams p;
+  p.M = M, p.N = K, p.K = N;
+  p.A = dY, p.lda = N, p.a_mn = false;
+  p.B = W, p.ldb = K, p.b_mn = true;
+  p.C = dX, p.ldc = K, p.epi = epi, p.aux = aux, p.ldaux = K;
+  ck(gemm_bf16(p, st_), "gemm dgrad");
+}
+
+// dW[N,K] += dY[M,N]^T . X[M,K]   (fp32 main grad)
+void Stage::gemm_wgrad(const bf16* dY, const bf16* X, float* dW, int M, int N, int K) {
+  GemmParams p;
+  p.M = N, p.N = K, p.K = M;
+  p.A = dY, p.lda = N, p.a_mn = true;
+  p.B = X, p.ldb = K, p.b_mn = true;
+  p.C = dW, p.ldc = K, p.epi = EPI_F32, p.accumulate = 1;
+  ck(gemm_bf16(p, st_), "gemm wgrad");
+}
+
+// ------------------------------------------------------------------------------ forward
+void Stage::prepare_tokens(int mb, int slot) {
+  const int64_t sample0 = static_cast<int64_t>(comms_.me.d) * (cfg_.gbs / cfg_.dp) + static_cast<int64_t>(mb) * mbs_;
+  ck(split_tokens(tokens_ + sample0 * (s_ + 1), mbs_, s_, slots_act_[slot].inputs, slots_act_[slot].labels, st_),
+     "split_tokens");
+}
+
+static DropKey drop_key(const TrainOptions& o, int step, int layer, int site, int64_t sample0, int s, int d) {
+  DropKey k;
+  k.seed = o.seed;
+  k.step = step;
+  k.layer = layer;
+  k.site = site;
+  k.p = o.dropout;
+  k.elem_base = sample0 * s * static_cast<int64_t>(d);
+  return k;
+}
+
+void Stage::layer_fwd(int l, LayerActs& A, const bf16* hin, bf16* hout, bool fuse_next, int slot) {
+  const int lg = layer0_ + l;
+  const LayerW W = w(l);
+  const int64_t sample0 = static_cast<int64_t>(comms_.me.d) * (cfg_.gbs / cfg_.dp) +
+                          static_cast<int64_t>(cur_mb_) * mbs_;
+  gemm_fwd(A.a, W.wqkv, W.bqkv, A.qkv, M_, 3 * dt_, d_);
+  ck(flash_attn_fwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, A.lse, st_), "flash fwd");
+  gemm_fwd(A.o, W.wo, nullptr, tmp_md_, M_, d_, dt_);
+  tp_allreduce(tmp_md_);
+  ResidLnArgs r;
+  r.rows = M_, r.d = d_, r.seq = s_;
+  r.y = tmp_md_, r.bias = W.bo, r.resid = hin;
+  r.drop = drop_key(opts_, step_no_, lg, 0, sample0, s_, d_);
+  r.h_out = A.hmid, r.gamma = W.ln2g, r.beta = W.ln2b, r.ln_out = A.m2, r.mean = A.mu2, r.rstd = A.rs2;
+  ck(resid_ln_fwd(r, st_), "resid+ln2");
+  gemm_fwd(A.m2, W.w1, W.b1, A.u, M_, 4 * dt_, d_, EPI_BIAS_GELU, A.g);
+  gemm_fwd(A.g, W.w2, nullptr, tmp_md_, M_, d_, 4 * dt_);
+  tp_allreduce(tmp_md_);
+  ResidLnArgs r2;
+  r2.rows = M_, r2.d = d_, r2.seq = s_;
+  r2.y = tmp_md_, r2.bias = W.b2, r2.resid = A.hmid;
+  r2.drop = drop_key(opts_, step_no_, lg, 1, sample0, s_, d_);
+  r2.h_out = hout;
+  if (fuse_next) {
+    if (l + 1 < Ll_) {
+      LayerActs& N = acts_for(slot, l + 1);
+      const LayerW Wn = w(l + 1);
+      r2.gamma = Wn.ln1g, r2.beta = Wn.ln1b, r2.ln_out = N.a, r2.mean = N.mu1, r2.rstd = N.rs1;
+    } else {
+      r2.gamma = params_ + slot_offset(2 + kPerLayer * L_);
+      r2.beta = params_ + slot_offset(2 + kPerLayer * L_ + 1);
+      r2.ln_out = hf_, r2.mean = muf_, r2.rstd = rsf_;
+    }
+  }
+  ck(resid_ln_fwd(r2, st_), "resid+ln1");
+}
+
+void Stage::layer_recompute(int l, LayerActs& A, const bf16* hin) {
+  const int lg = layer0_ + l;
+  const LayerW W = w(l);
+  const int64_t sample0 = static_cast<int64_t>(comms_.me.d) * (cfg_.gbs / cfg_.dp) +
+                          static_cast<int64_t>(cur_mb_) * mbs_;
+  ResidLnArgs r0;
+  r0.rows = M_, r0.d = d_, r0.seq = s_;
+  r0.resid = hin, r0.gamma = W.ln1g, r0.beta = W.ln1b, r0.ln_out = A.a, r0.mean = A.mu1, r0.rstd = A.rs1;
+  ck(resid_ln_fwd(r0, st_), "recompute ln1");
+  gemm_fwd(A.a, W.wqkv, W.bqkv, A.qkv, M_, 3 * dt_, d_);
+  ck(flash_attn_fwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, A.lse, st_), "flash fwd");
+  gemm_fwd(A.o, W.wo, nullptr, tmp_md_, M_, d_, dt_);
+  tp_allreduce(tmp_md_);
+  ResidLnArgs r;
+  r.rows = M_, r.d = d_, r.seq = s_;
+  r.y = tmp_md_, r.bias = W.bo, r.resid = hin;
+  r.drop = drop_key(opts_, step_no_, lg, 0, sample0, s_, d_);
+  r.h_out = A.hmid, r.gamma = W.ln2g, r.beta = W.ln2b, r.ln_out = A.m2, r.mean = A.mu2, r.rstd = A.rs2;
+  ck(resid_ln_fwd(r, st_), "recompute ln2");
+  gemm_fwd(A.m2, W.w1, W.b1, A.u, M_, 4 * dt_, d_, EPI_BIAS_GELU, A.g);
+}
+
+void Stage::tp_allreduce(bf16* buf) {
+  if (cfg_.tp == 1) return;
+  ++launches_;
+  try {
+    comms_.tp_allreduce_bf16(buf, static_cast<size_t>(M_) * d_, st_);
+  } catch (const CommError& e) {
+    throw StepError{e.code, e.msg};
+  }
+}
+
+void Stage::forward_op(int mb, bool with_loss) {
+  cur_mb_ = mb;
+  const int slot = mb % nslots_;
+  Slot& S = slots_act_[slot];
+  if (first_ || last_) prepare_tokens(mb, slot);
+  LayerActs& A0 = acts_for(slot, 0);
+  const LayerW W0 = w(0);
+  ResidLnArgs r;
+  r.rows = M_, r.d = d_, r.seq = s_;
+  r.gamma = W0.ln1g, r.beta = W0.ln1b, r.ln_out = A0.a, r.mean = A0.mu1, r.rstd = A0.rs1;
+  if (first_) {
+    ck(embed_lookup(S.inputs, M_, params_ + slot_offset(0), comms_.me.t * Vt_, Vt_, d_, tmp_md_, st_), "embed");
+    tp_allreduce(tmp_md_);
+    const int64_t sample0 = static_cast<int64_t>(comms_.me.d) * (cfg_.gbs / cfg_.dp) + static_cast<int64_t>(mb) * mbs_;
+    r.y = tmp_md_, r.resid = params_ + slot_offset(1), r.resid_pos_table = true;
+    r.drop = drop_key(opts_, step_no_, kEmbedLayer, 2, sample0, s_, d_);
+    r.h_out = S.h[0];
+  } else {
+    r.resid = S.h[0];
+  }
+  ck(resid_ln_fwd(r, st_), "embed+ln1");
+  for (int l = 0; l < Ll_; ++l) layer_fwd(l, acts_for(slot, l), S.h[l], S.h[l + 1], (l + 1 < Ll_) || last_, slot);
+  if (last_) head_and_loss(slot, with_loss);
+}
+
+void Stage::head_and_loss(int slot, bool /*with_grad*/) {
+  Slot& S = slots_act_[slot];
+  gemm_fwd(hf_, params_ + slot_offset(0), nullptr, logits_, M_, Vt_, d_);
+  ck(xent_stats(logits_, M_, Vt_, S.labels, comms_.me.t * Vt_, xstats_, st_), "xent stats");
+  try {
+    comms_.tp_allgather_f32(xstats_, xall_, static_cast<size_t>(M_) * 3, st_);
+  } catch (const CommError& e) {
+    throw StepError{e.code, e.msg};
+  }
+  const float scale = static_cast<float>(1.0 / (static_cast<double>(cfg_.gbs) * s_));
+  ck(xent_finish(logits_, M_, Vt_, S.labels, comms_.me.t * Vt_, xall_, cfg_.tp, scale, row_loss_, st_), "xent finish");
+  if (comms_.me.t == 0) ck(accumulate_sum(row_loss_, M_, loss_acc_, st_), "loss sum");
+}
+
+// ------------------------------------------------------------------------------ backward
+void Stage::head_bwd(bf16* dh) {
+  // logits_ holds scale*(softmax - onehot). Vocab-parallel: partial dX summed over TP.
+  gemm_dgrad(logits_, params_ + slot_offset(0), tmp_md_, M_, Vt_, d_);
+  tp_allreduce(tmp_md_);
+  gemm_wgrad(logits_, hf_, grads_ + slot_offset(0), M_, Vt_, d_);
+}
+
+void Stage::layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2) {
+  const int lg = layer0_ + l;
+  const LayerW W = w(l);
+  const LayerG G = gr(l);
+  const bool drop_on = opts_.dropout > 0.f;
+  const int64_t sample0 = static_cast<int64_t>(comms_.me.d) * (cfg_.gbs / cfg_.dp) +
+                          static_cast<int64_t>(cur_mb_) * mbs_;
+  // MLP branch
+  gemm_dgrad(dy2, W.w2, du_, M_, d_, 4 * dt_, EPI_DGELU, A.u);
+  gemm_wgrad(dy2, A.g, G.w2, M_, d_, 4 * dt_);
+  ck(colsum_bf16(du_, M_, 4 * dt_, G.b1, ws_, st_), "db1");
+  gemm_dgrad(du_, W.w1, dm_, M_, 4 * dt_, d_);
+  tp_allreduce(dm_);
+  gemm_wgrad(du_, A.m2, G.w1, M_, 4 * dt_, d_);
+  LnBwdArgs b;
+  b.rows = M_, b.d = d_;
+  b.x = A.hmid, b.dy = dm_, b.resid_grad = dh, b.gamma = W.ln2g, b.mean = A.mu2, b.rstd = A.rs2;
+  b.dx = dh;
+  b.drop = drop_key(opts_, step_no_, lg, 0, sample0, s_, d_);
+  b.dxd = drop_on ? dy_ : dh;
+  b.dgamma = G.ln2g, b.dbeta = G.ln2b, b.dbias = G.bo, b.workspace = ws_;
+  ck(ln_bwd(b, st_), "ln2 bwd");
+  const bf16* dya = drop_on ? dy_ : dh;
+  // attention branch
+  gemm_dgrad(dya, W.wo, do_, M_, d_, dt_);
+  gemm_wgrad(dya, A.o, G.wo, M_, d_, dt_);
+  ck(flash_attn_bwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, do_, A.lse, attn_D_, dq_acc_, dqkv_, st_), "flash bwd");
+  ck(colsum_bf16(dqkv_, M_, 3 * dt_, G.bqkv, ws_, st_), "dbqkv");
+  gemm_dgrad(dqkv_, W.wqkv, dm_, M_, 3 * dt_, d_);
+  tp_allreduce(dm_);
+  gemm_wgrad(dqkv_, A.a, G.wqkv, M_, 3 * dt_, d_);
+  LnBwdArgs c;
+  c.rows = M_, c.d = d_;
+  c.x = hin, c.dy = dm_, c.resid_grad = dh, c.gamma = W.ln1g, c.mean = A.mu1, c.rstd = A.rs1;
+  c.dx = dh;
+  c.dgamma = G.ln1g, c.dbeta = G.ln1b, c.workspace = ws_;
+  if (l > 0) {  // preceding branch: MLP of layer l-1 on this stage
+    c.drop = drop_key(opts_, step_no_, lg - 1, 1, sample0, s_, d_);
+    c.dxd = drop_on ? dy_ : dh;
+    c.dbias = gr(l - 1).b2;
+  } else if (first_) {  // preceding branch: embedding dropout
+    c.drop = drop_key(opts_, step_no_, kEmbedLayer, 2, sample0, s_, d_);
+    c.dxd = drop_on ? dy_ : dh;
+  }
+  ck(ln_bwd(c, st_), "ln1 bwd");
+}
+
+void Stage::backward_op(int mb, bf16* dh) {
+  cur_mb_ = mb;
+  const int slot = mb % nslots_;
+  Slot& S = slots_act_[slot];
+  const bool drop_on = opts_.dropout > 0.f;
+  const int64_t sample0 = static_cast<int64_t>(comms_.me.d) * (cfg_.gbs / cfg_.dp) + static_cast<int64_t>(mb) * mbs_;
+  LnBwdArgs b;
+  b.rows = M_, b.d = d_, b.workspace = ws_;
+  b.drop = drop_key(opts_, step_no_, layer0_ + Ll_ - 1, 1, sample0, s_, d_);
+  b.dxd = drop_on ? dy_ : dh;
+  b.dbias = gr(Ll_ - 1).b2;
+  if (last_) {
+    if (ckpt_) {
+      // hf_ / logits_ are still those of this microbatch (1F1B: F(k) is followed by B(k))
+    }
+    head_bwd(dh);
+    const int f = 2 + kPerLayer * L_;
+    b.x = S.h[Ll_], b.dy = tmp_md_, b.gamma = params_ + slot_offset(f), b.mean = muf_, b.rstd = rsf_;
+    b.dx = dh, b.dgamma = grads_ + slot_offset(f), b.dbeta = grads_ + slot_offset(f + 1);
+  } else {
+    b.resid_grad = dh;  // received gradient of the stage output
+    b.dx = nullptr;
+    if (!drop_on) b.dxd = nullptr;
+  }
+  ck(ln_bwd(b, st_), "final ln / stage-boundary bwd");
+  for (int l = Ll_ - 1; l >= 0; --l) {
+    LayerActs& A = acts_for(slot, l);
+    if (ckpt_) layer_recompute(l, A, S.h[l]);
+    layer_bwd(l, A, S.h[l], dh, drop_on ? dy_ : dh);
+  }
+  if (first_) {
+    const bf16* g = drop_on ? dy_ : dh;
+    ck(embed_bwd(S.inputs, M_, g, comms_.me.t * Vt_, Vt_, d_, s_, grads_ + slot_offset(0), grads_ + slot_offset(1), st_),
+       "embed bwd");
+  }
+}
+
+// ------------------------------------------------------------------------------ step
+void Stage::optimizer_step() {
+  AdamArgs a;
+  a.n = shard_;
+  a.master = master_;
+  a.m = adam_m_;
+  a.v = adam_v_;
+  a.grad = grads_ + comms_.me.d * shard_;
+  a.param = params_ + comms_.me.d * shard_;
+  a.lr = opts_.lr, a.beta1 = opts_.beta1, a.beta2 = opts_.beta2, a.eps = opts_.eps, a.weight_decay = opts_.weight_decay;
+  a.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(opts_.beta1), step_no_));
+  a.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(opts_.beta2), step_no_));
+  ck(adam_step(a, st_), "adam");
+}
+
+void Stage::step() {
+  ++step_no_;
+  launches_ = 0;
+  cudaMemsetAsync(grads_, 0, P_ * sizeof(float), st_);
+  cudaMemsetAsync(loss_acc_, 0, sizeof(float), st_);
+  const auto ops = trainplan::pipeline_order(ScheduleKind::OneF1B, cfg_.pp, m_, 1, comms_.me.p);
+  const size_t n_act = static_cast<size_t>(M_) * d_;
+  const void* pending = nullptr;
+  int pending_peer = -1, dh_idx = 0;
+  try {
+    for (const PipeOp& op : ops) {
+      void* recv = nullptr;
+      int recv_peer = -1;
+      if (!op.backward && !first_) {
+        recv = slots_act_[op.microbatch % nslots_].h[0];
+        recv_peer = comms_.me.p - 1;
+      } else if (op.backward && !last_) {
+        recv = dh_[dh_idx];
+        recv_peer = comms_.me.p + 1;
+      }
+      if (pending || recv) ++launches_;
+      comms_.pp_exchange(pending, pending_peer, recv, recv_peer, n_act, st_);
+      pending = nullptr;
+      if (!op.backward) {
+        forward_op(op.microbatch, true);
+        if (!last_) {
+          pending = slots_act_[op.microbatch % nslots_].h[Ll_];
+          pending_peer = comms_.me.p + 1;
+        }
+      } else {
+        backward_op(op.microbatch, dh_[dh_idx]);
+        if (!first_) {
+          pending = dh_[dh_idx];
+          pending_peer = comms_.me.p - 1;
+        }
+        dh_idx ^= 1;
+      }
+    }
+    if (pending) {
+      ++launches_;
+      comms_.pp_exchange(pending, pending_peer, nullptr, -1, n_act, st_);
+    }
+    if (cfg_.pp > 1 && (first_ || last_)) comms_.emb_allreduce_f32(grads_ + slot_offset(0), static_cast<size_t>(Vt_) * d_, st_);
+    comms_.dp_reduce_scatter_f32(grads_, shard_, st_);
+    optimizer_step();
+    comms_.dp_allgather_bf16(params_, shard_, st_);
+    comms_.world_allreduce_f32(loss_acc_, 1, st_);
+  } catch (const CommError& e) {
+    throw StepError{e.code, e.msg};
+  }
+}
+
+float Stage::read_loss() {
+  float v = 0.f;
+  cudaMemcpyAsync(&v, loss_acc_, sizeof(float), cudaMemcpyDeviceToHost, st_);
+  cudaStreamSynchronize(st_);
+  return static_cast<float>(v / (static_cast<double>(cfg_.gbs) * s_));
+}
+
+float Stage::eval_loss() {
+  cudaMemsetAsync(loss_acc_, 0, sizeof(float), st_);
+  const size_t n_act = static_cast<size_t>(M_) * d_;
+  try {
+    for (int mb = 0; mb < m_; ++mb) {
+      if (!first_) comms_.pp_exchange(nullptr, -1, slots_act_[mb % nslots_].h[0], comms_.me.p - 1, n_act, st_);
+      forward_op(mb, true);
+      if (!last_) comms_.pp_exchange(slots_act_[mb % nslots_].h[Ll_], comms_.me.p + 1, nullptr, -1, n_act, st_);
+    }
+    comms_.world_allreduce_f32(loss_acc_, 1, st_);
+  } catch (const CommError& e) {
+    throw StepError{e.code, e.msg};
+  }
+  return read_loss();
+}
+
+void Stage::sync() {
+  cudaError_t e = cudaStreamSynchronize(st_);
+  if (e != cudaSuccess) throw StepError{TP_ERR_CUDA, std::string("stream sync: ") + cudaGetErrorString(e)};
+}
+
+void Stage::barrier() {
+  if (comms_.world > 1) {
+    float* one = loss_acc_;  // any device float works; value is irrelevant after the step read
+    (void)one;
+    float* tmp = static_cast<float*>(ws_);
+    try {
+      comms_.world_allreduce_f32(tmp, 1, st_);
+    } catch (const CommError& e) {
+      throw StepError{e.code, e.msg};
+    }
+  }
+  sync();
+}
+
+void Stage::read_tensor(int which, int tid, float* host) const {
+  const ParamSlot* s = slot(tid);
+  if (!s) throw StepError{TP_ERR_INVALID, "tensor " + std::to_string(tid) + " not on this rank"};
+  const int64_t n = s->rows * s->cols;
+  cudaStreamSynchronize(st_);
+  if (which == 0) {
+    std::vector<uint16_t> tmp(n);
+    cudaMemcpy(tmp.data(), params_ + s->offset, n * 2, cudaMemcpyDeviceToHost);
+    for (int64_t i = 0; i < n; ++i) {
+      uint32_t u = static_cast<uint32_t>(tmp[i]) << 16;
+      std::memcpy(&host[i], &u, 4);
+    }
+    return;
+  }
+  const float* base = nullptr;
+  int64_t off = s->offset;
+  if (which == 1) {
+    base = grads_;
+  } else {
+    off -= comms_.me.d * shard_;
+    if (off < 0 || off + n > shard_) throw StepError{TP_ERR_INVALID, "tensor outside this rank's ZeRO shard"};
+    base = which == 2 ? master_ : (which == 3 ? adam_m_ : adam_v_);
+  }
+  cudaMemcpy(host, base + off, n * 4, cudaMemcpyDeviceToHost);
+}
+
+}  // namespace gptb200

@@ -1,0 +1,161 @@
+// One rank's share of the GPT train step: its pipeline stage's layers, TP-sharded, with the
+// ZeRO-1 optimizer shard of its DP group. Executes what trainplan::estimate() models
+// (/root/reference/proj/src/perf.cpp:36-122) on sm_100a kernels + NCCL.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels/ops.h"
+#include "runtime/comm.h"
+#include "trainplan/core.hpp"
+
+namespace gptb200 {
+
+struct TrainOptions {
+  uint64_t seed = 1234;  // init + dropout key
+  float dropout = 0.f;   // hidden dropout (embedding, attention-out, mlp-out)
+  float lr = 1e-4f, beta1 = 0.9f, beta2 = 0.95f, eps = 1e-8f, weight_decay = 0.f;
+};
+
+struct StepError {
+  int code;
+  std::string msg;
+};
+
+// Local shard of one global parameter tensor inside the stage's flat buffers.
+struct ParamSlot {
+  int tensor_id = 0;
+  int64_t rows = 0, cols = 0, offset = 0;
+  int64_t rseg = 1, rstride = 0, roff = 0, coff = 0, gcols = 1;  // local -> global index map
+  float stddev = 0.f, constant = 0.f;
+};
+
+// Per-layer tensors kept for backward (or recomputed under activation checkpointing).
+struct LayerActs {
+  bf16 *a = nullptr, *qkv = nullptr, *o = nullptr, *hmid = nullptr, *m2 = nullptr, *u = nullptr,
+       *g = nullptr;
+  float *mu1 = nullptr, *rs1 = nullptr, *mu2 = nullptr, *rs2 = nullptr, *lse = nullptr;
+};
+
+struct StepTimes {  // milliseconds of the last step on this rank (CUDA events)
+  float total = 0, tp_comm = 0, pp_comm = 0, dp_comm = 0, optimizer = 0;
+};
+
+class Stage {
+ public:
+  Stage(const trainplan::ModelSpec& model, const trainplan::ParallelConfig& resolved,
+        const TrainOptions& opts, int rank, int world, int device, const void* nccl_id);
+  ~Stage();
+  Stage(const Stage&) = delete;
+  Stage& operator=(const Stage&) = delete;
+
+  void init_params();
+  // Global batch tokens [gbs, s+1] (inputs = [:, :s], labels = [:, 1:]); host or device src.
+  void upload_tokens(const int32_t* src, int64_t n, bool src_on_device);
+  // One iteration: zero grads, 1F1B over the microbatches, tied-embedding + DP reductions,
+  // ZeRO-1 Adam, parameter allgather. Loss stays on device (read_loss).
+  void step();
+  float read_loss();  // mean CE of the last step over the global batch (blocking)
+  void sync();
+  void barrier();
+
+  const ParamSlot* slot(int tensor_id) const;
+  // which: 0 = working bf16 param, 1 = fp32 grad (accumulated this step), 2 = fp32 master
+  // (dp must be 1 or the tensor must lie in this rank's ZeRO shard), 3 = Adam m, 4 = Adam v.
+  void read_tensor(int which, int tensor_id, float* host) const;
+  // Forward-only loss of the uploaded batch with the current parameters (no update).
+  float eval_loss();
+
+  int64_t flat_params() const { return P_; }
+  int64_t shard_params() const { return shard_; }
+  size_t device_bytes() const { return dev_bytes_; }
+  StepTimes last_times() const { return times_; }
+  int microbatches() const { return m_; }
+  int kernel_launches_per_step() const { return launches_; }
+  bool profile_comm = false;
+
+ private:
+  struct LayerW {
+    const bf16 *ln1g, *ln1b, *wqkv, *bqkv, *wo, *bo, *ln2g, *ln2b, *w1, *b1, *w2, *b2;
+  };
+  struct LayerG {
+    float *ln1g, *ln1b, *wqkv, *bqkv, *wo, *bo, *ln2g, *ln2b, *w1, *b1, *w2, *b2;
+  };
+  struct Slot {
+    std::vector<bf16*> h;         // Ll+1 residual-stream tensors [M, d]
+    std::vector<LayerActs> acts;  // per layer (empty under checkpointing)
+    int32_t* inputs = nullptr;    // [M]
+    int32_t* labels = nullptr;    // [M]
+  };
+
+  void* alloc(size_t bytes);
+  void build_layout();
+  void allocate();
+  LayerW w(int l) const;
+  LayerG gr(int l) const;
+  LayerActs& acts_for(int slot, int l);
+
+  void forward_op(int mb, bool with_loss);
+  void backward_op(int mb, bf16* dh);
+  void layer_fwd(int l, LayerActs& A, const bf16* hin, bf16* hout, bool fuse_next_ln, int slot);
+  void layer_recompute(int l, LayerActs& A, const bf16* hin);
+  void layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2);
+  void head_and_loss(int slot, bool with_grad);
+  void head_bwd(bf16* dh_out);
+  void optimizer_step();
+  void prepare_tokens(int mb, int slot);
+
+  void gemm_fwd(const bf16* X, const bf16* W, const bf16* bias, bf16* Y, int M, int N, int K, int epi = 0,
+                bf16* C2 = nullptr);
+  void gemm_dgrad(const bf16* dY, const bf16* W, bf16* dX, int M, int N, int K, int epi = 0,
+                  const bf16* aux = nullptr);
+  void gemm_wgrad(const bf16* dY, const bf16* X, float* dW, int M, int N, int K);
+  void ck(int status, const char* what);
+  void tp_allreduce(bf16* buf);
+  int64_t slot_offset(int tid) const { return slot(tid)->offset; }
+
+  trainplan::ModelSpec model_;
+  trainplan::ParallelConfig cfg_;
+  TrainOptions opts_;
+  Comms comms_;
+  int device_ = 0;
+  cudaStream_t st_ = nullptr;
+  std::vector<void*> allocations_;
+  size_t dev_bytes_ = 0;
+
+  // shape
+  int L_ = 0, Ll_ = 0, layer0_ = 0, d_ = 0, dt_ = 0, ht_ = 0, hd_ = 0, V_ = 0, Vt_ = 0, s_ = 0;
+  int mbs_ = 1, M_ = 0, m_ = 1, nslots_ = 1;
+  bool first_ = true, last_ = true, ckpt_ = false;
+  int step_no_ = 0;
+  int cur_mb_ = 0;
+  int launches_ = 0;
+
+  // parameters
+  std::vector<ParamSlot> slots_;
+  std::vector<int> slot_index_;  // tensor_id -> index in slots_ or -1
+  int64_t P_ = 0, shard_ = 0;
+  bf16* params_ = nullptr;
+  float *grads_ = nullptr, *master_ = nullptr, *adam_m_ = nullptr, *adam_v_ = nullptr;
+
+  // activations / workspaces
+  std::vector<Slot> slots_act_;
+  LayerActs scratch_;  // checkpointing recompute buffers
+  int32_t* tokens_ = nullptr;
+  bf16 *tmp_md_ = nullptr, *dh_[2] = {nullptr, nullptr}, *dy_ = nullptr, *du_ = nullptr, *dm_ = nullptr,
+       *do_ = nullptr, *dqkv_ = nullptr;
+  float *attn_D_ = nullptr, *dq_acc_ = nullptr, *ws_ = nullptr;
+  bf16* hf_ = nullptr;
+  float *muf_ = nullptr, *rsf_ = nullptr;
+  bf16* logits_ = nullptr;
+  float *xstats_ = nullptr, *xall_ = nullptr, *row_loss_ = nullptr, *loss_acc_ = nullptr;
+  StepTimes times_;
+};
+
+}  // namespace gptb200
