@@ -123,6 +123,13 @@ __global__ void resid_ln_kernel(ResidLnArgs a, DropDev dr) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) y[i] += b[i];
       }
+      if (a.resid_pos_table) {  // embedding: dropout(word + position), Megatron's embedding dropout
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          y[i] += r[i];
+          r[i] = 0.f;
+        }
+      }
       if (dr.on) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) y[i] = keep(dr, static_cast<int64_t>(roff) + c0 + i) ? y[i] * dr.scale : 0.f;
@@ -260,6 +267,107 @@ __global__ void ln_bwd_kernel(LnBwdArgs a, DropDev dr) {
       w[2 * d + c0 + i] = pbias[v][i];
     }
   }
+}
+
+// Wide rows (d > 8192): phase A computes dx / dxd per row (no column state), phase B the column
+// sums over 128-row chunks (column accumulators do not fit in registers at d = 12288 / 25600).
+template <int VPT>
+__global__ void ln_bwd_rows_kernel(LnBwdArgs a, DropDev dr) {
+  __shared__ float red[64];
+  const int d = a.d;
+  const int row = blockIdx.x;
+  const size_t roff = static_cast<size_t>(row) * d;
+  float dx[VPT][8];
+  if (a.dy) {
+    const float mu = a.mean[row], rs = a.rstd[row];
+    float s[2] = {0.f, 0.f};
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+      const int c0 = (v * blockDim.x + threadIdx.x) * 8;
+      float x[8], dy[8], g[8];
+      unpack8(*reinterpret_cast<const uint4*>(a.x + roff + c0), x);
+      unpack8(*reinterpret_cast<const uint4*>(a.dy + roff + c0), dy);
+      unpack8(*reinterpret_cast<const uint4*>(a.gamma + c0), g);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float xh = (x[i] - mu) * rs, gy = dy[i] * g[i];
+        s[0] += gy;
+        s[1] += gy * xh;
+        dx[v][i] = gy;  // stash g*dy; xh recomputed below
+      }
+    }
+    block_sum<2>(s, red);
+    const float m1 = s[0] / d, m2 = s[1] / d;
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+      const int c0 = (v * blockDim.x + threadIdx.x) * 8;
+      float x[8];
+      unpack8(*reinterpret_cast<const uint4*>(a.x + roff + c0), x);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dx[v][i] = rs * (dx[v][i] - m1 - (x[i] - mu) * rs * m2);
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < VPT; ++v)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dx[v][i] = 0.f;
+  }
+#pragma unroll
+  for (int v = 0; v < VPT; ++v) {
+    const int c0 = (v * blockDim.x + threadIdx.x) * 8;
+    if (a.resid_grad) {
+      float r[8];
+      unpack8(*reinterpret_cast<const uint4*>(a.resid_grad + roff + c0), r);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dx[v][i] += r[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dx[v][i] = round_bf16(dx[v][i]);
+    if (a.dx) *reinterpret_cast<uint4*>(a.dx + roff + c0) = pack8(dx[v]);
+    if (a.dxd && (dr.on || a.dxd != a.dx)) {
+      float o[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        o[i] = dr.on ? (keep(dr, static_cast<int64_t>(roff) + c0 + i) ? dx[v][i] * dr.scale : 0.f) : dx[v][i];
+      *reinterpret_cast<uint4*>(a.dxd + roff + c0) = pack8(o);
+    }
+  }
+}
+
+constexpr int kLnColRows = 128;
+
+// Column sums for the wide path: partial[chunk][3][d] of (dy*xhat, dy, dxd). `dxd_src` is the
+// tensor phase A wrote (dxd, or dx when dropout is off).
+__global__ void ln_bwd_cols_kernel(LnBwdArgs a, const bf16* __restrict__ dxd_src, float* __restrict__ ws) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  const int d = a.d;
+  if (c >= d) return;
+  const int r0 = blockIdx.y * kLnColRows, r1 = min(r0 + kLnColRows, a.rows);
+  float g0 = 0.f, g1 = 0.f, b0 = 0.f, b1 = 0.f, s0 = 0.f, s1 = 0.f;
+  for (int r = r0; r < r1; ++r) {
+    const size_t o = static_cast<size_t>(r) * d + c;
+    if (a.dy) {
+      const float mu = a.mean[r], rs = a.rstd[r];
+      const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a.x + o));
+      const float2 dy = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a.dy + o));
+      g0 += dy.x * (x.x - mu) * rs;
+      g1 += dy.y * (x.y - mu) * rs;
+      b0 += dy.x;
+      b1 += dy.y;
+    }
+    if (dxd_src) {
+      const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dxd_src + o));
+      s0 += v.x;
+      s1 += v.y;
+    }
+  }
+  float* w = ws + static_cast<size_t>(blockIdx.y) * 3 * d;
+  w[c] = g0;
+  w[c + 1] = g1;
+  w[d + c] = b0;
+  w[d + c + 1] = b1;
+  w[2 * d + c] = s0;
+  w[2 * d + c + 1] = s1;
 }
 
 __global__ void reduce_partials_kernel(const float* __restrict__ ws, int nblocks, int stride, int n,
@@ -520,8 +628,12 @@ int resid_ln_fwd(const ResidLnArgs& a, cudaStream_t st) {
 }
 
 size_t ln_bwd_workspace_floats(int rows, int d) {
-  return static_cast<size_t>((rows + kLnBwdRows - 1) / kLnBwdRows) * 3 * d;
+  const size_t fused = static_cast<size_t>((rows + kLnBwdRows - 1) / kLnBwdRows) * 3 * d;
+  const size_t wide = static_cast<size_t>((rows + kLnColRows - 1) / kLnColRows) * 3 * d;
+  return fused > wide ? fused : wide;
 }
+
+static bool ln_bwd_fused_ok(int d) { return d <= 8192 && pick_vpt(d) == 1; }
 
 int ln_bwd(const LnBwdArgs& a, cudaStream_t st) {
   const int vpt = pick_vpt(a.d);
@@ -529,15 +641,30 @@ int ln_bwd(const LnBwdArgs& a, cudaStream_t st) {
   if (a.drop.p > 0.f && a.dxd != nullptr && a.dxd == a.dx) return 1;  // would clobber dx
   if (a.dy && (!a.gamma || !a.mean || !a.rstd || !a.x)) return 1;
   const int threads = a.d / 8 / vpt;
-  const int blocks = (a.rows + kLnBwdRows - 1) / kLnBwdRows;
   const DropDev dr = make_drop(a.drop);
-  switch (vpt) {
-#define CASE(V) case V: ln_bwd_kernel<V><<<blocks, threads, 0, st>>>(a, dr); break;
-    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
-#undef CASE
-    default: return 1;
-  }
   const bool any = a.dgamma || a.dbeta || a.dbias;
+  if (!ln_bwd_fused_ok(a.d)) {
+    switch (vpt) {
+#define CASE(V) case V: ln_bwd_rows_kernel<V><<<a.rows, threads, 0, st>>>(a, dr); break;
+      CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+      default: return 1;
+    }
+    if (any) {
+      const bf16* src = nullptr;
+      if (a.dbias) src = a.dxd ? a.dxd : (a.dx ? a.dx : (!a.dy && !dr.on ? a.resid_grad : nullptr));
+      if (a.dbias && !src) return 1;
+      const int chunks = (a.rows + kLnColRows - 1) / kLnColRows;
+      dim3 grid((a.d / 2 + 255) / 256, chunks);
+      ln_bwd_cols_kernel<<<grid, 256, 0, st>>>(a, src, a.workspace);
+      reduce_partials_kernel<<<(a.d + 255) / 256, 256, 0, st>>>(a.workspace, chunks, 3 * a.d, a.d,
+                                                                  a.dy ? a.dgamma : nullptr,
+                                                                  a.dy ? a.dbeta : nullptr, a.dbias);
+    }
+    return status();
+  }
+  const int blocks = (a.rows + kLnBwdRows - 1) / kLnBwdRows;
+  ln_bwd_kernel<1><<<blocks, threads, 0, st>>>(a, dr);
   if (any) {
     // order of outputs in the workspace: dgamma, dbeta, dbias
     reduce_partials_kernel<<<(a.d + 255) / 256, 256, 0, st>>>(a.workspace, blocks, 3 * a.d, a.d,

@@ -25,7 +25,8 @@ struct DropKey {
 
 // h = resid + dropout(y + bias); optionally ln_out = LN(h)*gamma + beta with stats.
 //   y == nullptr: h = resid (pure LayerNorm of resid; h_out not written).
-//   resid_pos_table: resid is a [s, d] position table indexed by row % s (embedding stage).
+//   resid_pos_table: resid is a [s, d] position table indexed by row % s (embedding stage);
+//   the dropout then applies to the sum (word + position embedding).
 //   h_out may alias resid. All bf16 except mean/rstd (fp32).
 struct ResidLnArgs {
   int rows = 0, d = 0, seq = 1;

@@ -6,9 +6,11 @@ Tolerances (bf16 GPU vs fp32 oracle):
   * loss: |dL| <= 1e-2 * max(1, L);
   * gradients: per tensor, relative L2 <= 3e-2 and cosine >= 0.999 (tensors with a meaningful
     norm; bf16 activations + fp32 accumulation);
-  * one Adam step: relative L2 of the parameter update <= 0.25 (first-step Adam is sign-like, so
-    near-zero gradients flip; the update arithmetic itself is checked exactly in
-    test_gpu_kernels.py::test_adam_step_vs_reference_formula).
+  * one Adam step: the fp32 master after the step equals Adam applied on the host to the GPU's own
+    gradients (rtol 1e-5) — proves the optimizer consumed the right (ZeRO-)shard of the right
+    gradients; first-step Adam is sign-like, so comparing against the oracle's update would only
+    measure near-zero-gradient sign flips. The Adam arithmetic itself is checked in
+    test_gpu_kernels.py::test_adam_step_vs_reference_formula.
 """
 import numpy as np
 import pytest
@@ -82,20 +84,19 @@ def run_parity(L, d, heads, V, s, mbs, gbs, dropout=0.0, ckpt=False, steps=1):
         report["grads"] = worst
         bad = [w for w in worst if w[1] > 3e-2 or w[2] < 0.999]
         assert not bad, bad
-        # 3. Adam update
-        mom = np.zeros_like(params)
-        var = np.zeros_like(params)
-        new = params.copy()
-        O.load().orc_adam(params.size, new, grads, mom, var, 1, oo)
+        # 3. Adam update on the GPU's own gradients
+        b1, b2, lr, eps, wd = np.float32(0.9), np.float32(0.95), np.float32(1e-3), np.float32(1e-8), np.float32(0.01)
         for tid in range(ntens):
             info = sess.tensor_info(tid)
             if info is None:
                 continue
-            before = _global_slice(O.tensor(om, params, tid), info)
-            ref_upd = _global_slice(O.tensor(om, new, tid), info) - before
-            got_upd = sess.read_tensor(T.Session.READ_MASTER, tid) - before
-            if np.linalg.norm(ref_upd) > 0:
-                assert _rel(got_upd, ref_upd) < 0.25, (tid, _rel(got_upd, ref_upd))
+            before = _global_slice(O.tensor(om, params, tid), info).astype(np.float32)
+            g = sess.read_tensor(T.Session.READ_GRAD, tid)
+            m = (1 - b1) * g
+            v = (1 - b2) * g * g
+            mh, vh = m / (1 - b1), v / (1 - b2)
+            ref = before - lr * (mh / (np.sqrt(vh) + eps) + wd * before)
+            np.testing.assert_allclose(sess.read_tensor(T.Session.READ_MASTER, tid), ref, rtol=1e-5, atol=1e-7)
         for _ in range(steps - 1):
             sess.train_step(tokens)
         report["final_loss"] = sess.eval_loss()
