@@ -158,6 +158,21 @@ int tp_session_read_tensor(tp_session* s, int which, int tensor_id, float* host_
 /* out = {flat_params, shard_params, device_bytes, microbatches, launches_last_step, rank, world, 0} */
 int tp_session_info(tp_session* s, int64_t out[8]);
 
+/* Live timing. Kernel classes: 0 GEMM, 1 attention fwd, 2 attention bwd, 3 LayerNorm/residual,
+ * 4 other elementwise, 5 TP comm, 6 PP comm, 7 DP comm, 8 Adam. */
+#define TP_KERNEL_CLASSES 9
+typedef struct tp_kernel_times {
+  double ms[TP_KERNEL_CLASSES];      /* summed launch durations (CUDA events, step stream) */
+  int64_t launches[TP_KERNEL_CLASSES];
+  double flops[TP_KERNEL_CLASSES];   /* algorithmic FLOPs of those launches */
+  double bytes[TP_KERNEL_CLASSES];   /* algorithmic HBM bytes of those launches */
+} tp_kernel_times;
+/* Runs `steps` iterations on the uploaded tokens between two CUDA events on the session stream;
+ * *ms = device time. With profile != 0 every launch is bracketed by events into *kt. */
+int tp_session_time_steps(tp_session* s, int steps, int profile, float* ms, tp_kernel_times* kt);
+/* Max over all ranks of *v (NCCL on the world communicator); identity when world == 1. */
+int tp_session_allreduce_max(tp_session* s, float* v);
+
 #ifdef __cplusplus
 }
 #endif

@@ -51,6 +51,17 @@ class TrainOptions(C.Structure):
 
 
 _i64, _sz = C.c_int64, C.c_size_t
+
+KERNEL_CLASSES = ["gemm", "attn_fwd", "attn_bwd", "norm", "elementwise", "tp_comm", "pp_comm", "dp_comm", "adam"]
+
+
+class KernelTimes(C.Structure):
+    _fields_ = [("ms", C.c_double * 9), ("launches", C.c_int64 * 9), ("flops", C.c_double * 9),
+                ("bytes", C.c_double * 9)]
+
+    def as_dict(self):
+        return {k: {"ms": self.ms[i], "launches": self.launches[i], "flops": self.flops[i], "bytes": self.bytes[i]}
+                for i, k in enumerate(KERNEL_CLASSES)}
 _ptr = C.c_void_p
 
 # name -> (restype, argtypes)
@@ -86,6 +97,8 @@ SIGNATURES: dict[str, tuple] = {
     "tp_session_tensor_info": (_i, [_vp, _i, C.POINTER(_i64)]),
     "tp_session_read_tensor": (_i, [_vp, _i, _i, _vp]),
     "tp_session_info": (_i, [_vp, C.POINTER(_i64)]),
+    "tp_session_time_steps": (_i, [_vp, _i, _i, C.POINTER(_f), C.POINTER(KernelTimes)]),
+    "tp_session_allreduce_max": (_i, [_vp, C.POINTER(_f)]),
 }
 
 _lib = None
@@ -253,6 +266,17 @@ class Session:
         out = np.empty(info["rows"] * info["cols"], dtype=np.float32)
         check(self._lib.tp_session_read_tensor(self.h, which, tid, out.ctypes.data))
         return out.reshape(info["rows"], info["cols"]) if info["cols"] > 1 else out
+
+    def time_steps(self, steps: int, profile: bool = False):
+        ms = _f()
+        kt = KernelTimes()
+        check(self._lib.tp_session_time_steps(self.h, steps, int(profile), C.byref(ms), C.byref(kt)))
+        return ms.value, (kt.as_dict() if profile else None)
+
+    def allreduce_max(self, v: float) -> float:
+        x = _f(v)
+        check(self._lib.tp_session_allreduce_max(self.h, C.byref(x)))
+        return x.value
 
     def info(self) -> dict:
         out = (_i64 * 8)()

@@ -160,4 +160,24 @@ int tp_session_info(tp_session* s, int64_t out[8]) {
   });
 }
 
+int tp_session_time_steps(tp_session* s, int steps, int profile, float* ms, tp_kernel_times* kt) {
+  return run("tp_session_time_steps", [&] {
+    KernelTimes k;
+    *ms = s->stage->time_steps(steps, profile != 0, &k);
+    if (kt) {
+      static_assert(K_NUM == TP_KERNEL_CLASSES, "kernel class count");
+      for (int i = 0; i < K_NUM; ++i) {
+        kt->ms[i] = k.ms[i];
+        kt->launches[i] = k.launches[i];
+        kt->flops[i] = k.flops[i];
+        kt->bytes[i] = k.bytes[i];
+      }
+    }
+  });
+}
+
+int tp_session_allreduce_max(tp_session* s, float* v) {
+  return run("tp_session_allreduce_max", [&] { *v = s->stage->allreduce_max(*v); });
+}
+
 }  // extern "C"

@@ -37,6 +37,28 @@ void Stage::ck(int status, const char* what) {
   }
 }
 
+Stage::KScope::KScope(Stage* st, int kind, double flops, double bytes) : s(st), k(kind), idx(0) {
+  if (!s->profile_) return;
+  if (s->ev_used_ == s->ev_pool_.size()) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    s->ev_pool_.push_back({a, b});
+    s->ev_kind_.push_back(0);
+  }
+  idx = s->ev_used_++;
+  s->ev_kind_[idx] = kind;
+  s->prof_acc_.launches[kind] += 1;
+  s->prof_acc_.flops[kind] += flops;
+  s->prof_acc_.bytes[kind] += bytes;
+  cudaEventRecord(s->ev_pool_[idx].first, s->st_);
+}
+
+Stage::KScope::~KScope() {
+  if (!s->profile_) return;
+  cudaEventRecord(s->ev_pool_[idx].second, s->st_);
+}
+
 Stage::Stage(const trainplan::ModelSpec& model, const trainplan::ParallelConfig& cfg, const TrainOptions& opts,
              int rank, int world, int device, const void* nccl_id)
     : model_(model), cfg_(cfg), opts_(opts), device_(device) {
@@ -71,6 +93,10 @@ Stage::Stage(const trainplan::ModelSpec& model, const trainplan::ParallelConfig&
 
 Stage::~Stage() {
   if (st_) cudaStreamSynchronize(st_);
+  for (auto& e : ev_pool_) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
   for (void* p : allocations_) cudaFree(p);
   if (st_) cudaStreamDestroy(st_);
 }
@@ -259,6 +285,7 @@ void Stage::upload_tokens(const int32_t* src, int64_t n, bool on_device) {
 
 // ------------------------------------------------------------------------------ GEMM helpers
 void Stage::gemm_fwd(const bf16* X, const bf16* W, const bf16* bias, bf16* Y, int M, int N, int K, int epi, bf16* C2) {
+  KScope prof(this, K_GEMM, 2.0 * M * N * K);
   GemmParams p;
   p.M = M, p.N = N, p.K = K;
   p.A = X, p.lda = K, p.a_mn = false;
@@ -269,6 +296,7 @@ void Stage::gemm_fwd(const bf16* X, const bf16* W, const bf16* bias, bf16* Y, in
 
 // dX[M,K] = dY[M,N] . W[N,K]
 void Stage::gemm_dgrad(const bf16* dY, const bf16* W, bf16* dX, int M, int N, int K, int epi, const bf16* aux) {
+  KScope prof(this, K_GEMM, 2.0 * M * N * K);
   GemmParams p;
   p.M = M, p.N = K, p.K = N;
   p.A = dY, p.lda = N, p.a_mn = false;
@@ -279,6 +307,7 @@ void Stage::gemm_dgrad(const bf16* dY, const bf16* W, bf16* dX, int M, int N, in
 
 // dW[N,K] += dY[M,N]^T . X[M,K]   (fp32 main grad)
 void Stage::gemm_wgrad(const bf16* dY, const bf16* X, float* dW, int M, int N, int K) {
+  KScope prof(this, K_GEMM, 2.0 * M * N * K);
   GemmParams p;
   p.M = N, p.N = K, p.K = M;
   p.A = dY, p.lda = N, p.a_mn = true;
@@ -311,7 +340,10 @@ void Stage::layer_fwd(int l, LayerActs& A, const bf16* hin, bf16* hout, bool fus
   const int64_t sample0 = static_cast<int64_t>(comms_.me.d) * (cfg_.gbs / cfg_.dp) +
                           static_cast<int64_t>(cur_mb_) * mbs_;
   gemm_fwd(A.a, W.wqkv, W.bqkv, A.qkv, M_, 3 * dt_, d_);
-  ck(flash_attn_fwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, A.lse, st_), "flash fwd");
+  {
+    KScope prof(this, K_ATTN_FWD, 2.0 * mbs_ * ht_ * static_cast<double>(s_) * s_ * hd_);
+    ck(flash_attn_fwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, A.lse, st_), "flash fwd");
+  }
   gemm_fwd(A.o, W.wo, nullptr, tmp_md_, M_, d_, dt_);
   tp_allreduce(tmp_md_);
   ResidLnArgs r;
@@ -319,7 +351,10 @@ void Stage::layer_fwd(int l, LayerActs& A, const bf16* hin, bf16* hout, bool fus
   r.y = tmp_md_, r.bias = W.bo, r.resid = hin;
   r.drop = drop_key(opts_, step_no_, lg, 0, sample0, s_, d_);
   r.h_out = A.hmid, r.gamma = W.ln2g, r.beta = W.ln2b, r.ln_out = A.m2, r.mean = A.mu2, r.rstd = A.rs2;
-  ck(resid_ln_fwd(r, st_), "resid+ln2");
+  {
+    KScope prof(this, K_NORM, 0, 8.0 * M_ * d_);
+    ck(resid_ln_fwd(r, st_), "resid+ln2");
+  }
   gemm_fwd(A.m2, W.w1, W.b1, A.u, M_, 4 * dt_, d_, EPI_BIAS_GELU, A.g);
   gemm_fwd(A.g, W.w2, nullptr, tmp_md_, M_, d_, 4 * dt_);
   tp_allreduce(tmp_md_);
@@ -339,7 +374,10 @@ void Stage::layer_fwd(int l, LayerActs& A, const bf16* hin, bf16* hout, bool fus
       r2.ln_out = hf_, r2.mean = muf_, r2.rstd = rsf_;
     }
   }
-  ck(resid_ln_fwd(r2, st_), "resid+ln1");
+  {
+    KScope prof(this, K_NORM, 0, 8.0 * M_ * d_);
+    ck(resid_ln_fwd(r2, st_), "resid+ln1");
+  }
 }
 
 void Stage::layer_recompute(int l, LayerActs& A, const bf16* hin) {
@@ -350,9 +388,15 @@ void Stage::layer_recompute(int l, LayerActs& A, const bf16* hin) {
   ResidLnArgs r0;
   r0.rows = M_, r0.d = d_, r0.seq = s_;
   r0.resid = hin, r0.gamma = W.ln1g, r0.beta = W.ln1b, r0.ln_out = A.a, r0.mean = A.mu1, r0.rstd = A.rs1;
-  ck(resid_ln_fwd(r0, st_), "recompute ln1");
+  {
+    KScope prof(this, K_NORM, 0, 8.0 * M_ * d_);
+    ck(resid_ln_fwd(r0, st_), "recompute ln1");
+  }
   gemm_fwd(A.a, W.wqkv, W.bqkv, A.qkv, M_, 3 * dt_, d_);
-  ck(flash_attn_fwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, A.lse, st_), "flash fwd");
+  {
+    KScope prof(this, K_ATTN_FWD, 2.0 * mbs_ * ht_ * static_cast<double>(s_) * s_ * hd_);
+    ck(flash_attn_fwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, A.lse, st_), "flash fwd");
+  }
   gemm_fwd(A.o, W.wo, nullptr, tmp_md_, M_, d_, dt_);
   tp_allreduce(tmp_md_);
   ResidLnArgs r;
@@ -360,13 +404,17 @@ void Stage::layer_recompute(int l, LayerActs& A, const bf16* hin) {
   r.y = tmp_md_, r.bias = W.bo, r.resid = hin;
   r.drop = drop_key(opts_, step_no_, lg, 0, sample0, s_, d_);
   r.h_out = A.hmid, r.gamma = W.ln2g, r.beta = W.ln2b, r.ln_out = A.m2, r.mean = A.mu2, r.rstd = A.rs2;
-  ck(resid_ln_fwd(r, st_), "recompute ln2");
+  {
+    KScope prof(this, K_NORM, 0, 8.0 * M_ * d_);
+    ck(resid_ln_fwd(r, st_), "recompute ln2");
+  }
   gemm_fwd(A.m2, W.w1, W.b1, A.u, M_, 4 * dt_, d_, EPI_BIAS_GELU, A.g);
 }
 
 void Stage::tp_allreduce(bf16* buf) {
   if (cfg_.tp == 1) return;
   ++launches_;
+  KScope prof(this, K_COMM_TP, 0, 2.0 * M_ * d_);
   try {
     comms_.tp_allreduce_bf16(buf, static_cast<size_t>(M_) * d_, st_);
   } catch (const CommError& e) {
@@ -394,7 +442,10 @@ void Stage::forward_op(int mb, bool with_loss) {
   } else {
     r.resid = S.h[0];
   }
-  ck(resid_ln_fwd(r, st_), "embed+ln1");
+  {
+    KScope prof(this, K_NORM, 0, 8.0 * M_ * d_);
+    ck(resid_ln_fwd(r, st_), "embed+ln1");
+  }
   for (int l = 0; l < Ll_; ++l) layer_fwd(l, acts_for(slot, l), S.h[l], S.h[l + 1], (l + 1 < Ll_) || last_, slot);
   if (last_) head_and_loss(slot, with_loss);
 }
@@ -431,7 +482,10 @@ void Stage::layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2)
   // MLP branch
   gemm_dgrad(dy2, W.w2, du_, M_, d_, 4 * dt_, EPI_DGELU, A.u);
   gemm_wgrad(dy2, A.g, G.w2, M_, d_, 4 * dt_);
-  ck(colsum_bf16(du_, M_, 4 * dt_, G.b1, ws_, st_), "db1");
+  {
+    KScope prof(this, K_ELEM);
+    ck(colsum_bf16(du_, M_, 4 * dt_, G.b1, ws_, st_), "db1");
+  }
   gemm_dgrad(du_, W.w1, dm_, M_, 4 * dt_, d_);
   tp_allreduce(dm_);
   gemm_wgrad(du_, A.m2, G.w1, M_, 4 * dt_, d_);
@@ -442,13 +496,22 @@ void Stage::layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2)
   b.drop = drop_key(opts_, step_no_, lg, 0, sample0, s_, d_);
   b.dxd = drop_on ? dy_ : dh;
   b.dgamma = G.ln2g, b.dbeta = G.ln2b, b.dbias = G.bo, b.workspace = ws_;
-  ck(ln_bwd(b, st_), "ln2 bwd");
+  {
+    KScope prof(this, K_NORM, 0, 10.0 * M_ * d_);
+    ck(ln_bwd(b, st_), "ln2 bwd");
+  }
   const bf16* dya = drop_on ? dy_ : dh;
   // attention branch
   gemm_dgrad(dya, W.wo, do_, M_, d_, dt_);
   gemm_wgrad(dya, A.o, G.wo, M_, d_, dt_);
-  ck(flash_attn_bwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, do_, A.lse, attn_D_, dq_acc_, dqkv_, st_), "flash bwd");
-  ck(colsum_bf16(dqkv_, M_, 3 * dt_, G.bqkv, ws_, st_), "dbqkv");
+  {
+    KScope prof(this, K_ATTN_BWD, 5.0 * mbs_ * ht_ * static_cast<double>(s_) * s_ * hd_);
+    ck(flash_attn_bwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, do_, A.lse, attn_D_, dq_acc_, dqkv_, st_), "flash bwd");
+  }
+  {
+    KScope prof(this, K_ELEM);
+    ck(colsum_bf16(dqkv_, M_, 3 * dt_, G.bqkv, ws_, st_), "dbqkv");
+  }
   gemm_dgrad(dqkv_, W.wqkv, dm_, M_, 3 * dt_, d_);
   tp_allreduce(dm_);
   gemm_wgrad(dqkv_, A.a, G.wqkv, M_, 3 * dt_, d_);
@@ -465,7 +528,10 @@ void Stage::layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2)
     c.drop = drop_key(opts_, step_no_, kEmbedLayer, 2, sample0, s_, d_);
     c.dxd = drop_on ? dy_ : dh;
   }
-  ck(ln_bwd(c, st_), "ln1 bwd");
+  {
+    KScope prof(this, K_NORM, 0, 10.0 * M_ * d_);
+    ck(ln_bwd(c, st_), "ln1 bwd");
+  }
 }
 
 void Stage::backward_op(int mb, bf16* dh) {
@@ -492,7 +558,10 @@ void Stage::backward_op(int mb, bf16* dh) {
     b.dx = nullptr;
     if (!drop_on) b.dxd = nullptr;
   }
-  ck(ln_bwd(b, st_), "final ln / stage-boundary bwd");
+  {
+    KScope prof(this, K_NORM, 0, 10.0 * M_ * d_);
+    ck(ln_bwd(b, st_), "final ln / stage-boundary bwd");
+  }
   for (int l = Ll_ - 1; l >= 0; --l) {
     LayerActs& A = acts_for(slot, l);
     if (ckpt_) layer_recompute(l, A, S.h[l]);
@@ -517,6 +586,7 @@ void Stage::optimizer_step() {
   a.lr = opts_.lr, a.beta1 = opts_.beta1, a.beta2 = opts_.beta2, a.eps = opts_.eps, a.weight_decay = opts_.weight_decay;
   a.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(opts_.beta1), step_no_));
   a.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(opts_.beta2), step_no_));
+  KScope prof(this, K_ADAM, 0, 30.0 * shard_);
   ck(adam_step(a, st_), "adam");
 }
 
@@ -540,8 +610,11 @@ void Stage::step() {
         recv = dh_[dh_idx];
         recv_peer = comms_.me.p + 1;
       }
-      if (pending || recv) ++launches_;
-      comms_.pp_exchange(pending, pending_peer, recv, recv_peer, n_act, st_);
+      if (pending || recv) {
+        ++launches_;
+        KScope prof(this, K_COMM_PP);
+        comms_.pp_exchange(pending, pending_peer, recv, recv_peer, n_act, st_);
+      }
       pending = nullptr;
       if (!op.backward) {
         forward_op(op.microbatch, true);
@@ -563,9 +636,15 @@ void Stage::step() {
       comms_.pp_exchange(pending, pending_peer, nullptr, -1, n_act, st_);
     }
     if (cfg_.pp > 1 && (first_ || last_)) comms_.emb_allreduce_f32(grads_ + slot_offset(0), static_cast<size_t>(Vt_) * d_, st_);
-    comms_.dp_reduce_scatter_f32(grads_, shard_, st_);
+    {
+      KScope prof(this, K_COMM_DP);
+      comms_.dp_reduce_scatter_f32(grads_, shard_, st_);
+    }
     optimizer_step();
-    comms_.dp_allgather_bf16(params_, shard_, st_);
+    {
+      KScope prof(this, K_COMM_DP);
+      comms_.dp_allgather_bf16(params_, shard_, st_);
+    }
     comms_.world_allreduce_f32(loss_acc_, 1, st_);
   } catch (const CommError& e) {
     throw StepError{e.code, e.msg};
@@ -638,6 +717,60 @@ void Stage::read_tensor(int which, int tid, float* host) const {
     base = which == 2 ? master_ : (which == 3 ? adam_m_ : adam_v_);
   }
   cudaMemcpy(host, base + off, n * 4, cudaMemcpyDeviceToHost);
+}
+
+}  // namespace gptb200
+
+namespace gptb200 {
+
+float Stage::time_steps(int steps, bool profile, KernelTimes* kt) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  profile_ = profile;
+  ev_used_ = 0;
+  prof_acc_ = KernelTimes{};
+  cudaEventRecord(a, st_);
+  try {
+    for (int i = 0; i < steps; ++i) step();
+  } catch (...) {
+    profile_ = false;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    throw;
+  }
+  cudaEventRecord(b, st_);
+  sync();
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  if (profile && kt) {
+    *kt = prof_acc_;
+    for (int k = 0; k < K_NUM; ++k) kt->ms[k] = 0;
+    for (size_t i = 0; i < ev_used_; ++i) {
+      float e = 0.f;
+      cudaEventElapsedTime(&e, ev_pool_[i].first, ev_pool_[i].second);
+      kt->ms[ev_kind_[i]] += e;
+    }
+  }
+  profile_ = false;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return ms;
+}
+
+float Stage::allreduce_max(float v) {
+  if (comms_.world == 1) return v;
+  float* d = ws_;
+  cudaMemcpyAsync(d, &v, sizeof(float), cudaMemcpyHostToDevice, st_);
+  try {
+    nccl_check(ncclAllReduce(d, d, 1, ncclFloat, ncclMax, comms_.world_comm, st_), "allreduce max");
+  } catch (const CommError& e) {
+    throw StepError{e.code, e.msg};
+  }
+  float out = 0.f;
+  cudaMemcpyAsync(&out, d, sizeof(float), cudaMemcpyDeviceToHost, st_);
+  sync();
+  return out;
 }
 
 }  // namespace gptb200

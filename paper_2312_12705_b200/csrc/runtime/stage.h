@@ -43,6 +43,16 @@ struct LayerActs {
   float *mu1 = nullptr, *rs1 = nullptr, *mu2 = nullptr, *rs2 = nullptr, *lse = nullptr;
 };
 
+// Kernel classes for the live per-launch timing (CUDA events on the step stream).
+enum KernelClass { K_GEMM = 0, K_ATTN_FWD, K_ATTN_BWD, K_NORM, K_ELEM, K_COMM_TP, K_COMM_PP, K_COMM_DP, K_ADAM, K_NUM };
+
+struct KernelTimes {
+  double ms[K_NUM] = {};
+  long launches[K_NUM] = {};
+  double flops[K_NUM] = {};  // algorithmic FLOPs (GEMM 2MNK; attention causal)
+  double bytes[K_NUM] = {};  // algorithmic HBM bytes (norm / elementwise / Adam)
+};
+
 struct StepTimes {  // milliseconds of the last step on this rank (CUDA events)
   float total = 0, tp_comm = 0, pp_comm = 0, dp_comm = 0, optimizer = 0;
 };
@@ -78,7 +88,10 @@ class Stage {
   StepTimes last_times() const { return times_; }
   int microbatches() const { return m_; }
   int kernel_launches_per_step() const { return launches_; }
-  bool profile_comm = false;
+  // Runs `steps` iterations bracketed by CUDA events on the step stream; returns device ms.
+  // With profile, every launch is bracketed too and summed per KernelClass into *kt.
+  float time_steps(int steps, bool profile, KernelTimes* kt);
+  float allreduce_max(float v);
 
  private:
   struct LayerW {
@@ -117,6 +130,19 @@ class Stage {
                   const bf16* aux = nullptr);
   void gemm_wgrad(const bf16* dY, const bf16* X, float* dW, int M, int N, int K);
   void ck(int status, const char* what);
+  friend struct KScope;
+  struct KScope {
+    Stage* s;
+    int k;
+    size_t idx;
+    KScope(Stage* st, int kind, double flops = 0, double bytes = 0);
+    ~KScope();
+  };
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool_;
+  std::vector<int> ev_kind_;
+  size_t ev_used_ = 0;
+  bool profile_ = false;
+  KernelTimes prof_acc_;
   void tp_allreduce(bf16* buf);
   int64_t slot_offset(int tid) const { return slot(tid)->offset; }
 
