@@ -463,6 +463,12 @@ int bwd_impl(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* 
 
 int flash_attn_fwd(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse,
                    cudaStream_t st) {
+  return flash_attn_fwd_tc(a, qkv, out, lse, st);
+}
+
+// mma.sync (FA2) forward, kept only as a cross-check for the tcgen05 kernel in the GPU tests.
+int flash_attn_fwd_mma(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse,
+                       cudaStream_t st) {
   if (a.seq % 128 != 0) return 1;
   switch (a.head_dim) {
     case 64: return fwd_impl<64>(a, qkv, out, lse, st);

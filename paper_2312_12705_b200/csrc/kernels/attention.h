@@ -17,6 +17,10 @@ struct AttnShape {
 int flash_attn_fwd(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse,
                    cudaStream_t st);
 
+// tcgen05/TMEM forward (attention_sm100.cu); flash_attn_fwd dispatches to it.
+int flash_attn_fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse,
+                      cudaStream_t st);
+
 // Writes dqkv[M, 3*heads*hd]. Workspaces: D[batch*heads*seq] fp32, dq_acc[M*heads*hd] fp32.
 int flash_attn_bwd(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* out,
                    const __nv_bfloat16* dout, const float* lse, float* D, float* dq_acc,

@@ -1,0 +1,17 @@
+// Host-side TMA descriptor encoding shared by the tcgen05 kernels.
+#pragma once
+
+#include <cuda.h>
+
+#include <cstdint>
+
+namespace gptb200 {
+
+// 2D bf16 tensor map over a row-major [outer][inner] matrix with leading dimension ld
+// (elements), box {box_inner, box_outer}, 128B swizzle (box_inner * 2 <= 128).
+bool make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+                    uint32_t box_inner, uint32_t box_outer);
+
+int device_sm_count();
+
+}  // namespace gptb200
