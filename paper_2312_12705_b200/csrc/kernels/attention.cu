@@ -451,9 +451,15 @@ int bwd_impl(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* 
   const int warps = M * a.heads;
   flash_bwd_pre_kernel<HD><<<(warps + 7) / 8, 256, 0, st>>>(out, dout, D, dq_acc, a.seq, a.heads, M);
   const float scale = 1.f / sqrtf(static_cast<float>(HD));
-  dim3 grid(a.seq / Cfg::BN, a.batch * a.heads);
-  flash_bwd_kernel<HD><<<grid, 128, Cfg::kSmem, st>>>(qkv, dout, lse, D, dq_acc, dqkv, a.seq, a.heads,
-                                                      scale * kLog2e, scale);
+  if (HD != 160) {
+    // tcgen05 main kernel (attention_sm100.cu); TMEM cannot hold dK+dV+S+dP at hd=160
+    const int r = flash_attn_bwd_tc_main(a, qkv, dout, lse, D, dq_acc, dqkv, st);
+    if (r != 0) return r;
+  } else {
+    dim3 grid(a.seq / Cfg::BN, a.batch * a.heads);
+    flash_bwd_kernel<HD><<<grid, 128, Cfg::kSmem, st>>>(qkv, dout, lse, D, dq_acc, dqkv, a.seq, a.heads,
+                                                        scale * kLog2e, scale);
+  }
   const int dt = a.heads * HD;
   flash_bwd_dq_kernel<<<1184, 256, 0, st>>>(dq_acc, dqkv, M, dt, scale);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;

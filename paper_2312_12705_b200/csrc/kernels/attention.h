@@ -21,6 +21,12 @@ int flash_attn_fwd(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* 
 int flash_attn_fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse,
                       cudaStream_t st);
 
+// tcgen05 backward main kernel (hd 64/128): dK, dV into dqkv and dQ into the zeroed fp32 dq_acc
+// (D must already hold rowsum(dO*O)).
+int flash_attn_bwd_tc_main(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout,
+                           const float* lse, const float* D, float* dq_acc, __nv_bfloat16* dqkv,
+                           cudaStream_t st);
+
 // Writes dqkv[M, 3*heads*hd]. Workspaces: D[batch*heads*seq] fp32, dq_acc[M*heads*hd] fp32.
 int flash_attn_bwd(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* out,
                    const __nv_bfloat16* dout, const float* lse, float* D, float* dq_acc,

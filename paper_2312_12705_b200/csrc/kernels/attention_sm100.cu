@@ -289,6 +289,280 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// ----------------------------------------------------------------------------- backward
+// K6 on tcgen05. CTA = one (sequence, head, 128-row KV block); loops over the 128-row query tiles
+// at and after the diagonal. Per tile:  S^T = K Q^T and dP^T = V dO^T (TMEM), one thread per KV
+// row builds P^T = exp2(S^T*scale - lse) and dS^T = P^T (dP^T - D) in 128B-swizzled smem, then
+// dV += P^T dO and dK += dS^T Q accumulate in TMEM for the whole loop while dQ_tile = dS K
+// (dS^T re-read as an MN-major operand) lands in the S^T columns and is flushed with vector
+// fp32 reductions into dq_acc. TMEM: S^T|dQ (128) + dP^T (128) + dV (hd) + dK (hd) <= 512.
+template <int HD>
+struct TcBwdCfg {
+  static constexpr int NC = HD / 64;
+  static constexpr int kTileBytes = 128 * 128;
+  static constexpr int kOpBytes = NC * kTileBytes;  // one [128][HD] operand
+  static constexpr int kSmem = 4 * kOpBytes + 2 * 2 * kTileBytes + 4 * 128 * 4 + 1024 + 256;
+};
+
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+template <int HD>
+__global__ void __launch_bounds__(192, 1)
+    fa_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                     const float* __restrict__ lse, const float* __restrict__ Dg, float* __restrict__ dq_acc,
+                     __nv_bfloat16* __restrict__ dqkv, int s, int ht, float scale_log2, float scale) {
+  using Cfg = TcBwdCfg<HD>;
+  constexpr int NC = Cfg::NC, TB = Cfg::kTileBytes;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + Cfg::kOpBytes;
+  uint8_t* sQ = sV + Cfg::kOpBytes;
+  uint8_t* sdO = sQ + Cfg::kOpBytes;
+  uint8_t* sPT = sdO + Cfg::kOpBytes;  // [2 q-chunks][128 kv][64]
+  uint8_t* sdST = sPT + 2 * TB;        // [2 q-chunks][128 kv][64]
+  float* sL = reinterpret_cast<float*>(sdST + 2 * TB);  // [2][128]
+  float* sD = sL + 2 * 128;                              // [2][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * 128);
+  uint64_t* kv_full = bars;
+  uint64_t* qdo_full = bars + 1;
+  uint64_t* qdo_empty = bars + 2;
+  uint64_t* sdp_full = bars + 3;
+  uint64_t* sdp_free = bars + 4;
+  uint64_t* pds_full = bars + 5;
+  uint64_t* pds_free = bars + 6;
+  uint64_t* dq_full = bars + 7;
+  uint64_t* dq_free = bars + 8;
+  uint64_t* kdv_full = bars + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kvb = blockIdx.x;
+  const int b = blockIdx.y / ht, h = blockIdx.y % ht;
+  const int dt = ht * HD;
+  const int row0 = b * s;
+  const int kv0 = kvb * 128;
+  const int qt_first = kvb, qt_end = s / 128;
+  const int n_it = qt_end - qt_first;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tm_qkv);
+    ptx::tma_prefetch_desc(&tm_do);
+    ptx::mbar_init(kv_full, 1);
+    ptx::mbar_init(qdo_full, 1);
+    ptx::mbar_init(qdo_empty, 1);
+    ptx::mbar_init(sdp_full, 1);
+    ptx::mbar_init(sdp_free, 4);
+    ptx::mbar_init(pds_full, 4);
+    ptx::mbar_init(pds_free, 1);
+    ptx::mbar_init(dq_full, 1);
+    ptx::mbar_init(dq_free, 4);
+    ptx::mbar_init(kdv_full, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 256 + HD;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(kv_full, 2 * Cfg::kOpBytes);
+      for (int c = 0; c < NC; ++c) {
+        ptx::tma_load_2d(sK + c * TB, &tm_qkv, kv_full, dt + h * HD + 64 * c, row0 + kv0);
+        ptx::tma_load_2d(sV + c * TB, &tm_qkv, kv_full, 2 * dt + h * HD + 64 * c, row0 + kv0);
+      }
+      for (int it = 0; it < n_it; ++it) {
+        const int q0 = (qt_first + it) * 128;
+        WAIT(qdo_empty, (it & 1) ^ 1, 20);
+        ptx::mbar_arrive_expect_tx(qdo_full, 2 * Cfg::kOpBytes);
+        for (int c = 0; c < NC; ++c) {
+          ptx::tma_load_2d(sQ + c * TB, &tm_qkv, qdo_full, h * HD + 64 * c, row0 + q0);
+          ptx::tma_load_2d(sdO + c * TB, &tm_do, qdo_full, h * HD + 64 * c, row0 + q0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_sq = ptx::idesc_bf16_f32(128, 128, false, false);  // S^T, dP^T
+      constexpr uint32_t id_acc = ptx::idesc_bf16_f32(128, HD, false, true);   // dV, dK
+      constexpr uint32_t id_dq = ptx::idesc_bf16_f32(128, HD, true, true);     // dQ
+      const uint32_t aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV), aQ = ptx::smem_u32(sQ),
+                     adO = ptx::smem_u32(sdO), aPT = ptx::smem_u32(sPT), adST = ptx::smem_u32(sdST);
+      WAIT(kv_full, 0, 21);
+      for (int it = 0; it < n_it; ++it) {
+        WAIT(qdo_full, it & 1, 22);
+        WAIT(dq_free, (it & 1) ^ 1, 23);
+        WAIT(sdp_free, (it & 1) ^ 1, 24);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk / 4) * TB + (kk % 4) * 32;
+          ptx::mma_bf16_ss(tS, ptx::smem_desc_sw128(aK + off, 16, 1024), ptx::smem_desc_sw128(aQ + off, 16, 1024),
+                           id_sq, kk > 0 ? 1u : 0u);
+          ptx::mma_bf16_ss(tdP, ptx::smem_desc_sw128(aV + off, 16, 1024), ptx::smem_desc_sw128(adO + off, 16, 1024),
+                           id_sq, kk > 0 ? 1u : 0u);
+        }
+        ptx::mma_commit(sdp_full);
+        WAIT(pds_full, it & 1, 25);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 128 / 16; ++kk) {  // K = 128 query rows
+          const uint32_t aoff = (kk / 4) * TB + (kk % 4) * 32;
+          const uint64_t bdo = ptx::smem_desc_sw128(adO + kk * 2048, TB, 1024);
+          const uint64_t bq = ptx::smem_desc_sw128(aQ + kk * 2048, TB, 1024);
+          const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+          ptx::mma_bf16_ss(tdV, ptx::smem_desc_sw128(aPT + aoff, 16, 1024), bdo, id_acc, acc);
+          ptx::mma_bf16_ss(tdK, ptx::smem_desc_sw128(adST + aoff, 16, 1024), bq, id_acc, acc);
+        }
+#pragma unroll
+        for (int kk = 0; kk < 128 / 16; ++kk) {  // K = 128 kv rows
+          ptx::mma_bf16_ss(tS, ptx::smem_desc_sw128(adST + kk * 2048, TB, 1024),
+                           ptx::smem_desc_sw128(aK + kk * 2048, TB, 1024), id_dq, kk > 0 ? 1u : 0u);
+        }
+        ptx::mma_commit(dq_full);
+        ptx::mma_commit(qdo_empty);
+        ptx::mma_commit(pds_free);
+      }
+      ptx::mma_commit(kdv_full);
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;  // TMEM lane: kv row for S^T/dP^T/dK/dV, q row for dQ
+    const uint32_t lb = static_cast<uint32_t>(quarter * 32) << 16;
+    const int tid = threadIdx.x - 64;
+    const float* gL = lse + (static_cast<size_t>(b) * ht + h) * s;
+    const float* gD = Dg + (static_cast<size_t>(b) * ht + h) * s;
+    for (int it = 0; it < n_it; ++it) {
+      const int q0 = (qt_first + it) * 128;
+      const int lb2 = (it & 1) * 128;
+      sL[lb2 + tid] = gL[q0 + tid];
+      sD[lb2 + tid] = gD[q0 + tid];
+      named_sync(1, 128);
+      WAIT(sdp_full, it & 1, 26);
+      ptx::tc_fence_after();
+      WAIT(pds_free, (it & 1) ^ 1, 27);
+      const bool diag = (it == 0);
+      uint8_t* prow = sPT + r * 128;
+      uint8_t* drow = sdST + r * 128;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {  // 32 query columns at a time
+        uint32_t sv[32], dv[32];
+        ptx::tmem_ld_32x32b_x32(tS + lb + c * 32, sv);
+        ptx::tmem_ld_32x32b_x32(tdP + lb + c * 32, dv);
+        ptx::tmem_ld_wait();
+        uint32_t pk[16], dk[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          float p0 = exp2f(__uint_as_float(sv[e]) * scale_log2 - sL[lb2 + c * 32 + e]);
+          float p1 = exp2f(__uint_as_float(sv[e + 1]) * scale_log2 - sL[lb2 + c * 32 + e + 1]);
+          if (diag) {
+            if (c * 32 + e < r) p0 = 0.f;
+            if (c * 32 + e + 1 < r) p1 = 0.f;
+          }
+          const float d0 = p0 * (__uint_as_float(dv[e]) - sD[lb2 + c * 32 + e]);
+          const float d1 = p1 * (__uint_as_float(dv[e + 1]) - sD[lb2 + c * 32 + e + 1]);
+          pk[e / 2] = ptx::pack_bf16(p0, p1);
+          dk[e / 2] = ptx::pack_bf16(d0, d1);
+        }
+        // columns c*32..c*32+31 = chunk c/2, 16B units u0..u0+3 with u0 = (c%2)*4
+        const int chunk = c >> 1, u0 = (c & 1) * 4;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int off = chunk * TB + (((u0 + u) ^ (r & 7)) * 16);
+          *reinterpret_cast<uint4*>(prow + off) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          *reinterpret_cast<uint4*>(drow + off) = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+        }
+      }
+      ptx::fence_proxy_async();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        ptx::mbar_arrive(sdp_free);
+        ptx::mbar_arrive(pds_full);
+      }
+      // dQ tile (thread = query row q0 + r) -> fp32 reductions into dq_acc
+      WAIT(dq_full, it & 1, 28);
+      ptx::tc_fence_after();
+      float* dqrow = dq_acc + static_cast<size_t>(row0 + q0 + r) * dt + h * HD;
+#pragma unroll 1
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(tS + lb + c * 32, v);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; e += 4)
+          red_add_v4(dqrow + c * 32 + e, __uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
+                     __uint_as_float(v[e + 3]));
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(dq_free);
+    }
+    // dK (scaled) and dV rows of this KV block
+    WAIT(kdv_full, 0, 29);
+    ptx::tc_fence_after();
+    __nv_bfloat16* krow = dqkv + static_cast<size_t>(row0 + kv0 + r) * 3 * dt + dt + h * HD;
+    __nv_bfloat16* vrow = krow + dt;
+#pragma unroll 1
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t kv[32], vv[32];
+      ptx::tmem_ld_32x32b_x32(tdK + lb + c * 32, kv);
+      ptx::tmem_ld_32x32b_x32(tdV + lb + c * 32, vv);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 a, bb;
+        a.x = ptx::pack_bf16(__uint_as_float(kv[8 * q]) * scale, __uint_as_float(kv[8 * q + 1]) * scale);
+        a.y = ptx::pack_bf16(__uint_as_float(kv[8 * q + 2]) * scale, __uint_as_float(kv[8 * q + 3]) * scale);
+        a.z = ptx::pack_bf16(__uint_as_float(kv[8 * q + 4]) * scale, __uint_as_float(kv[8 * q + 5]) * scale);
+        a.w = ptx::pack_bf16(__uint_as_float(kv[8 * q + 6]) * scale, __uint_as_float(kv[8 * q + 7]) * scale);
+        bb.x = ptx::pack_bf16(__uint_as_float(vv[8 * q]), __uint_as_float(vv[8 * q + 1]));
+        bb.y = ptx::pack_bf16(__uint_as_float(vv[8 * q + 2]), __uint_as_float(vv[8 * q + 3]));
+        bb.z = ptx::pack_bf16(__uint_as_float(vv[8 * q + 4]), __uint_as_float(vv[8 * q + 5]));
+        bb.w = ptx::pack_bf16(__uint_as_float(vv[8 * q + 6]), __uint_as_float(vv[8 * q + 7]));
+        reinterpret_cast<uint4*>(krow + c * 32)[q] = a;
+        reinterpret_cast<uint4*>(vrow + c * 32)[q] = bb;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int HD>
+int bwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* D,
+           float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st) {
+  using Cfg = TcBwdCfg<HD>;
+  static bool init = false;
+  if (!init) {
+    if (cudaFuncSetAttribute(fa_bwd_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
+        cudaSuccess)
+      return 3;
+    init = true;
+  }
+  const int dt = a.heads * HD;
+  const uint64_t M = static_cast<uint64_t>(a.batch) * a.seq;
+  CUtensorMap tq, tdo;
+  if (!make_tmap_bf16(&tq, qkv, 3 * static_cast<uint64_t>(dt), M, 3 * dt, 64, 128)) return 3;
+  if (!make_tmap_bf16(&tdo, dout, static_cast<uint64_t>(dt), M, dt, 64, 128)) return 3;
+  dim3 grid(a.seq / 128, a.batch * a.heads);
+  const float scale = 1.f / sqrtf(static_cast<float>(HD));
+  fa_bwd_tc_kernel<HD><<<grid, 192, Cfg::kSmem, st>>>(tq, tdo, lse, D, dq_acc, dqkv, a.seq, a.heads, scale * kLog2e,
+                                                       scale);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
 template <int HD>
 int fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, cudaStream_t st) {
   using Cfg = TcFwdCfg<HD>;
@@ -310,6 +584,16 @@ int fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, flo
 }
 
 }  // namespace
+
+int flash_attn_bwd_tc_main(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse,
+                           const float* D, float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st) {
+  if (a.seq % 128 != 0) return 1;
+  switch (a.head_dim) {
+    case 64: return bwd_tc<64>(a, qkv, dout, lse, D, dq_acc, dqkv, st);
+    case 128: return bwd_tc<128>(a, qkv, dout, lse, D, dq_acc, dqkv, st);
+    default: return 1;
+  }
+}
 
 int flash_attn_fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, cudaStream_t st) {
   if (a.seq % kBM != 0) return 1;
