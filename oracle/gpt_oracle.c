@@ -49,11 +49,13 @@ float orc_init_value(uint64_t seed, int tensor_id, int64_t idx, float stddev) {
 }
 
 int orc_dropout_keep(uint64_t seed, int step, int layer, int site, int64_t elem, float p) {
+  /* one 64-bit hash per 4 consecutive elements; element e uses bits [16*(e%4), 16*(e%4)+16) */
   if (p <= 0.f) return 1;
   uint64_t key = mix64(seed ^ 0xD6E8FEB86659FD93ULL ^ ((uint64_t)(uint32_t)step << 40) ^
                        ((uint64_t)(uint32_t)(layer & 0xFFFF) << 16) ^ (uint64_t)(uint32_t)site);
-  uint32_t r = (uint32_t)(mix64(key + (uint64_t)elem) >> 40);
-  uint32_t thr = (uint32_t)((double)p * 16777216.0);
+  uint64_t h = mix64(key + ((uint64_t)elem >> 2));
+  uint32_t r = (uint32_t)(h >> (16 * (elem & 3))) & 0xFFFFu;
+  uint32_t thr = (uint32_t)((double)p * 65536.0);
   return r >= thr;
 }
 

@@ -42,14 +42,31 @@ DropDev make_drop(const DropKey& k) {
   d.key = mix(k.seed ^ 0xD6E8FEB86659FD93ULL ^ (static_cast<uint64_t>(static_cast<uint32_t>(k.step)) << 40) ^
               (static_cast<uint64_t>(static_cast<uint32_t>(k.layer & 0xFFFF)) << 16) ^
               static_cast<uint64_t>(static_cast<uint32_t>(k.site)));
-  d.thr = static_cast<uint32_t>(static_cast<double>(k.p) * 16777216.0);
+  d.thr = static_cast<uint32_t>(static_cast<double>(k.p) * 65536.0);
   d.scale = static_cast<float>(1.0 / (1.0 - static_cast<double>(k.p)));
   d.base = k.elem_base;
   return d;
 }
 
+// Dropout decision of one element: one 64-bit hash per 4 consecutive global elements, element e
+// uses the 16-bit field (e % 4) (restated in oracle/gpt_oracle.c orc_dropout_keep).
 __device__ __forceinline__ bool keep(const DropDev& d, int64_t elem) {
-  return static_cast<uint32_t>(mix64(d.key + static_cast<uint64_t>(d.base + elem)) >> 40) >= d.thr;
+  const uint64_t e = static_cast<uint64_t>(d.base + elem);
+  return static_cast<uint32_t>((mix64(d.key + (e >> 2)) >> (16 * (e & 3))) & 0xFFFFu) >= d.thr;
+}
+
+// Keep bits of 8 consecutive elements starting at `elem` (global index a multiple of 4): 2 hashes.
+__device__ __forceinline__ uint32_t keep8(const DropDev& d, int64_t elem) {
+  const uint64_t e = static_cast<uint64_t>(d.base + elem);
+  uint32_t bits = 0;
+#pragma unroll
+  for (int hgrp = 0; hgrp < 2; ++hgrp) {
+    const uint64_t h = mix64(d.key + ((e >> 2) + hgrp));
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      bits |= (static_cast<uint32_t>((h >> (16 * i)) & 0xFFFFu) >= d.thr ? 1u : 0u) << (4 * hgrp + i);
+  }
+  return bits;
 }
 
 __device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
@@ -131,8 +148,9 @@ __global__ void resid_ln_kernel(ResidLnArgs a, DropDev dr) {
         }
       }
       if (dr.on) {
+        const uint32_t kb = keep8(dr, static_cast<int64_t>(roff) + c0);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) y[i] = keep(dr, static_cast<int64_t>(roff) + c0 + i) ? y[i] * dr.scale : 0.f;
+        for (int i = 0; i < 8; ++i) y[i] = (kb >> i) & 1u ? y[i] * dr.scale : 0.f;
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) h[v][i] = round_bf16(r[i] + y[i]);
@@ -176,95 +194,162 @@ __global__ void resid_ln_kernel(ResidLnArgs a, DropDev dr) {
   }
 }
 
-// ---------------------------------------------------------------- LN backward (+residual, dropout')
-constexpr int kLnBwdRows = 64;
-
-template <int VPT>
-__global__ void ln_bwd_kernel(LnBwdArgs a, DropDev dr) {
-  __shared__ float red[64];
+// Warp-per-row variant for d <= 4096 (d % 256 == 0): lane owns VPL 16-byte vectors at columns
+// (v*32 + lane)*8; both row reductions are warp shuffles (no block barriers).
+template <int VPL>
+__global__ void __launch_bounds__(256, 2) resid_ln_warp_kernel(ResidLnArgs a, DropDev dr) {
+  const int row = blockIdx.x * 8 + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= a.rows) return;
   const int d = a.d;
-  const int r0 = blockIdx.x * kLnBwdRows;
-  const int r1 = min(r0 + kLnBwdRows, a.rows);
-  float pg[VPT][8], pb[VPT][8], pbias[VPT][8], gam[VPT][8];
+  const size_t roff = static_cast<size_t>(row) * d;
+  const bf16* rsrc = a.resid_pos_table ? a.resid + static_cast<size_t>(row % a.seq) * d : a.resid + roff;
+  uint4 hp[VPL], yv[VPL];  // all row loads in flight first; hp then holds the new residual (bf16)
 #pragma unroll
-  for (int v = 0; v < VPT; ++v)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) pg[v][i] = pb[v][i] = pbias[v][i] = 0.f;
-  if (a.dy) {
-#pragma unroll
-    for (int v = 0; v < VPT; ++v)
-      unpack8(*reinterpret_cast<const uint4*>(a.gamma + (v * blockDim.x + threadIdx.x) * 8), gam[v]);
+  for (int v = 0; v < VPL; ++v) {
+    const int c0 = (v * 32 + lane) * 8;
+    hp[v] = *reinterpret_cast<const uint4*>(rsrc + c0);
+    if (a.y) yv[v] = *reinterpret_cast<const uint4*>(a.y + roff + c0);
   }
-  for (int row = r0; row < r1; ++row) {
-    const size_t roff = static_cast<size_t>(row) * d;
-    float dx[VPT][8];
-    if (a.dy) {
-      const float mu = a.mean[row], rs = a.rstd[row];
-      float xh[VPT][8], gy[VPT][8];
-      float s[2] = {0.f, 0.f};
+  float sum = 0.f;
 #pragma unroll
-      for (int v = 0; v < VPT; ++v) {
-        const int c0 = (v * blockDim.x + threadIdx.x) * 8;
-        float x[8], dy[8];
-        unpack8(*reinterpret_cast<const uint4*>(a.x + roff + c0), x);
-        unpack8(*reinterpret_cast<const uint4*>(a.dy + roff + c0), dy);
+  for (int v = 0; v < VPL; ++v) {
+    const int c0 = (v * 32 + lane) * 8;
+    if (a.y) {
+      float r[8], y[8];
+      unpack8(hp[v], r);
+      unpack8(yv[v], y);
+      if (a.bias) {
+        float b[8];
+        unpack8(*reinterpret_cast<const uint4*>(a.bias + c0), b);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[i] += b[i];
+      }
+      if (a.resid_pos_table) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          xh[v][i] = (x[i] - mu) * rs;
-          gy[v][i] = dy[i] * gam[v][i];
-          s[0] += gy[v][i];
-          s[1] += gy[v][i] * xh[v][i];
-          pg[v][i] += dy[i] * xh[v][i];
-          pb[v][i] += dy[i];
+          y[i] += r[i];
+          r[i] = 0.f;
         }
       }
-      block_sum<2>(s, red);
-      const float m1 = s[0] / d, m2 = s[1] / d;
+      if (dr.on) {
+        const uint32_t kb = keep8(dr, static_cast<int64_t>(roff) + c0);
 #pragma unroll
-      for (int v = 0; v < VPT; ++v)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) dx[v][i] = rs * (gy[v][i] - m1 - xh[v][i] * m2);
-    } else {
-#pragma unroll
-      for (int v = 0; v < VPT; ++v)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) dx[v][i] = 0.f;
-    }
-#pragma unroll
-    for (int v = 0; v < VPT; ++v) {
-      const int c0 = (v * blockDim.x + threadIdx.x) * 8;
-      if (a.resid_grad) {
-        float r[8];
-        unpack8(*reinterpret_cast<const uint4*>(a.resid_grad + roff + c0), r);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) dx[v][i] += r[i];
+        for (int i = 0; i < 8; ++i) y[i] = (kb >> i) & 1u ? y[i] * dr.scale : 0.f;
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) dx[v][i] = round_bf16(dx[v][i]);
-      if (a.dx) *reinterpret_cast<uint4*>(a.dx + roff + c0) = pack8(dx[v]);
-      if (a.dxd || a.dbias) {
-        float o[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          o[i] = dx[v][i];
-          if (dr.on) o[i] = keep(dr, static_cast<int64_t>(roff) + c0 + i) ? o[i] * dr.scale : 0.f;
-          o[i] = round_bf16(o[i]);
-          pbias[v][i] += o[i];
-        }
-        if (a.dxd && (dr.on || a.dxd != a.dx)) *reinterpret_cast<uint4*>(a.dxd + roff + c0) = pack8(o);
-      }
+      for (int i = 0; i < 8; ++i) r[i] += y[i];
+      hp[v] = pack8(r);
+      if (a.h_out) *reinterpret_cast<uint4*>(a.h_out + roff + c0) = hp[v];
     }
+    float h[8];
+    unpack8(hp[v], h);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sum += h[i];
   }
-  // per-block column partials: workspace[block][3][d]
-  float* w = a.workspace + static_cast<size_t>(blockIdx.x) * 3 * d;
+  if (!a.gamma) return;
+  for (int off = 16; off; off >>= 1) sum += __shfl_xor_sync(0xffffffff, sum, off);
+  const float mean = sum / d;
+  float q = 0.f;
 #pragma unroll
-  for (int v = 0; v < VPT; ++v) {
-    const int c0 = (v * blockDim.x + threadIdx.x) * 8;
+  for (int v = 0; v < VPL; ++v) {
+    float h[8];
+    unpack8(hp[v], h);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      w[c0 + i] = pg[v][i];
-      w[d + c0 + i] = pb[v][i];
-      w[2 * d + c0 + i] = pbias[v][i];
+      const float t = h[i] - mean;
+      q += t * t;
+    }
+  }
+  for (int off = 16; off; off >>= 1) q += __shfl_xor_sync(0xffffffff, q, off);
+  const float rstd = rsqrtf(q / d + 1e-5f);
+  if (lane == 0) {
+    a.mean[row] = mean;
+    a.rstd[row] = rstd;
+  }
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    const int c0 = (v * 32 + lane) * 8;
+    float h[8], g[8], b[8], o[8];
+    unpack8(hp[v], h);
+    unpack8(*reinterpret_cast<const uint4*>(a.gamma + c0), g);
+    unpack8(*reinterpret_cast<const uint4*>(a.beta + c0), b);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = (h[i] - mean) * rstd * g[i] + b[i];
+    *reinterpret_cast<uint4*>(a.ln_out + roff + c0) = pack8(o);
+  }
+}
+
+// ---------------------------------------------------------------- LN backward (+residual, dropout')
+
+// Phase A, rows of d <= 4096: one warp per row, shuffle-only reductions (no block barriers).
+template <int VPL>
+__global__ void __launch_bounds__(256, 4) ln_bwd_warp_kernel(LnBwdArgs a, DropDev dr) {
+  const int row = blockIdx.x * 8 + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= a.rows) return;
+  const int d = a.d;
+  const size_t roff = static_cast<size_t>(row) * d;
+  float m1 = 0.f, m2 = 0.f, mu = 0.f, rs = 0.f;
+  if (a.dy) {  // pass 1: the two row sums (x, dy re-read in pass 2 hit L1/L2)
+    mu = a.mean[row];
+    rs = a.rstd[row];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      const int c0 = (v * 32 + lane) * 8;
+      float x[8], dy[8], g[8];
+      unpack8(*reinterpret_cast<const uint4*>(a.x + roff + c0), x);
+      unpack8(*reinterpret_cast<const uint4*>(a.dy + roff + c0), dy);
+      unpack8(*reinterpret_cast<const uint4*>(a.gamma + c0), g);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float gy = dy[i] * g[i];
+        s1 += gy;
+        s2 += gy * (x[i] - mu) * rs;
+      }
+    }
+    for (int off = 16; off; off >>= 1) {
+      s1 += __shfl_xor_sync(0xffffffff, s1, off);
+      s2 += __shfl_xor_sync(0xffffffff, s2, off);
+    }
+    m1 = s1 / d;
+    m2 = s2 / d;
+  }
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    const int c0 = (v * 32 + lane) * 8;
+    float dx[8];
+    if (a.dy) {
+      float x[8], dy[8], g[8];
+      unpack8(*reinterpret_cast<const uint4*>(a.x + roff + c0), x);
+      unpack8(*reinterpret_cast<const uint4*>(a.dy + roff + c0), dy);
+      unpack8(*reinterpret_cast<const uint4*>(a.gamma + c0), g);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dx[i] = rs * (dy[i] * g[i] - m1 - (x[i] - mu) * rs * m2);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dx[i] = 0.f;
+    }
+    if (a.resid_grad) {
+      float r[8];
+      unpack8(*reinterpret_cast<const uint4*>(a.resid_grad + roff + c0), r);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dx[i] += r[i];
+    }
+    const uint4 dxp = pack8(dx);
+    if (a.dx) *reinterpret_cast<uint4*>(a.dx + roff + c0) = dxp;
+    if (a.dxd && (dr.on || a.dxd != a.dx)) {
+      uint4 op = dxp;
+      if (dr.on) {
+        float o[8];
+        unpack8(dxp, o);
+        const uint32_t kb = keep8(dr, static_cast<int64_t>(roff) + c0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = (kb >> i) & 1u ? o[i] * dr.scale : 0.f;
+        op = pack8(o);
+      }
+      *reinterpret_cast<uint4*>(a.dxd + roff + c0) = op;
     }
   }
 }
@@ -327,63 +412,88 @@ __global__ void ln_bwd_rows_kernel(LnBwdArgs a, DropDev dr) {
     if (a.dxd && (dr.on || a.dxd != a.dx)) {
       float o[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        o[i] = dr.on ? (keep(dr, static_cast<int64_t>(roff) + c0 + i) ? dx[v][i] * dr.scale : 0.f) : dx[v][i];
+      const uint32_t kb = dr.on ? keep8(dr, static_cast<int64_t>(roff) + c0) : 0xFFu;
+      for (int i = 0; i < 8; ++i) o[i] = dr.on ? ((kb >> i) & 1u ? dx[v][i] * dr.scale : 0.f) : dx[v][i];
       *reinterpret_cast<uint4*>(a.dxd + roff + c0) = pack8(o);
     }
   }
 }
 
-constexpr int kLnColRows = 128;
+constexpr int kLnColRows = 64;
 
-// Column sums for the wide path: partial[chunk][3][d] of (dy*xhat, dy, dxd). `dxd_src` is the
-// tensor phase A wrote (dxd, or dx when dropout is off).
-__global__ void ln_bwd_cols_kernel(LnBwdArgs a, const bf16* __restrict__ dxd_src, float* __restrict__ ws) {
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+// Phase B: column sums over 64-row chunks of (dy*xhat, dy, dxd); one thread = 8 columns,
+// 4 rows in flight per iteration. partial[chunk][3][d].
+__global__ void __launch_bounds__(256) ln_bwd_cols_kernel(LnBwdArgs a, const bf16* __restrict__ dxd_src,
+                                                          float* __restrict__ ws) {
+  const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   const int d = a.d;
-  if (c >= d) return;
+  if (c0 >= d) return;
   const int r0 = blockIdx.y * kLnColRows, r1 = min(r0 + kLnColRows, a.rows);
-  float g0 = 0.f, g1 = 0.f, b0 = 0.f, b1 = 0.f, s0 = 0.f, s1 = 0.f;
+  float g[8], bb[8], sb[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) g[i] = bb[i] = sb[i] = 0.f;
+#pragma unroll 4
   for (int r = r0; r < r1; ++r) {
-    const size_t o = static_cast<size_t>(r) * d + c;
+    const size_t o = static_cast<size_t>(r) * d + c0;
     if (a.dy) {
       const float mu = a.mean[r], rs = a.rstd[r];
-      const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a.x + o));
-      const float2 dy = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a.dy + o));
-      g0 += dy.x * (x.x - mu) * rs;
-      g1 += dy.y * (x.y - mu) * rs;
-      b0 += dy.x;
-      b1 += dy.y;
+      float x[8], dy[8];
+      unpack8(*reinterpret_cast<const uint4*>(a.x + o), x);
+      unpack8(*reinterpret_cast<const uint4*>(a.dy + o), dy);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        g[i] += dy[i] * (x[i] - mu) * rs;
+        bb[i] += dy[i];
+      }
     }
     if (dxd_src) {
-      const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dxd_src + o));
-      s0 += v.x;
-      s1 += v.y;
+      float v[8];
+      unpack8(*reinterpret_cast<const uint4*>(dxd_src + o), v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sb[i] += v[i];
     }
   }
   float* w = ws + static_cast<size_t>(blockIdx.y) * 3 * d;
-  w[c] = g0;
-  w[c + 1] = g1;
-  w[d + c] = b0;
-  w[d + c + 1] = b1;
-  w[2 * d + c] = s0;
-  w[2 * d + c + 1] = s1;
+  *reinterpret_cast<float4*>(w + c0) = make_float4(g[0], g[1], g[2], g[3]);
+  *reinterpret_cast<float4*>(w + c0 + 4) = make_float4(g[4], g[5], g[6], g[7]);
+  *reinterpret_cast<float4*>(w + d + c0) = make_float4(bb[0], bb[1], bb[2], bb[3]);
+  *reinterpret_cast<float4*>(w + d + c0 + 4) = make_float4(bb[4], bb[5], bb[6], bb[7]);
+  *reinterpret_cast<float4*>(w + 2 * d + c0) = make_float4(sb[0], sb[1], sb[2], sb[3]);
+  *reinterpret_cast<float4*>(w + 2 * d + c0 + 4) = make_float4(sb[4], sb[5], sb[6], sb[7]);
 }
 
+// out_k[c] += sum_b ws[b*stride + k*n + c] for k = 0..2 (outputs may be null). Block (32, 8):
+// 32 consecutive columns x 8 partial-row lanes, fixed summation order (deterministic).
 __global__ void reduce_partials_kernel(const float* __restrict__ ws, int nblocks, int stride, int n,
                                        float* out0, float* out1, float* out2) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
+  __shared__ float red[3][8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + tx;
   float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-  for (int b = 0; b < nblocks; ++b) {
-    const float* w = ws + static_cast<size_t>(b) * stride;
-    s0 += w[c];
-    if (out1) s1 += w[n + c];
-    if (out2) s2 += w[2 * n + c];
+  if (c < n) {
+    for (int b = ty; b < nblocks; b += 8) {
+      const float* w = ws + static_cast<size_t>(b) * stride;
+      s0 += w[c];
+      if (out1) s1 += w[n + c];
+      if (out2) s2 += w[2 * n + c];
+    }
   }
-  if (out0) out0[c] += s0;
-  if (out1) out1[c] += s1;
-  if (out2) out2[c] += s2;
+  red[0][ty][tx] = s0;
+  red[1][ty][tx] = s1;
+  red[2][ty][tx] = s2;
+  __syncthreads();
+  if (ty == 0 && c < n) {
+    float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      t0 += red[0][k][tx];
+      t1 += red[1][k][tx];
+      t2 += red[2][k][tx];
+    }
+    if (out0) out0[c] += t0;
+    if (out1) out1[c] += t1;
+    if (out2) out2[c] += t2;
+  }
 }
 
 // ---------------------------------------------------------------- column sums
@@ -615,9 +725,20 @@ int status() { return cudaGetLastError() == cudaSuccess ? 0 : 3; }
 int resid_ln_fwd(const ResidLnArgs& a, cudaStream_t st) {
   const int vpt = pick_vpt(a.d);
   if (vpt == 0 || a.rows <= 0) return 1;
+  if (a.drop.p > 0.f && a.drop.elem_base % 8 != 0) return 1;  // keep8 works on 8-aligned groups
   if (a.gamma && (!a.ln_out || !a.mean || !a.rstd)) return 1;
   const int threads = a.d / 8 / vpt;
   const DropDev dr = make_drop(a.drop);
+  if (a.d % 256 == 0 && a.d <= 4096) {
+    const int blocks = (a.rows + 7) / 8;
+    switch (a.d / 256) {
+#define WCASE(V) case V: resid_ln_warp_kernel<V><<<blocks, 256, 0, st>>>(a, dr); return status();
+      WCASE(1) WCASE(2) WCASE(3) WCASE(4) WCASE(5) WCASE(6) WCASE(7) WCASE(8)
+      WCASE(9) WCASE(10) WCASE(11) WCASE(12) WCASE(13) WCASE(14) WCASE(15) WCASE(16)
+#undef WCASE
+      default: break;
+    }
+  }
   switch (vpt) {
 #define CASE(V) case V: resid_ln_kernel<V><<<a.rows, threads, 0, st>>>(a, dr); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
@@ -628,48 +749,52 @@ int resid_ln_fwd(const ResidLnArgs& a, cudaStream_t st) {
 }
 
 size_t ln_bwd_workspace_floats(int rows, int d) {
-  const size_t fused = static_cast<size_t>((rows + kLnBwdRows - 1) / kLnBwdRows) * 3 * d;
-  const size_t wide = static_cast<size_t>((rows + kLnColRows - 1) / kLnColRows) * 3 * d;
-  return fused > wide ? fused : wide;
+  return static_cast<size_t>((rows + kLnColRows - 1) / kLnColRows) * 3 * d;
 }
-
-static bool ln_bwd_fused_ok(int d) { return d <= 8192 && pick_vpt(d) == 1; }
 
 int ln_bwd(const LnBwdArgs& a, cudaStream_t st) {
   const int vpt = pick_vpt(a.d);
   if (vpt == 0 || a.rows <= 0 || !a.workspace) return 1;
   if (a.drop.p > 0.f && a.dxd != nullptr && a.dxd == a.dx) return 1;  // would clobber dx
+  if (a.drop.p > 0.f && a.drop.elem_base % 8 != 0) return 1;
   if (a.dy && (!a.gamma || !a.mean || !a.rstd || !a.x)) return 1;
-  const int threads = a.d / 8 / vpt;
   const DropDev dr = make_drop(a.drop);
-  const bool any = a.dgamma || a.dbeta || a.dbias;
-  if (!ln_bwd_fused_ok(a.d)) {
-    switch (vpt) {
+  // phase A: dx (+ dropout'(dx)) per row
+  if (a.dx || a.dxd) {
+    if (a.d % 256 == 0 && a.d <= 4096) {
+      const int blocks = (a.rows + 7) / 8;
+      switch (a.d / 256) {
+#define WCASE(V) case V: ln_bwd_warp_kernel<V><<<blocks, 256, 0, st>>>(a, dr); break;
+        WCASE(1) WCASE(2) WCASE(3) WCASE(4) WCASE(5) WCASE(6) WCASE(7) WCASE(8)
+        WCASE(9) WCASE(10) WCASE(11) WCASE(12) WCASE(13) WCASE(14) WCASE(15) WCASE(16)
+#undef WCASE
+        default: return 1;
+      }
+    } else {
+      const int threads = a.d / 8 / vpt;
+      switch (vpt) {
 #define CASE(V) case V: ln_bwd_rows_kernel<V><<<a.rows, threads, 0, st>>>(a, dr); break;
-      CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
-      default: return 1;
+        default: return 1;
+      }
     }
-    if (any) {
-      const bf16* src = nullptr;
-      if (a.dbias) src = a.dxd ? a.dxd : (a.dx ? a.dx : (!a.dy && !dr.on ? a.resid_grad : nullptr));
-      if (a.dbias && !src) return 1;
-      const int chunks = (a.rows + kLnColRows - 1) / kLnColRows;
-      dim3 grid((a.d / 2 + 255) / 256, chunks);
-      ln_bwd_cols_kernel<<<grid, 256, 0, st>>>(a, src, a.workspace);
-      reduce_partials_kernel<<<(a.d + 255) / 256, 256, 0, st>>>(a.workspace, chunks, 3 * a.d, a.d,
-                                                                  a.dy ? a.dgamma : nullptr,
-                                                                  a.dy ? a.dbeta : nullptr, a.dbias);
-    }
-    return status();
   }
-  const int blocks = (a.rows + kLnBwdRows - 1) / kLnBwdRows;
-  ln_bwd_kernel<1><<<blocks, threads, 0, st>>>(a, dr);
+  // phase B: column sums
+  const bool any = (a.dy && (a.dgamma || a.dbeta)) || a.dbias;
   if (any) {
-    // order of outputs in the workspace: dgamma, dbeta, dbias
-    reduce_partials_kernel<<<(a.d + 255) / 256, 256, 0, st>>>(a.workspace, blocks, 3 * a.d, a.d,
-                                                                a.dy ? a.dgamma : nullptr,
-                                                                a.dy ? a.dbeta : nullptr, a.dbias);
+    const bf16* src = nullptr;
+    if (a.dbias) {
+      src = a.dxd ? a.dxd : (a.dx ? a.dx : nullptr);
+      if (!src && !a.dy && !dr.on) src = a.resid_grad;  // no LN, no dropout: dxd == resid_grad
+      if (!src) return 1;
+    }
+    const int chunks = (a.rows + kLnColRows - 1) / kLnColRows;
+    dim3 grid((a.d / 8 + 255) / 256, chunks);
+    ln_bwd_cols_kernel<<<grid, 256, 0, st>>>(a, src, a.workspace);
+    reduce_partials_kernel<<<(a.d + 31) / 32, 256, 0, st>>>(a.workspace, chunks, 3 * a.d, a.d,
+                                                              a.dy ? a.dgamma : nullptr, a.dy ? a.dbeta : nullptr,
+                                                              a.dbias);
   }
   return status();
 }
@@ -683,7 +808,7 @@ int colsum_bf16(const bf16* X, int rows, int n, float* out, float* ws, cudaStrea
   const int splits = (rows + kColsumRows - 1) / kColsumRows;
   dim3 grid((n / 2 + 255) / 256, splits);
   colsum_kernel<<<grid, 256, 0, st>>>(X, rows, n, ws);
-  reduce_partials_kernel<<<(n + 255) / 256, 256, 0, st>>>(ws, splits, n, n, out, nullptr, nullptr);
+  reduce_partials_kernel<<<(n + 31) / 32, 256, 0, st>>>(ws, splits, n, n, out, nullptr, nullptr);
   return status();
 }
 

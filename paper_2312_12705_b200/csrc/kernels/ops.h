@@ -13,7 +13,8 @@ using bf16 = __nv_bfloat16;
 
 // Dropout site key. Element e of an activation [rows, d] has global index
 // elem_base + row * d + col; kept iff hash(key, global index) >= p * 2^24 (oracle/gpt_oracle.c
-// orc_dropout_keep restates the same hash). p == 0 disables dropout.
+// orc_dropout_keep restates the same hash). p == 0 disables dropout. elem_base % 8 == 0 and
+// d % 8 == 0 are required (decisions are drawn 4 per 64-bit hash).
 struct DropKey {
   uint64_t seed = 0;
   int step = 0;

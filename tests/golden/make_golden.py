@@ -44,14 +44,17 @@ def init_values(seed: int, tid: int, n: int, std: float) -> np.ndarray:
 
 
 def dropout_keep(seed: int, step: int, layer: int, site: int, elems: np.ndarray, p: float) -> np.ndarray:
+    """One 64-bit hash per 4 consecutive elements; element e keeps iff its 16-bit field >= p*2^16."""
     if p <= 0:
         return np.ones(elems.shape, dtype=bool)
     with np.errstate(over="ignore"):
         key = np.uint64(seed) ^ np.uint64(0xD6E8FEB86659FD93) ^ np.uint64(step << 40) ^ \
             np.uint64((layer & 0xFFFF) << 16) ^ np.uint64(site)
         key = mix64(np.array([key], dtype=np.uint64))[0]
-        r = (mix64(key + elems.astype(np.uint64)) >> np.uint64(40)).astype(np.uint32)
-    return r >= np.uint32(int(p * 16777216.0))
+        e = elems.astype(np.uint64)
+        h = mix64(key + (e >> np.uint64(2)))
+        r = ((h >> (np.uint64(16) * (e & np.uint64(3)))) & np.uint64(0xFFFF)).astype(np.uint32)
+    return r >= np.uint32(int(p * 65536.0))
 
 
 def mt19937_64_tokens(seed: int, n: int, vocab: int) -> np.ndarray:
