@@ -85,6 +85,10 @@ int tp_gemm_bf16(int M, int N, int K, const void* A, int lda, int a_mn, const vo
                  int b_mn, void* C, int ldc, int epi, const void* bias, void* C2, const void* aux,
                  int ldaux, int accumulate, void* stream);
 
+/* Test/tuning hook: 0 = automatic GEMM tile choice, 1 = single-CTA 128xN tiles only,
+ * 2 = CTA-pair (cta_group::2) 256x256 tiles whenever M, N are multiples of 256. */
+int tp_gemm_force_cta_group(int cg);
+
 /* ------------------------------------------------------------------ K5/K6 flash attention
  * Causal; qkv[b*s, 3*heads*hd] (q | k | v heads, bf16) -> out[b*s, heads*hd], lse[b, heads, s]
  * (fp32, log2 units). Backward writes dqkv; workspaces D[b*heads*s], dq_acc[b*s*heads*hd] fp32. */

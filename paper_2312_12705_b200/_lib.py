@@ -74,6 +74,7 @@ SIGNATURES: dict[str, tuple] = {
     "tp_pipeline_order": (_i, [_i, _i, _i, _i, _i, C.POINTER(_i), _i, C.POINTER(_i)]),
     "tp_rank_coords": (_i, [_i, _i, _i, _i, C.POINTER(_i)]),
     "tp_gemm_bf16": (_i, [_i, _i, _i, _vp, _i, _i, _vp, _i, _i, _vp, _i, _i, _vp, _vp, _vp, _i, _i, _vp]),
+    "tp_gemm_force_cta_group": (_i, [_i]),
     "tp_flash_attn_fwd": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "tp_flash_attn_bwd": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "tp_resid_layernorm_fwd": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _u64, _i, _i, _i, _f, _i64, _vp]),

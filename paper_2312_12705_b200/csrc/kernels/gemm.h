@@ -36,4 +36,7 @@ struct GemmParams {
 // Requires M % 128 == 0, K % 64 == 0, N % 64 == 0, 16-byte aligned rows.
 int gemm_bf16(const GemmParams& p, cudaStream_t stream);
 
+// Test hook: 0 = automatic tile choice, 1 = single-CTA tiles only, 2 = CTA pairs when divisible.
+void gemm_force_cta_group(int cg);
+
 }  // namespace gptb200

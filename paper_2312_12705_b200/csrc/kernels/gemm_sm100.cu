@@ -29,25 +29,34 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr int kThreads = 192;
 
-template <int BN>
+// CG = 1: one CTA computes a 128 x BN tile.  CG = 2: a CTA pair (cluster of 2) computes a
+// 256 x BN tile with tcgen05.mma.cta_group::2 — each CTA stages 128 rows of A and BN/2 rows of B,
+// halving the per-SM operand traffic through shared memory.
+template <int BN, int CG>
 struct GemmCfg {
   static constexpr int kABytes = kBM * kBK * 2;
-  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kBBytes = (BN / CG) * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (BN == 256) ? 4 : 6;
+  static constexpr int kStages = (kStageBytes <= 32768) ? 6 : 4;
   static constexpr int kTmemCols = 2 * BN;
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
 };
 
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  float t = tanhf(k0 * (x + k1 * x * x * x));
+  const float t = tanh_fast(k0 * (x + k1 * x * x * x));
   return 0.5f * x * (1.f + t);
 }
 
 __device__ __forceinline__ float gelu_tanh_grad(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  float t = tanhf(k0 * (x + k1 * x * x * x));
+  const float t = tanh_fast(k0 * (x + k1 * x * x * x));
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
 }
 
@@ -63,12 +72,14 @@ __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int&
   nb = in_group / gsize;
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+template <int BN, int CG, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, CG>;
   constexpr int kStages = Cfg::kStages;
+  constexpr int kTileM = kBM * CG;   // rows of C per tile (per CTA pair)
+  constexpr int kBN_cta = BN / CG;   // rows of B staged by each CTA
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -80,6 +91,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x / CG;
+  const int num_clusters = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmA);
@@ -90,49 +105,61 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 4);
+      ptx::mbar_init(&tempty[a], 4 * CG);
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (CG == 2)
+      ptx::tmem_alloc_cg2<Cfg::kTmemCols>(tmem_slot);
+    else
+      ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    ptx::cluster_sync();
+  else
+    __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int num_m = p.M / kBM;
+  const int num_m = p.M / kTileM;
   const int num_n = p.N / BN;
   const int num_tiles = num_m * num_n;
   const int kblocks = p.K / kBK;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int mb, nb;
         tile_coords(tile, num_m, num_n, mb, nb);
-        const int m0 = mb * kBM, n0 = nb * BN;
+        const int m0 = mb * kTileM + rank * kBM, n0 = nb * BN + rank * kBN_cta;
         for (int kb = 0; kb < kblocks; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::kStageBytes;
           uint8_t* sb = sa + Cfg::kABytes;
-          ptx::mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], CG * Cfg::kStageBytes);
           const int k0 = kb * kBK;
+          auto load = [&](void* dst, const CUtensorMap* tm, int c0, int c1) {
+            if constexpr (CG == 2)
+              ptx::tma_load_2d_cg2(dst, tm, &full[stage], c0, c1);
+            else
+              ptx::tma_load_2d(dst, tm, &full[stage], c0, c1);
+          };
           if constexpr (A_MN) {
 #pragma unroll
-            for (int c = 0; c < kBM / 64; ++c)
-              ptx::tma_load_2d(sa + c * kBK * 128, &tmA, &full[stage], m0 + 64 * c, k0);
+            for (int c = 0; c < kBM / 64; ++c) load(sa + c * kBK * 128, &tmA, m0 + 64 * c, k0);
           } else {
-            ptx::tma_load_2d(sa, &tmA, &full[stage], k0, m0);
+            load(sa, &tmA, k0, m0);
           }
           if constexpr (B_MN) {
 #pragma unroll
-            for (int c = 0; c < BN / 64; ++c)
-              ptx::tma_load_2d(sb + c * kBK * 128, &tmB, &full[stage], n0 + 64 * c, k0);
+            for (int c = 0; c < kBN_cta / 64; ++c) load(sb + c * kBK * 128, &tmB, n0 + 64 * c, k0);
           } else {
-            ptx::tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+            load(sb, &tmB, k0, n0);
           }
           if (++stage == kStages) {
             stage = 0;
@@ -142,13 +169,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kBM, BN, A_MN, B_MN);
+    // ------------------------------------------------------------ MMA issuer (leader CTA only)
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kTileM, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
         const int acc = it & 1;
         ptx::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
@@ -169,28 +196,37 @@ __global__ void __launch_bounds__(kThreads, 1)
               bdesc = ptx::smem_desc_sw128(sb + k * 2048, kBK * 128, 1024);
             else
               bdesc = ptx::smem_desc_sw128(sb + k * 32, 16, 1024);
-            ptx::mma_bf16_ss(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+            if constexpr (CG == 2)
+              ptx::mma_bf16_ss_cg2(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+            else
+              ptx::mma_bf16_ss(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
           }
-          ptx::mma_commit(&empty[stage]);
+          if constexpr (CG == 2)
+            ptx::mma_commit_cg2(&empty[stage]);
+          else
+            ptx::mma_commit(&empty[stage]);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::mma_commit(&tfull[acc]);
+        if constexpr (CG == 2)
+          ptx::mma_commit_cg2(&tfull[acc]);
+        else
+          ptx::mma_commit(&tfull[acc]);
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue
+    // ------------------------------------------------------------ epilogue (both CTAs)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
       int mb, nb;
       tile_coords(tile, num_m, num_n, mb, nb);
       const int acc = it & 1;
       ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
       ptx::tc_fence_after();
-      const int row = mb * kBM + 32 * q + lane;
+      const int row = mb * kTileM + rank * kBM + 32 * q + lane;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * BN;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
@@ -273,14 +309,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2)
+          ptx::mbar_arrive_cluster(&tempty[acc], 0);  // the leader's MMA thread waits on it
+        else
+          ptx::mbar_arrive(&tempty[acc]);
+      }
     }
   }
 
-  __syncthreads();
+  if constexpr (CG == 2)
+    ptx::cluster_sync();
+  else
+    __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+    if constexpr (CG == 2)
+      ptx::tmem_dealloc_cg2<Cfg::kTmemCols>(tmem_base);
+    else
+      ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
   }
 }
 
@@ -291,10 +338,10 @@ bool make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, 
 
 int num_sms() { return device_sm_count(); }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+template <int BN, int CG, bool A_MN, bool B_MN, int EPI>
 int launch(const GemmParams& p, cudaStream_t stream) {
-  using Cfg = GemmCfg<BN>;
-  auto kern = gemm_sm100_kernel<BN, A_MN, B_MN, EPI>;
+  using Cfg = GemmCfg<BN, CG>;
+  auto kern = gemm_sm100_kernel<BN, CG, A_MN, B_MN, EPI>;
   static bool attr_set = false;  // per instantiation; set once per process (single device)
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -306,45 +353,66 @@ int launch(const GemmParams& p, cudaStream_t stream) {
   bool ok = A_MN ? make_tmap(&ta, p.A, p.M, p.K, p.lda, 64)
                  : make_tmap(&ta, p.A, p.K, p.M, p.lda, kBM);
   ok = ok && (B_MN ? make_tmap(&tb, p.B, p.N, p.K, p.ldb, 64)
-                   : make_tmap(&tb, p.B, p.K, p.N, p.ldb, BN));
+                   : make_tmap(&tb, p.B, p.K, p.N, p.ldb, BN / CG));
   if (!ok) return kGemmErrTmap;
-  const int tiles = (p.M / kBM) * (p.N / BN);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, p);
+  const int tiles = (p.M / (kBM * CG)) * (p.N / BN);
+  const int max_clusters = num_sms() / CG;
+  const int grid = CG * (tiles < max_clusters ? tiles : max_clusters);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, ta, tb, p) != cudaSuccess) return kGemmErrCuda;
   return cudaGetLastError() == cudaSuccess ? kGemmOk : kGemmErrCuda;
 }
 
-template <int BN, int EPI>
+template <int BN, int CG, int EPI>
 int dispatch_major(const GemmParams& p, cudaStream_t s) {
-  if (!p.a_mn && !p.b_mn) return launch<BN, false, false, EPI>(p, s);
-  if (!p.a_mn && p.b_mn) return launch<BN, false, true, EPI>(p, s);
-  if (p.a_mn && p.b_mn) return launch<BN, true, true, EPI>(p, s);
-  return launch<BN, true, false, EPI>(p, s);
+  if (!p.a_mn && !p.b_mn) return launch<BN, CG, false, false, EPI>(p, s);
+  if (!p.a_mn && p.b_mn) return launch<BN, CG, false, true, EPI>(p, s);
+  if (p.a_mn && p.b_mn) return launch<BN, CG, true, true, EPI>(p, s);
+  return launch<BN, CG, true, false, EPI>(p, s);
 }
 
-template <int BN>
+template <int BN, int CG>
 int dispatch_epi(const GemmParams& p, cudaStream_t s) {
   switch (p.epi) {
-    case EPI_BF16: return dispatch_major<BN, EPI_BF16>(p, s);
-    case EPI_BIAS_GELU: return dispatch_major<BN, EPI_BIAS_GELU>(p, s);
-    case EPI_F32: return dispatch_major<BN, EPI_F32>(p, s);
-    case EPI_DGELU: return dispatch_major<BN, EPI_DGELU>(p, s);
+    case EPI_BF16: return dispatch_major<BN, CG, EPI_BF16>(p, s);
+    case EPI_BIAS_GELU: return dispatch_major<BN, CG, EPI_BIAS_GELU>(p, s);
+    case EPI_F32: return dispatch_major<BN, CG, EPI_F32>(p, s);
+    case EPI_DGELU: return dispatch_major<BN, CG, EPI_DGELU>(p, s);
     default: return kGemmErrShape;
   }
 }
 
+int g_force_cg = 0;  // test hook: 1 or 2 forces the CTA-group choice (0 = automatic)
+
 }  // namespace
+
+void gemm_force_cta_group(int cg) { g_force_cg = cg; }
 
 int gemm_bf16(const GemmParams& p, cudaStream_t stream) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0) return kGemmErrShape;
   if (p.M % kBM != 0 || p.K % kBK != 0 || p.N % 64 != 0) return kGemmErrShape;
   if (p.epi == EPI_BIAS_GELU && p.C2 == nullptr) return kGemmErrShape;
   if (p.epi == EPI_DGELU && p.aux == nullptr) return kGemmErrShape;
-  // Prefer the widest N tile that divides N and still yields at least one full wave.
+  // CTA pairs (256 x 256 tiles) when the problem yields at least one full wave of pairs;
+  // otherwise single-CTA 128 x BN tiles with the widest BN that still fills the machine.
+  const bool pair_ok = p.M % 256 == 0 && p.N % 256 == 0;
+  const bool pair_wave = pair_ok && (p.M / 256) * (p.N / 256) >= num_sms() / 2;
+  if (g_force_cg == 2 ? pair_ok : (g_force_cg == 0 && pair_wave)) return dispatch_epi<256, 2>(p, stream);
   const bool n256 = (p.N % 256 == 0) && (p.M / kBM) * (p.N / 256) >= num_sms();
-  if (n256) return dispatch_epi<256>(p, stream);
-  if (p.N % 128 == 0) return dispatch_epi<128>(p, stream);
-  return dispatch_epi<64>(p, stream);
+  if (n256) return dispatch_epi<256, 1>(p, stream);
+  if (p.N % 128 == 0) return dispatch_epi<128, 1>(p, stream);
+  return dispatch_epi<64, 1>(p, stream);
 }
 
 }  // namespace gptb200

@@ -29,9 +29,12 @@ def _gpu(native_lib):
     yield
 
 
+@pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1)])
-@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (256, 384, 192), (2048, 2304, 768), (1024, 51200 // 8, 256)])
-def test_gemm_layouts_vs_torch(a_mn, b_mn, M, N, K):
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (256, 384, 192), (2048, 2304, 768), (1024, 51200 // 8, 256),
+                                   (512, 512, 2048)])
+def test_gemm_layouts_vs_torch(a_mn, b_mn, M, N, K, cg):
+    T.check(T.load().tp_gemm_force_cta_group(cg))
     g = torch.Generator(device=DEV).manual_seed(1)
     A = torch.randn((K, M) if a_mn else (M, K), device=DEV, generator=g).bfloat16()
     B = torch.randn((K, N) if b_mn else (N, K), device=DEV, generator=g).bfloat16()
@@ -40,10 +43,13 @@ def test_gemm_layouts_vs_torch(a_mn, b_mn, M, N, K):
                 stream=_stream())
     ref = (A.t() if a_mn else A).float() @ (B.t() if b_mn else B).float().t()
     torch.cuda.synchronize()
+    T.check(T.load().tp_gemm_force_cta_group(0))
     assert _rel(C.float(), ref) < 5e-3  # bf16 output rounding (2^-9) dominates
 
 
-def test_gemm_fp32_accumulate_epilogue():
+@pytest.mark.parametrize("cg", [1, 2])
+def test_gemm_fp32_accumulate_epilogue(cg):
+    T.check(T.load().tp_gemm_force_cta_group(cg))
     M, N, K = 256, 512, 1024
     A = torch.randn(K, M, device=DEV).bfloat16()
     B = torch.randn(K, N, device=DEV).bfloat16()
@@ -51,6 +57,7 @@ def test_gemm_fp32_accumulate_epilogue():
     C0 = C.clone()
     T.gemm_bf16(M, N, K, A.data_ptr(), M, 1, B.data_ptr(), N, 1, C.data_ptr(), N, epi=2, accumulate=1, stream=_stream())
     torch.cuda.synchronize()
+    T.check(T.load().tp_gemm_force_cta_group(0))
     assert _rel(C, C0 + A.float().t() @ B.float()) < 1e-5  # fp32 out: only summation order differs
 
 

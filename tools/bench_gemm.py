@@ -99,7 +99,9 @@ def run_case(M, N, K, a_mn, b_mn, epi=0, iters=20, check=True):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--cg", type=int, default=0)
     args = ap.parse_args()
+    _lib.check(_lib.load().tp_gemm_force_cta_group(args.cg))
     bad = 0
     small = [(256, 256, 128), (128, 64, 64), (384, 640, 192)]
     for (M, N, K) in small:
