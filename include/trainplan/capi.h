@@ -159,6 +159,10 @@ int tp_session_barrier(tp_session* s);
 int tp_session_tensor_info(tp_session* s, int tensor_id, int64_t info[9]);
 /* which: 0 bf16 working param, 1 fp32 grad of the last step, 2 fp32 master, 3 Adam m, 4 Adam v. */
 int tp_session_read_tensor(tp_session* s, int which, int tensor_id, float* host_out);
+/* Raw read of the rank's flat buffers: which 0 = bf16 params [P], 1 = fp32 grads [P] (after a step
+ * only this rank's ZeRO shard [d*P/dp, (d+1)*P/dp) holds DP-reduced values), 2/3/4 = fp32 master /
+ * Adam m / Adam v shard [P/dp]. offset and n in elements of that buffer. */
+int tp_session_read_flat(tp_session* s, int which, int64_t offset, int64_t n, float* host_out);
 /* out = {flat_params, shard_params, device_bytes, microbatches, launches_last_step, rank, world, 0} */
 int tp_session_info(tp_session* s, int64_t out[8]);
 

@@ -98,6 +98,7 @@ SIGNATURES: dict[str, tuple] = {
     "tp_session_tensor_info": (_i, [_vp, _i, C.POINTER(_i64)]),
     "tp_session_read_tensor": (_i, [_vp, _i, _i, _vp]),
     "tp_session_info": (_i, [_vp, C.POINTER(_i64)]),
+    "tp_session_read_flat": (_i, [_vp, _i, _i64, _i64, _vp]),
     "tp_session_time_steps": (_i, [_vp, _i, _i, C.POINTER(_f), C.POINTER(KernelTimes)]),
     "tp_session_allreduce_max": (_i, [_vp, C.POINTER(_f)]),
 }
@@ -278,6 +279,12 @@ class Session:
         x = _f(v)
         check(self._lib.tp_session_allreduce_max(self.h, C.byref(x)))
         return x.value
+
+    def read_flat(self, which: int, offset: int, n: int):
+        import numpy as np
+        out = np.empty(n, dtype=np.float32)
+        check(self._lib.tp_session_read_flat(self.h, which, offset, n, out.ctypes.data))
+        return out
 
     def info(self) -> dict:
         out = (_i64 * 8)()

@@ -147,6 +147,10 @@ int tp_session_read_tensor(tp_session* s, int which, int tensor_id, float* host_
   return run("tp_session_read_tensor", [&] { s->stage->read_tensor(which, tensor_id, host_out); });
 }
 
+int tp_session_read_flat(tp_session* s, int which, int64_t offset, int64_t n, float* host_out) {
+  return run("tp_session_read_flat", [&] { s->stage->read_flat(which, offset, n, host_out); });
+}
+
 int tp_session_info(tp_session* s, int64_t out[8]) {
   return run("tp_session_info", [&] {
     out[0] = s->stage->flat_params();

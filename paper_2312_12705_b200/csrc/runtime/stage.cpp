@@ -693,6 +693,23 @@ void Stage::barrier() {
   sync();
 }
 
+void Stage::read_flat(int which, int64_t offset, int64_t n, float* host) const {
+  const int64_t len = (which <= 1) ? P_ : shard_;
+  if (offset < 0 || n < 0 || offset + n > len) throw StepError{TP_ERR_INVALID, "read_flat: range out of bounds"};
+  cudaStreamSynchronize(st_);
+  if (which == 0) {
+    std::vector<uint16_t> tmp(n);
+    cudaMemcpy(tmp.data(), params_ + offset, n * 2, cudaMemcpyDeviceToHost);
+    for (int64_t i = 0; i < n; ++i) {
+      uint32_t u = static_cast<uint32_t>(tmp[i]) << 16;
+      std::memcpy(&host[i], &u, 4);
+    }
+    return;
+  }
+  const float* base = which == 1 ? grads_ : which == 2 ? master_ : which == 3 ? adam_m_ : adam_v_;
+  cudaMemcpy(host, base + offset, n * 4, cudaMemcpyDeviceToHost);
+}
+
 void Stage::read_tensor(int which, int tid, float* host) const {
   const ParamSlot* s = slot(tid);
   if (!s) throw StepError{TP_ERR_INVALID, "tensor " + std::to_string(tid) + " not on this rank"};

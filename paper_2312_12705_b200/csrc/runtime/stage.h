@@ -79,6 +79,7 @@ class Stage {
   // which: 0 = working bf16 param, 1 = fp32 grad (accumulated this step), 2 = fp32 master
   // (dp must be 1 or the tensor must lie in this rank's ZeRO shard), 3 = Adam m, 4 = Adam v.
   void read_tensor(int which, int tensor_id, float* host) const;
+  void read_flat(int which, int64_t offset, int64_t n, float* host) const;
   // Forward-only loss of the uploaded batch with the current parameters (no update).
   float eval_loss();
 
