@@ -6,11 +6,14 @@ shared object is missing or does not export every symbol the header declares.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import re
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "lib" / "libtrainplan_b200.so"
+if os.environ.get("GPTB200_LIB"):  # debugging aid: load an alternative build of the same library
+    LIB_PATH = Path(os.environ["GPTB200_LIB"])
 HEADER = PKG.parent / "include" / "trainplan" / "capi.h"
 
 _vp, _i, _f, _u64 = C.c_void_p, C.c_int, C.c_float, C.c_uint64

@@ -22,13 +22,14 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
           f"-I{ROOT / 'include'}", f"-I{CSRC}", "-I/usr/local/cuda/include"]
-# NCCL is linked statically with its symbols hidden: the library carries its own NCCL and cannot
-# clash with (or be interposed by) another NCCL already loaded in the process, e.g. torch's.
-NCCL_STATIC = Path("/usr/lib/x86_64-linux-gnu/libnccl_static.a")
-NCCL_PRUNED = BUILD / "libnccl_static_sm100.a"  # device code pruned to sm_100 (nvprune)
-LINK = ["-shared", "-lcudart", str(NCCL_PRUNED), "-lgomp", "-lrt", "-lpthread", "-ldl",
-        "-Xlinker", "--exclude-libs,libnccl_static_sm100.a", "-Xlinker", "-Bsymbolic",
-        "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+# NCCL: link the libnccl.so.2 that the image's PyTorch bundles (rpath'd), so a process that loads
+# both this library and torch — in either order — holds exactly one NCCL (same SONAME).
+# Fallback: the system libnccl.so.2.
+_TORCH_NCCL = Path(sys.prefix) / "lib" / f"python{sys.version_info.major}.{sys.version_info.minor}" / \
+    "site-packages" / "nvidia" / "nccl" / "lib"
+NCCL_DIR = _TORCH_NCCL if (_TORCH_NCCL / "libnccl.so.2").exists() else Path("/usr/lib/x86_64-linux-gnu")
+LINK = ["-shared", "-lcudart", f"-L{NCCL_DIR}", "-l:libnccl.so.2", "-lgomp",
+        "-Xlinker", f"-rpath={NCCL_DIR}", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
 
 
 def _sources() -> list[Path]:
@@ -60,9 +61,6 @@ def build(verbose: bool = False) -> Path:
     srcs = _sources()
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         objs = list(ex.map(lambda s: _compile(s, hdr), srcs))
-    if not NCCL_PRUNED.exists():
-        nvprune = str(Path(NVCC).with_name("nvprune"))
-        subprocess.run([nvprune, "-arch", "sm_100", str(NCCL_STATIC), "-o", str(NCCL_PRUNED)], check=True)
     newest = max(o.stat().st_mtime for o in objs)
     if not LIB.exists() or LIB.stat().st_mtime < newest:
         cmd = [NVCC, *ARCH, *[str(o) for o in objs], "-o", str(LIB), *LINK]
