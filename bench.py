@@ -38,9 +38,21 @@ NOMINAL_PEAK_TFLOPS = 2250.0
 FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}
 
 WORKLOADS = {
-    # name: (L, d, heads, V, s, mbs, tp, pp, ckpt, dropout)
-    "gpt-1.4b": (24, 2048, 16, 51200, 2048, 8, 1, 1, False, 0.1),
-    "gpt-tiny": (2, 256, 4, 51200, 128, 1, 1, 1, False, 0.0),
+    # name: (L, d, heads, V, s, mbs, tp, pp, ckpt, dropout, microbatches per DP replica)
+    # BASELINE config 2 (headline): 1.4B on 1 GPU, DP = N with ZeRO-1 beyond.
+    "gpt-1.4b": (24, 2048, 16, 51200, 2048, 8, 1, 1, False, 0.1, 1),
+    # BASELINE config 1 shape (tiny GPT) — smoke-sized.
+    "gpt-tiny": (2, 256, 4, 51200, 128, 1, 1, 1, False, 0.0, 1),
+    # BASELINE config 3: 22B shape with TP = 2/4/8 and activation checkpointing, MBS 1, m = 8.
+    "gpt-22b-tp2": (48, 6144, 48, 51200, 2048, 1, 2, 1, True, 0.1, 8),
+    "gpt-22b-tp4": (48, 6144, 48, 51200, 2048, 1, 4, 1, True, 0.1, 8),
+    "gpt-22b-tp8": (48, 6144, 48, 51200, 2048, 1, 8, 1, True, 0.1, 8),
+    # BASELINE config 4: 175B-shape layer slice (8 layers) TP4 x PP2 1F1B, m = 16, checkpointing.
+    "gpt-175b-slice-tp4pp2": (8, 12288, 96, 51200, 2048, 1, 4, 2, True, 0.1, 16),
+    "gpt-175b-slice-tp4": (4, 12288, 96, 51200, 2048, 1, 4, 1, True, 0.1, 8),
+    # BASELINE config 5: 1T-shape layer slice (4 layers, 160 heads, hd 160) TP8 / TP4 x PP2.
+    "gpt-1t-slice-tp8": (4, 25600, 160, 51200, 2048, 1, 8, 1, True, 0.1, 8),
+    "gpt-1t-slice-tp4pp2": (4, 25600, 160, 51200, 2048, 1, 4, 2, True, 0.1, 8),
 }
 
 
@@ -141,7 +153,7 @@ def run_reference(args, rank, world):
     """--impl reference: the reference-side CPU implementation of the path on the host cores."""
     if rank != 0:
         return 0
-    L, d, a, V, s, mbs, tp, pp, ckpt, drop = WORKLOADS[args.workload]
+    L, d, a, V, s, mbs, tp, pp, ckpt, drop, nmb = WORKLOADS[args.workload]
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
         cpu_layer_sample(L, d, a, V, s, threads)
@@ -151,7 +163,7 @@ def run_reference(args, rank, world):
         vals.append(tok_s)
         secs_all.append(secs)
     v = statistics.median(vals)
-    gbs = mbs * args.gpus
+    gbs = mbs * nmb * max(args.gpus // (tp * pp), 1)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * gbs * s / v,
@@ -169,10 +181,11 @@ def run_reference(args, rank, world):
 
 
 def workload_config(args, world):
-    L, d, a, V, s, mbs, tp, pp, ckpt, drop = WORKLOADS[args.workload]
-    dp = world // (tp * pp)
+    L, d, a, V, s, mbs, tp, pp, ckpt, drop, nmb = WORKLOADS[args.workload]
+    dp = max(world // (tp * pp), 1)
     return {"workload": f"{args.workload}: GPT L{L} d{d} a{a} V{V} s{s}, fwd+bwd+ZeRO-1 Adam step",
-            "global_batch": mbs * dp, "seq_len": s, "micro_batch": mbs, "parallelism": f"tp{tp}.pp{pp}.dp{dp}",
+            "global_batch": mbs * nmb * dp, "seq_len": s, "micro_batch": mbs, "microbatches": nmb,
+            "parallelism": f"tp{tp}.pp{pp}.dp{dp}",
             "zero_stage": 1, "activation_checkpointing": ckpt, "hidden_dropout": drop, "attention_dropout": 0.0,
             "flash_attention": True, "grad_accum_dtype": "fp32",
             "l2": "per-step working set (tens of GB) far larger than the 126 MB L2; no flush needed"}
@@ -198,9 +211,11 @@ def main():
     from paper_2312_12705_b200.build import LIB, build
     if not LIB.exists():
         build()
-    L, d, a, V, s, mbs, tp, pp, ckpt, drop = WORKLOADS[args.workload]
+    L, d, a, V, s, mbs, tp, pp, ckpt, drop, nmb = WORKLOADS[args.workload]
+    if world % (tp * pp) != 0:
+        raise SystemExit(f"{args.workload} needs a multiple of tp*pp = {tp * pp} GPUs, got {world}")
     dp = world // (tp * pp)
-    gbs = mbs * dp
+    gbs = mbs * nmb * dp
     spec = T.ModelSpec(L, d, a, V, s)
     cfg = T.ParallelConfig(tp=tp, pp=pp, dp=dp, mbs=mbs, gbs=gbs, zero_stage=1, checkpoint_activations=int(ckpt))
     opts = T.TrainOptions(seed=1234, dropout=drop, lr=1e-4, weight_decay=0.0)
