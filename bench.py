@@ -72,8 +72,10 @@ def share_nccl_id(rank: int, world: int) -> bytes | None:
     if world == 1:
         return None
     from paper_2312_12705_b200 import _lib as T
-    tag = f"{os.environ.get('MASTER_PORT', '0')}_{os.environ.get('TORCHELASTIC_RUN_ID', 'x')}_" \
-          f"{os.environ.get('TORCHELASTIC_RESTART_COUNT', '0')}"
+    # Unique per launch: all ranks of one torchrun launch share the agent process as parent
+    # (TORCHELASTIC_RUN_ID is constant under static rendezvous, so back-to-back launches on one
+    # box would otherwise read a stale id).
+    tag = f"{os.environ.get('MASTER_PORT', '0')}_{os.getppid()}_{os.environ.get('TORCHELASTIC_RESTART_COUNT', '0')}"
     path = Path(tempfile.gettempdir()) / f"gptb200_ncclid_{tag}"
     if rank == 0:
         nid = T.nccl_unique_id()
@@ -221,6 +223,10 @@ def main():
     opts = T.TrainOptions(seed=1234, dropout=drop, lr=1e-4, weight_decay=0.0)
     nid = share_nccl_id(rank, world)
     sess = T.Session(spec, cfg, opts, rank=rank, world=world, device=local, nccl_id=nid)
+    sess.barrier()  # every rank has joined the communicator: the id file is no longer needed
+    if world > 1 and rank == 0:
+        for f in Path(tempfile.gettempdir()).glob(f"gptb200_ncclid_{os.environ.get('MASTER_PORT', '0')}_{os.getppid()}_*"):
+            f.unlink(missing_ok=True)
     sess.init_params()
     tokens = np.random.default_rng(1234).integers(0, V, size=(gbs, s + 1), dtype=np.int32)
     sess.upload_tokens(tokens)
