@@ -163,6 +163,10 @@ int tp_session_read_tensor(tp_session* s, int which, int tensor_id, float* host_
  * only this rank's ZeRO shard [d*P/dp, (d+1)*P/dp) holds DP-reduced values), 2/3/4 = fp32 master /
  * Adam m / Adam v shard [P/dp]. offset and n in elements of that buffer. */
 int tp_session_read_flat(tp_session* s, int which, int64_t offset, int64_t n, float* host_out);
+/* ZeRO-1 buckets of the flat buffers: triples (flat_offset, length, master_offset); DP rank d owns
+ * [flat_offset + d*length/dp, flat_offset + (d+1)*length/dp) of each bucket, stored contiguously
+ * in its master/m/v shard at master_offset. Writes up to cap triples; *n = bucket count. */
+int tp_session_buckets(tp_session* s, int64_t* out, int cap, int* n);
 /* out = {flat_params, shard_params, device_bytes, microbatches, launches_last_step, rank, world, 0} */
 int tp_session_info(tp_session* s, int64_t out[8]);
 

@@ -102,6 +102,7 @@ SIGNATURES: dict[str, tuple] = {
     "tp_session_read_tensor": (_i, [_vp, _i, _i, _vp]),
     "tp_session_info": (_i, [_vp, C.POINTER(_i64)]),
     "tp_session_read_flat": (_i, [_vp, _i, _i64, _i64, _vp]),
+    "tp_session_buckets": (_i, [_vp, C.POINTER(_i64), _i, C.POINTER(_i)]),
     "tp_session_time_steps": (_i, [_vp, _i, _i, C.POINTER(_f), C.POINTER(KernelTimes)]),
     "tp_session_allreduce_max": (_i, [_vp, C.POINTER(_f)]),
 }
@@ -288,6 +289,13 @@ class Session:
         out = np.empty(n, dtype=np.float32)
         check(self._lib.tp_session_read_flat(self.h, which, offset, n, out.ctypes.data))
         return out
+
+    def buckets(self) -> list[tuple[int, int, int]]:
+        """ZeRO-1 buckets: (flat_offset, length, master_offset)."""
+        buf = (_i64 * (3 * 4096))()
+        n = _i()
+        check(self._lib.tp_session_buckets(self.h, buf, 4096, C.byref(n)))
+        return [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]) for i in range(n.value)]
 
     def info(self) -> dict:
         out = (_i64 * 8)()

@@ -151,6 +151,18 @@ int tp_session_read_flat(tp_session* s, int which, int64_t offset, int64_t n, fl
   return run("tp_session_read_flat", [&] { s->stage->read_flat(which, offset, n, host_out); });
 }
 
+int tp_session_buckets(tp_session* s, int64_t* out, int cap, int* n) {
+  return run("tp_session_buckets", [&] {
+    const auto& b = s->stage->buckets();
+    *n = static_cast<int>(b.size());
+    for (int i = 0; i < *n && i < cap; ++i) {
+      out[3 * i] = b[i].off;
+      out[3 * i + 1] = b[i].len;
+      out[3 * i + 2] = b[i].master_off;
+    }
+  });
+}
+
 int tp_session_info(tp_session* s, int64_t out[8]) {
   return run("tp_session_info", [&] {
     out[0] = s->stage->flat_params();

@@ -93,6 +93,12 @@ Stage::Stage(const trainplan::ModelSpec& model, const trainplan::ParallelConfig&
 
 Stage::~Stage() {
   if (st_) cudaStreamSynchronize(st_);
+  if (comm_st_) {
+    cudaStreamSynchronize(comm_st_);
+    for (auto& e : bucket_ev_) cudaEventDestroy(e);
+    cudaEventDestroy(comm_done_);
+    cudaStreamDestroy(comm_st_);
+  }
   for (auto& e : ev_pool_) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
@@ -141,8 +147,20 @@ void Stage::build_layout() {
     off = align64(off + rows * cols);
   };
   const int64_t d = d_, dt = dt_, Vt = Vt_;
+  const int64_t q = static_cast<int64_t>(cfg_.dp) * 64;
+  int64_t bucket_start = 0;
+  auto close_bucket = [&]() {
+    off = (off + q - 1) / q * q;
+    Bucket b;
+    b.off = bucket_start;
+    b.len = off - bucket_start;
+    b.master_off = buckets_.empty() ? 0 : buckets_.back().master_off + buckets_.back().len / cfg_.dp;
+    buckets_.push_back(b);
+    bucket_start = off;
+  };
   if (first_ || last_) add(0, Vt, d, Vt, 0, t * Vt, 0, d, std_base, 0.f);
   if (first_) add(1, s_, d, s_, 0, 0, 0, d, std_base, 0.f);
+  close_bucket();  // bucket 0: embeddings (possibly empty)
   for (int l = 0; l < Ll_; ++l) {
     const int b = 2 + kPerLayer * (layer0_ + l);
     add(b + LN1G, d, 1, d, 0, 0, 0, 1, 0.f, 1.f);
@@ -157,13 +175,14 @@ void Stage::build_layout() {
     add(b + B1, 4 * dt, 1, 4 * dt, 0, t * 4 * dt, 0, 1, 0.f, 0.f);
     add(b + W2, d, 4 * dt, d, 0, 0, t * 4 * dt, 4 * d, std_out, 0.f);
     add(b + B2, d, 1, d, 0, 0, 0, 1, 0.f, 0.f);
+    if (l == Ll_ - 1 && last_) {  // final LN grads are final before the last layer's
+      add(2 + kPerLayer * L_, d, 1, d, 0, 0, 0, 1, 0.f, 1.f);
+      add(2 + kPerLayer * L_ + 1, d, 1, d, 0, 0, 0, 1, 0.f, 0.f);
+    }
+    close_bucket();
+    layer_bucket_.push_back(static_cast<int>(buckets_.size()) - 1);
   }
-  if (last_) {
-    add(2 + kPerLayer * L_, d, 1, d, 0, 0, 0, 1, 0.f, 1.f);
-    add(2 + kPerLayer * L_ + 1, d, 1, d, 0, 0, 0, 1, 0.f, 0.f);
-  }
-  const int64_t q = static_cast<int64_t>(cfg_.dp) * 64;
-  P_ = (off + q - 1) / q * q;
+  P_ = off;
   shard_ = P_ / cfg_.dp;
   slot_index_.assign(2 + kPerLayer * L_ + 2, -1);
   for (size_t i = 0; i < slots_.size(); ++i) slot_index_[slots_[i].tensor_id] = static_cast<int>(i);
@@ -226,6 +245,13 @@ void Stage::allocate() {
     row_loss_ = static_cast<float*>(alloc(M * 4));
   }
   loss_acc_ = static_cast<float*>(alloc(4));
+  overlap_rs_ = cfg_.dp > 1;
+  if (overlap_rs_) {
+    cudaStreamCreateWithFlags(&comm_st_, cudaStreamNonBlocking);
+    bucket_ev_.resize(buckets_.size());
+    for (auto& e : bucket_ev_) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&comm_done_, cudaEventDisableTiming);
+  }
 }
 
 const ParamSlot* Stage::slot(int tid) const {
@@ -267,7 +293,11 @@ void Stage::init_params() {
     ck(init_tensor(a, st_), "init_tensor");
   }
   ck(cast_f32_bf16(grads_, params_, P_, st_), "cast params");
-  cudaMemcpyAsync(master_, grads_ + comms_.me.d * shard_, shard_ * sizeof(float), cudaMemcpyDeviceToDevice, st_);
+  for (const Bucket& b : buckets_) {
+    const int64_t n = b.len / cfg_.dp;
+    if (n) cudaMemcpyAsync(master_ + b.master_off, grads_ + b.off + comms_.me.d * n, n * sizeof(float),
+                           cudaMemcpyDeviceToDevice, st_);
+  }
   cudaMemsetAsync(adam_m_, 0, shard_ * sizeof(float), st_);
   cudaMemsetAsync(adam_v_, 0, shard_ * sizeof(float), st_);
   cudaMemsetAsync(grads_, 0, P_ * sizeof(float), st_);
@@ -566,6 +596,7 @@ void Stage::backward_op(int mb, bf16* dh) {
     LayerActs& A = acts_for(slot, l);
     if (ckpt_) layer_recompute(l, A, S.h[l]);
     layer_bwd(l, A, S.h[l], dh, drop_on ? dy_ : dh);
+    if (in_last_bwd_) grads_ready(layer_bucket_[l]);
   }
   if (first_) {
     const bf16* g = drop_on ? dy_ : dh;
@@ -577,17 +608,38 @@ void Stage::backward_op(int mb, bf16* dh) {
 // ------------------------------------------------------------------------------ step
 void Stage::optimizer_step() {
   AdamArgs a;
-  a.n = shard_;
-  a.master = master_;
-  a.m = adam_m_;
-  a.v = adam_v_;
-  a.grad = grads_ + comms_.me.d * shard_;
-  a.param = params_ + comms_.me.d * shard_;
   a.lr = opts_.lr, a.beta1 = opts_.beta1, a.beta2 = opts_.beta2, a.eps = opts_.eps, a.weight_decay = opts_.weight_decay;
   a.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(opts_.beta1), step_no_));
   a.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(opts_.beta2), step_no_));
   KScope prof(this, K_ADAM, 0, 30.0 * shard_);
-  ck(adam_step(a, st_), "adam");
+  if (cfg_.dp == 1) {  // owned slices == whole buckets == the flat buffer: one launch
+    a.n = P_, a.master = master_, a.m = adam_m_, a.v = adam_v_, a.grad = grads_, a.param = params_;
+    ck(adam_step(a, st_), "adam");
+    return;
+  }
+  for (const Bucket& b : buckets_) {
+    const int64_t n = b.len / cfg_.dp;
+    if (!n) continue;
+    const int64_t own = b.off + comms_.me.d * n;
+    a.n = n, a.master = master_ + b.master_off, a.m = adam_m_ + b.master_off, a.v = adam_v_ + b.master_off;
+    a.grad = grads_ + own, a.param = params_ + own;
+    ck(adam_step(a, st_), "adam");
+  }
+}
+
+// Overlapped ZeRO-1 reduce-scatter: the bucket's gradients are final on the compute stream; the
+// comm stream waits for them and reduce-scatters in place while backward continues.
+void Stage::grads_ready(int bucket) {
+  if (!overlap_rs_) return;
+  const Bucket& b = buckets_[bucket];
+  if (!b.len) return;
+  cudaEventRecord(bucket_ev_[bucket], st_);
+  cudaStreamWaitEvent(comm_st_, bucket_ev_[bucket], 0);
+  try {
+    comms_.dp_reduce_scatter_f32(grads_ + b.off, b.len / cfg_.dp, comm_st_);
+  } catch (const CommError& e) {
+    throw StepError{e.code, e.msg};
+  }
 }
 
 void Stage::step() {
@@ -596,6 +648,7 @@ void Stage::step() {
   cudaMemsetAsync(grads_, 0, P_ * sizeof(float), st_);
   cudaMemsetAsync(loss_acc_, 0, sizeof(float), st_);
   const auto ops = trainplan::pipeline_order(ScheduleKind::OneF1B, cfg_.pp, m_, 1, comms_.me.p);
+  const int last_bwd_mb = ops.back().microbatch;
   const size_t n_act = static_cast<size_t>(M_) * d_;
   const void* pending = nullptr;
   int pending_peer = -1, dh_idx = 0;
@@ -623,7 +676,9 @@ void Stage::step() {
           pending_peer = comms_.me.p + 1;
         }
       } else {
+        in_last_bwd_ = op.microbatch == last_bwd_mb;
         backward_op(op.microbatch, dh_[dh_idx]);
+        in_last_bwd_ = false;
         if (!first_) {
           pending = dh_[dh_idx];
           pending_peer = comms_.me.p - 1;
@@ -635,15 +690,26 @@ void Stage::step() {
       ++launches_;
       comms_.pp_exchange(pending, pending_peer, nullptr, -1, n_act, st_);
     }
-    if (cfg_.pp > 1 && (first_ || last_)) comms_.emb_allreduce_f32(grads_ + slot_offset(0), static_cast<size_t>(Vt_) * d_, st_);
-    {
-      KScope prof(this, K_COMM_DP);
-      comms_.dp_reduce_scatter_f32(grads_, shard_, st_);
+    cudaStream_t emb_st = overlap_rs_ ? comm_st_ : st_;
+    if (overlap_rs_) {
+      cudaEventRecord(bucket_ev_[0], st_);
+      cudaStreamWaitEvent(comm_st_, bucket_ev_[0], 0);
+    }
+    if (cfg_.pp > 1 && (first_ || last_))
+      comms_.emb_allreduce_f32(grads_ + slot_offset(0), static_cast<size_t>(Vt_) * d_, emb_st);
+    if (overlap_rs_) {
+      {
+        KScope prof(this, K_COMM_DP);
+        if (buckets_[0].len) comms_.dp_reduce_scatter_f32(grads_ + buckets_[0].off, buckets_[0].len / cfg_.dp, comm_st_);
+        cudaEventRecord(comm_done_, comm_st_);
+        cudaStreamWaitEvent(st_, comm_done_, 0);  // the compute stream waits for all reduce-scatters
+      }
     }
     optimizer_step();
-    {
+    if (cfg_.dp > 1) {
       KScope prof(this, K_COMM_DP);
-      comms_.dp_allgather_bf16(params_, shard_, st_);
+      for (const Bucket& b : buckets_)
+        if (b.len) comms_.dp_allgather_bf16(params_ + b.off, b.len / cfg_.dp, st_);
     }
     comms_.world_allreduce_f32(loss_acc_, 1, st_);
   } catch (const CommError& e) {
@@ -729,8 +795,13 @@ void Stage::read_tensor(int which, int tid, float* host) const {
   if (which == 1) {
     base = grads_;
   } else {
-    off -= comms_.me.d * shard_;
-    if (off < 0 || off + n > shard_) throw StepError{TP_ERR_INVALID, "tensor outside this rank's ZeRO shard"};
+    int64_t moff = -1;
+    for (const Bucket& b : buckets_) {
+      const int64_t per = b.len / cfg_.dp, own = b.off + comms_.me.d * per;
+      if (off >= own && off + n <= own + per) moff = b.master_off + (off - own);
+    }
+    if (moff < 0) throw StepError{TP_ERR_INVALID, "tensor outside this rank's ZeRO shard"};
+    off = moff;
     base = which == 2 ? master_ : (which == 3 ? adam_m_ : adam_v_);
   }
   cudaMemcpy(host, base + off, n * 4, cudaMemcpyDeviceToHost);

@@ -53,6 +53,12 @@ struct KernelTimes {
   double bytes[K_NUM] = {};  // algorithmic HBM bytes (norm / elementwise / Adam)
 };
 
+// ZeRO-1 bucket: a contiguous range of the flat buffers (padded to a multiple of 64*dp); DP rank
+// d owns [off + d*len/dp, off + (d+1)*len/dp), stored in the master/m/v shard at master_off.
+struct Bucket {
+  int64_t off = 0, len = 0, master_off = 0;
+};
+
 struct StepTimes {  // milliseconds of the last step on this rank (CUDA events)
   float total = 0, tp_comm = 0, pp_comm = 0, dp_comm = 0, optimizer = 0;
 };
@@ -83,6 +89,7 @@ class Stage {
   // Forward-only loss of the uploaded batch with the current parameters (no update).
   float eval_loss();
 
+  const std::vector<Bucket>& buckets() const { return buckets_; }
   int64_t flat_params() const { return P_; }
   int64_t shard_params() const { return shard_; }
   size_t device_bytes() const { return dev_bytes_; }
@@ -123,6 +130,7 @@ class Stage {
   void head_and_loss(int slot, bool with_grad);
   void head_bwd(bf16* dh_out);
   void optimizer_step();
+  void grads_ready(int bucket);  // last microbatch's grads of `bucket` final: start its reduce-scatter
   void prepare_tokens(int mb, int slot);
 
   void gemm_fwd(const bf16* X, const bf16* W, const bf16* bias, bf16* Y, int M, int N, int K, int epi = 0,
@@ -167,6 +175,12 @@ class Stage {
   // parameters
   std::vector<ParamSlot> slots_;
   std::vector<int> slot_index_;  // tensor_id -> index in slots_ or -1
+  std::vector<Bucket> buckets_;  // [0] = embeddings, then one per local layer (last + final LN)
+  std::vector<int> layer_bucket_;
+  cudaStream_t comm_st_ = nullptr;
+  std::vector<cudaEvent_t> bucket_ev_;
+  cudaEvent_t comm_done_ = nullptr;
+  bool overlap_rs_ = false, in_last_bwd_ = false;
   int64_t P_ = 0, shard_ = 0;
   bf16* params_ = nullptr;
   float *grads_ = nullptr, *master_ = nullptr, *adam_m_ = nullptr, *adam_v_ = nullptr;

@@ -63,7 +63,8 @@ def main():
             layout[tid] = ti
     coords = T.rank_coords(a.rank, c["tp"], c["pp"], c["dp"])
     np.savez(out / f"rank{a.rank}.npz", grads=grads, master0=master0, master1=master1, loss=np.array(loss),
-             coords=np.array(coords), P=np.array(P), shard=np.array(shard), layout=json.dumps(layout))
+             coords=np.array(coords), P=np.array(P), shard=np.array(shard), layout=json.dumps(layout),
+             buckets=np.array(sess.buckets(), dtype=np.int64).reshape(-1, 3))
     sess.barrier()
     sess.close()
 

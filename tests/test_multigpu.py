@@ -88,10 +88,15 @@ def run_layout(tp, pp, dp, L=2, d=256, a=4, V=1024, s=128, mbs=1, gbs=None, ckpt
         for p in range(pp):
             members = [r for r in ranks if tuple(r["coords"][:2]) == (t, p)]
             members.sort(key=lambda r: int(r["coords"][2]))
-            P, shard = int(members[0]["P"]), int(members[0]["shard"])
-            red = np.concatenate([m["grads"][k * shard:(k + 1) * shard] for k, m in enumerate(members)])
-            m0 = np.concatenate([m["master0"] for m in members])
-            m1 = np.concatenate([m["master1"] for m in members])
+            P = int(members[0]["P"])
+            red, m0, m1 = np.zeros(P, np.float32), np.zeros(P, np.float32), np.zeros(P, np.float32)
+            for off, ln, moff in members[0]["buckets"]:  # DP rank k owns slice k of every bucket
+                per = ln // dp
+                for k, m in enumerate(members):
+                    lo = off + k * per
+                    red[lo:lo + per] = m["grads"][lo:lo + per]
+                    m0[lo:lo + per] = m["master0"][moff:moff + per]
+                    m1[lo:lo + per] = m["master1"][moff:moff + per]
             layout = {int(k): v for k, v in json.loads(str(members[0]["layout"])).items()}
             for tid, info in layout.items():
                 n = info["rows"] * info["cols"]
