@@ -47,6 +47,15 @@ __device__ __forceinline__ void dwait(uint64_t* bar, uint32_t parity, int id) {
 #endif
 constexpr float kLog2e = 1.4426950408889634f;
 
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+// 2^x on the SFU, flush-to-zero (one MUFU.EX2; exp2f adds denormal range fix-ups we do not need).
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 template <int HD>
 struct TcFwdCfg {
   static constexpr int NC = (HD + 63) / 64;             // 64-wide swizzle chunks of the head dim
@@ -56,12 +65,12 @@ struct TcFwdCfg {
   static constexpr int kQBytes = NC * kTileBytes;
   static constexpr int kKVBytes = NC * kTileBytes;
   static constexpr int kPBytes = 2 * kTileBytes;        // P [128][128] = 2 chunks
-  static constexpr int kSmem = kQBytes + 2 * kStages * kKVBytes + kPBufs * kPBytes + 1024 + 256;
+  static constexpr int kSmem = kQBytes + 2 * kStages * kKVBytes + kPBufs * kPBytes + 1024 + 256 + 1024;
   static constexpr int kTmemCols = 512;                 // S0 | S1 | O
 };
 
 template <int HD>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     fa_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, __nv_bfloat16* __restrict__ out,
                      float* __restrict__ lse, int s, int ht, float scale_log2) {
   using Cfg = TcFwdCfg<HD>;
@@ -102,10 +111,10 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&s_free[i], 4);
+      ptx::mbar_init(&s_free[i], 8);
     }
     for (int i = 0; i < PB; ++i) {
-      ptx::mbar_init(&p_full[i], 4);
+      ptx::mbar_init(&p_full[i], 8);
       ptx::mbar_init(&pv_done[i], 1);
     }
     ptx::fence_mbar_init();
@@ -178,37 +187,56 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
+    // 8 warps: warp w owns TMEM lane quarter (w & 3) = query rows 32q..32q+31 and one half of the
+    // 128 score columns (the other half belongs to the warp with the same quarter); the two
+    // halves exchange their row max through smem once per tile and their row sums at the end.
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int r = quarter * 32 + lane;  // query row within the block == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
     const int q_row = qb * kBM + r;
+    constexpr int NCH = HD / 32;           // 32-column chunks of O
+    const int oc0 = half ? (NCH + 1) / 2 : 0, oc1 = half ? NCH : (NCH + 1) / 2;
+    float* xmax = reinterpret_cast<float*>(tmem_slot + 4);  // [2 halves][128]
     float m_used = -INFINITY, l = 0.f;
-    uint8_t* p_row0 = sP + r * 128;
+    uint8_t* p_row0 = sP + half * Cfg::kTileBytes + r * 128;
     for (int j = 0; j < n_tiles; ++j) {
       const int buf = j & 1;
       WAIT(&s_full[buf], (j >> 1) & 1, 8);
       ptx::tc_fence_after();
-      float x[kBN];
+      // raw scores (scale_log2 > 0 is applied inside the exponent: max commutes with it)
+      float x[64];
 #pragma unroll
-      for (int c = 0; c < kBN / 32; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(tmem + lane_base + buf * kBN + c * 32, v);
+        ptx::tmem_ld_32x32b_x32(tmem + lane_base + buf * kBN + half * 64 + c * 32, v);
         ptx::tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) x[c * 32 + i] = __uint_as_float(v[i]) * scale_log2;
+        for (int i = 0; i < 32; ++i) x[c * 32 + i] = __uint_as_float(v[i]);
       }
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&s_free[buf]);
-      const bool diag = (j == qb);
-      float mt = -INFINITY;
+      if (j == qb) {  // diagonal tile: causal mask (the only tile that needs one)
 #pragma unroll
-      for (int i = 0; i < kBN; ++i) {
-        if (diag && i > r) x[i] = -INFINITY;
-        mt = fmaxf(mt, x[i]);
+        for (int i = 0; i < 64; ++i)
+          if (half * 64 + i > r) x[i] = -INFINITY;
       }
+      float pm[8];  // 8 independent partial maxima (short dependency chains)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pm[k] = fmaxf(x[k], x[k + 8]);
+#pragma unroll
+      for (int i = 16; i < 64; i += 8)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pm[k] = fmaxf(pm[k], x[i + k]);
+      float mt = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+      mt *= scale_log2;
+      xmax[half * 128 + r] = mt;
+      named_sync(1, 256);
+      mt = fmaxf(mt, xmax[(half ^ 1) * 128 + r]);
+      named_sync(1, 256);  // exchange slots are reused next tile
       // Lazy rescale (only when a row's max grows by > 2^8). tcgen05.ld/st are warp-collective,
-      // so the decision is warp-uniform: every lane of the warp rescales (factor 1 if unchanged).
+      // so the decision is warp-uniform (and identical in both halves of a row).
       if (__any_sync(0xffffffffu, mt > m_used + 8.f)) {
         const float m_new = fmaxf(m_used, mt);
         if (j > 0) {
@@ -218,7 +246,7 @@ __global__ void __launch_bounds__(192, 1)
           l *= f;
           ptx::tc_fence_after();
 #pragma unroll 1
-          for (int c = 0; c < (HD + 31) / 32; ++c) {
+          for (int c = oc0; c < oc1; ++c) {
             uint32_t v[32];
             ptx::tmem_ld_32x32b_x32(tO + lane_base + c * 32, v);
             ptx::tmem_ld_wait();
@@ -233,54 +261,55 @@ __global__ void __launch_bounds__(192, 1)
       // the P buffer of tile j must be free of PV_{j-PB}
       if (j >= PB) WAIT(&pv_done[j % PB], ((j / PB) - 1) & 1, 10);
       uint8_t* p_row = p_row0 + (j % PB) * Cfg::kPBytes;
-      // P = exp2(x - m_used) -> bf16, 128B-swizzled K-major rows: chunk c2 (64 cols), 16B unit u
+      // P = exp2(x - m_used) -> bf16 into this half's 64-column swizzle chunk, 16B unit u
+      const float neg_m = -m_used;
+      float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // independent partial row sums
 #pragma unroll
-      for (int c2 = 0; c2 < 2; ++c2) {
+      for (int u = 0; u < 8; ++u) {
+        float p[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          float p[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            p[e] = exp2f(x[c2 * 64 + u * 8 + e] - m_used);
-            l += p[e];
-          }
-          uint4 pk;
-          pk.x = ptx::pack_bf16(p[0], p[1]);
-          pk.y = ptx::pack_bf16(p[2], p[3]);
-          pk.z = ptx::pack_bf16(p[4], p[5]);
-          pk.w = ptx::pack_bf16(p[6], p[7]);
-          *reinterpret_cast<uint4*>(p_row + c2 * Cfg::kTileBytes + ((u ^ (r & 7)) * 16)) = pk;
+        for (int e = 0; e < 8; ++e) {
+          p[e] = ex2(fmaf(x[u * 8 + e], scale_log2, neg_m));
+          ls[e] += p[e];
         }
+        uint4 pk;
+        pk.x = ptx::pack_bf16(p[0], p[1]);
+        pk.y = ptx::pack_bf16(p[2], p[3]);
+        pk.z = ptx::pack_bf16(p[4], p[5]);
+        pk.w = ptx::pack_bf16(p[6], p[7]);
+        *reinterpret_cast<uint4*>(p_row + ((u ^ (r & 7)) * 16)) = pk;
       }
+      l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
       ptx::fence_proxy_async();
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&p_full[j % PB]);
     }
+    // combine the two halves' row sums
+    xmax[half * 128 + r] = l;
+    named_sync(1, 256);
+    const float l_tot = l + xmax[(half ^ 1) * 128 + r];
     WAIT(&pv_done[(n_tiles - 1) % PB], ((n_tiles - 1) / PB) & 1, 11);
     ptx::tc_fence_after();
-    const float inv = 1.f / l;
+    const float inv = 1.f / l_tot;
     __nv_bfloat16* orow = out + static_cast<size_t>(row0 + q_row) * dt + h * HD;
 #pragma unroll 1
-    for (int c = 0; c < (HD + 31) / 32; ++c) {
+    for (int c = oc0; c < oc1; ++c) {
       uint32_t v[32];
       ptx::tmem_ld_32x32b_x32(tO + lane_base + c * 32, v);
       ptx::tmem_ld_wait();
-      const int ncol = (HD - c * 32) < 32 ? (HD - c * 32) : 32;
-      if (ncol == 32) {
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 pk;
-          pk.x = ptx::pack_bf16(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
-          pk.y = ptx::pack_bf16(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
-          pk.z = ptx::pack_bf16(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
-          pk.w = ptx::pack_bf16(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
-          dst[q] = pk;
-        }
+      for (int q = 0; q < 4; ++q) {
+        uint4 pk;
+        pk.x = ptx::pack_bf16(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
+        pk.y = ptx::pack_bf16(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
+        pk.z = ptx::pack_bf16(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
+        pk.w = ptx::pack_bf16(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
+        dst[q] = pk;
       }
     }
-    lse[(static_cast<size_t>(b) * ht + h) * s + q_row] = m_used + log2f(l);
+    if (half == 0) lse[(static_cast<size_t>(b) * ht + h) * s + q_row] = m_used + log2f(l_tot);
   }
   __syncthreads();
   if (warp == 1) {
@@ -309,10 +338,9 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
                : "memory");
 }
 
-__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 template <int HD>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     fa_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                      const float* __restrict__ lse, const float* __restrict__ Dg, float* __restrict__ dq_acc,
                      __nv_bfloat16* __restrict__ dqkv, int s, int ht, float scale_log2, float scale) {
@@ -357,11 +385,11 @@ __global__ void __launch_bounds__(192, 1)
     ptx::mbar_init(qdo_full, 1);
     ptx::mbar_init(qdo_empty, 1);
     ptx::mbar_init(sdp_full, 1);
-    ptx::mbar_init(sdp_free, 4);
-    ptx::mbar_init(pds_full, 4);
+    ptx::mbar_init(sdp_free, 8);
+    ptx::mbar_init(pds_full, 8);
     ptx::mbar_init(pds_free, 1);
     ptx::mbar_init(dq_full, 1);
-    ptx::mbar_init(dq_free, 4);
+    ptx::mbar_init(dq_free, 8);
     ptx::mbar_init(kdv_full, 1);
     ptx::fence_mbar_init();
   }
@@ -434,49 +462,65 @@ __global__ void __launch_bounds__(192, 1)
       ptx::mma_commit(kdv_full);
     }
   } else {
+    // 8 compute warps: warp w owns TMEM lane quarter (w & 3) and one half of the 128 query
+    // columns (P^T / dS^T) or of the head dim (dQ, dK, dV readout).
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int r = quarter * 32 + lane;  // TMEM lane: kv row for S^T/dP^T/dK/dV, q row for dQ
     const uint32_t lb = static_cast<uint32_t>(quarter * 32) << 16;
-    const int tid = threadIdx.x - 64;
+    const int tid = threadIdx.x - 64;   // 0..255
     const float* gL = lse + (static_cast<size_t>(b) * ht + h) * s;
     const float* gD = Dg + (static_cast<size_t>(b) * ht + h) * s;
+    constexpr int NCH = HD / 32;
+    const int hc0 = half ? NCH / 2 : 0, hc1 = half ? NCH : NCH / 2;
     for (int it = 0; it < n_it; ++it) {
       const int q0 = (qt_first + it) * 128;
       const int lb2 = (it & 1) * 128;
-      sL[lb2 + tid] = gL[q0 + tid];
-      sD[lb2 + tid] = gD[q0 + tid];
-      named_sync(1, 128);
+      if (tid < 128) sL[lb2 + tid] = gL[q0 + tid];
+      else sD[lb2 + tid - 128] = gD[q0 + tid - 128];
+      named_sync(1, 256);
       WAIT(sdp_full, it & 1, 26);
       ptx::tc_fence_after();
       WAIT(pds_free, (it & 1) ^ 1, 27);
-      const bool diag = (it == 0);
-      uint8_t* prow = sPT + r * 128;
-      uint8_t* drow = sdST + r * 128;
+      uint8_t* prow = sPT + half * TB + r * 128;
+      uint8_t* drow = sdST + half * TB + r * 128;
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {  // 32 query columns at a time
+      for (int c = 0; c < 2; ++c) {  // 32 query columns at a time: half*64 + c*32 ..
+        const int qc = half * 64 + c * 32;
         uint32_t sv[32], dv[32];
-        ptx::tmem_ld_32x32b_x32(tS + lb + c * 32, sv);
-        ptx::tmem_ld_32x32b_x32(tdP + lb + c * 32, dv);
+        ptx::tmem_ld_32x32b_x32(tS + lb + qc, sv);
+        ptx::tmem_ld_32x32b_x32(tdP + lb + qc, dv);
         ptx::tmem_ld_wait();
+        const float4* L4 = reinterpret_cast<const float4*>(sL + lb2 + qc);
+        const float4* D4 = reinterpret_cast<const float4*>(sD + lb2 + qc);
         uint32_t pk[16], dk[16];
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float p0 = exp2f(__uint_as_float(sv[e]) * scale_log2 - sL[lb2 + c * 32 + e]);
-          float p1 = exp2f(__uint_as_float(sv[e + 1]) * scale_log2 - sL[lb2 + c * 32 + e + 1]);
-          if (diag) {
-            if (c * 32 + e < r) p0 = 0.f;
-            if (c * 32 + e + 1 < r) p1 = 0.f;
+        for (int e4 = 0; e4 < 8; ++e4) {
+          const float4 l4 = L4[e4], d4 = D4[e4];
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dvv[4] = {d4.x, d4.y, d4.z, d4.w};
+          float p[4], ds[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            p[k] = ex2(fmaf(__uint_as_float(sv[4 * e4 + k]), scale_log2, -lv[k]));
+            ds[k] = p[k] * (__uint_as_float(dv[4 * e4 + k]) - dvv[k]);
           }
-          const float d0 = p0 * (__uint_as_float(dv[e]) - sD[lb2 + c * 32 + e]);
-          const float d1 = p1 * (__uint_as_float(dv[e + 1]) - sD[lb2 + c * 32 + e + 1]);
-          pk[e / 2] = ptx::pack_bf16(p0, p1);
-          dk[e / 2] = ptx::pack_bf16(d0, d1);
+          pk[2 * e4] = ptx::pack_bf16(p[0], p[1]);
+          pk[2 * e4 + 1] = ptx::pack_bf16(p[2], p[3]);
+          dk[2 * e4] = ptx::pack_bf16(ds[0], ds[1]);
+          dk[2 * e4 + 1] = ptx::pack_bf16(ds[2], ds[3]);
         }
-        // columns c*32..c*32+31 = chunk c/2, 16B units u0..u0+3 with u0 = (c%2)*4
-        const int chunk = c >> 1, u0 = (c & 1) * 4;
+        if (it == 0 && qc < r + 1) {  // diagonal tile: queries before this kv row see nothing
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (qc + e < r) {
+              pk[e / 2] &= (e & 1) ? 0x0000FFFFu : 0xFFFF0000u;
+              dk[e / 2] &= (e & 1) ? 0x0000FFFFu : 0xFFFF0000u;
+            }
+        }
+        // columns qc..qc+31 = 16B units u0..u0+3 (u0 = c*4) of this half's swizzle chunk
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int off = chunk * TB + (((u0 + u) ^ (r & 7)) * 16);
+          const int off = ((c * 4 + u) ^ (r & 7)) * 16;
           *reinterpret_cast<uint4*>(prow + off) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
           *reinterpret_cast<uint4*>(drow + off) = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
         }
@@ -488,12 +532,12 @@ __global__ void __launch_bounds__(192, 1)
         ptx::mbar_arrive(sdp_free);
         ptx::mbar_arrive(pds_full);
       }
-      // dQ tile (thread = query row q0 + r) -> fp32 reductions into dq_acc
+      // dQ tile (thread = query row q0 + r, this half's head-dim columns) -> fp32 reductions
       WAIT(dq_full, it & 1, 28);
       ptx::tc_fence_after();
       float* dqrow = dq_acc + static_cast<size_t>(row0 + q0 + r) * dt + h * HD;
 #pragma unroll 1
-      for (int c = 0; c < HD / 32; ++c) {
+      for (int c = hc0; c < hc1; ++c) {
         uint32_t v[32];
         ptx::tmem_ld_32x32b_x32(tS + lb + c * 32, v);
         ptx::tmem_ld_wait();
@@ -506,13 +550,13 @@ __global__ void __launch_bounds__(192, 1)
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(dq_free);
     }
-    // dK (scaled) and dV rows of this KV block
+    // dK (scaled) and dV rows of this KV block (this half's head-dim columns)
     WAIT(kdv_full, 0, 29);
     ptx::tc_fence_after();
     __nv_bfloat16* krow = dqkv + static_cast<size_t>(row0 + kv0 + r) * 3 * dt + dt + h * HD;
     __nv_bfloat16* vrow = krow + dt;
 #pragma unroll 1
-    for (int c = 0; c < HD / 32; ++c) {
+    for (int c = hc0; c < hc1; ++c) {
       uint32_t kv[32], vv[32];
       ptx::tmem_ld_32x32b_x32(tdK + lb + c * 32, kv);
       ptx::tmem_ld_32x32b_x32(tdV + lb + c * 32, vv);
@@ -558,7 +602,7 @@ int bwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* do
   if (!make_tmap_bf16(&tdo, dout, static_cast<uint64_t>(dt), M, dt, 64, 128)) return 3;
   dim3 grid(a.seq / 128, a.batch * a.heads);
   const float scale = 1.f / sqrtf(static_cast<float>(HD));
-  fa_bwd_tc_kernel<HD><<<grid, 192, Cfg::kSmem, st>>>(tq, tdo, lse, D, dq_acc, dqkv, a.seq, a.heads, scale * kLog2e,
+  fa_bwd_tc_kernel<HD><<<grid, 320, Cfg::kSmem, st>>>(tq, tdo, lse, D, dq_acc, dqkv, a.seq, a.heads, scale * kLog2e,
                                                        scale);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
@@ -578,7 +622,7 @@ int fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, flo
   if (!make_tmap_bf16(&tm, qkv, 3 * static_cast<uint64_t>(dt), static_cast<uint64_t>(a.batch) * a.seq, 3 * dt, 64, 128))
     return 3;
   dim3 grid(a.seq / kBM, a.batch * a.heads);
-  fa_fwd_tc_kernel<HD><<<grid, 192, Cfg::kSmem, st>>>(tm, out, lse, a.seq, a.heads,
+  fa_fwd_tc_kernel<HD><<<grid, 320, Cfg::kSmem, st>>>(tm, out, lse, a.seq, a.heads,
                                                        kLog2e / sqrtf(static_cast<float>(HD)));
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }

@@ -27,7 +27,7 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per TMEM lane quarter)
 
 // CG = 1: one CTA computes a 128 x BN tile.  CG = 2: a CTA pair (cluster of 2) computes a
 // 256 x BN tile with tcgen05.mma.cta_group::2 — each CTA stages 128 rows of A and BN/2 rows of B,
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 4 * CG);
+      ptx::mbar_init(&tempty[a], 8 * CG);
     }
     ptx::fence_mbar_init();
   }
@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int ehalf = (warp - 2) >> 2;  // which half of the tile's columns this warp converts
     int it = 0;
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
       int mb, nb;
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = mb * kTileM + rank * kBM + 32 * q + lane;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * BN;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = ehalf * (BN / 64); c < (ehalf + 1) * (BN / 64); ++c) {
         uint32_t r[32];
         ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
         ptx::tmem_ld_wait();
