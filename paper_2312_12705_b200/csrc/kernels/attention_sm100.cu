@@ -584,6 +584,306 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
+// K6 (hd 128), pipelined: 64-row query tiles so Q/dO and P^T/dS^T double-buffer in smem and
+// S^T/dP^T double-buffer in TMEM. Per tile j the MMA warp issues stage 1 (S^T_j = K Q_j^T,
+// dP^T_j = V dO_j^T) and then stage 2 of tile j-1 (dV += P^T dO, dK += dS^T Q, and
+// dQ^T = K^T dS^T into the S^T buffer the compute warps have just drained), so the compute warps'
+// exp/dS work on tile j overlaps the tensor core on tile j-1. TMEM: S^T|dQ^T (2x64) + dP^T
+// (2x64) + dV (128) + dK (128) = 512 columns. dQ^T rows are head-dim lanes: the flush into
+// dq_acc is one coalesced fp32 reduction per (query, 32 head dims) per warp.
+template <int HD>
+struct TcBwd2Cfg {
+  static constexpr int NC = HD / 64;
+  static constexpr int kTileBytes = 128 * 128;         // [128 rows][64] bf16
+  static constexpr int kKVBytes = NC * kTileBytes;     // [128 kv][HD]
+  static constexpr int kQBytes = NC * 64 * 128;        // [64 q][HD]
+  static constexpr int kPBytes = 128 * 128;            // [128 kv][64 q]
+  static constexpr int kDqBytes = 64 * HD * 4;             // dQ staging: [HD/32 boxes][64 q][32 hd] fp32
+  static constexpr int kSmem = 2 * kKVBytes + 4 * kQBytes + 4 * kPBytes + kDqBytes + 4 * 64 * 4 + 1024 + 256;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(320, 1)
+    fa_bwd_tc2_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
+                      const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_dq,
+                      const float* __restrict__ lse,
+                      const float* __restrict__ Dg, float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv,
+                      int s, int ht, float scale_log2, float scale) {
+  using Cfg = TcBwd2Cfg<HD>;
+  constexpr int NC = Cfg::NC, TB = Cfg::kTileBytes;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + Cfg::kKVBytes;
+  uint8_t* sQ = sV + Cfg::kKVBytes;          // [2][NC][64][64]
+  uint8_t* sdO = sQ + 2 * Cfg::kQBytes;      // [2][NC][64][64]
+  uint8_t* sPT = sdO + 2 * Cfg::kQBytes;     // [2][128 kv][64 q]
+  uint8_t* sdST = sPT + 2 * Cfg::kPBytes;    // [2][128 kv][64 q]
+  float* sDQ = reinterpret_cast<float*>(sdST + 2 * Cfg::kPBytes);  // [HD/32][64][32]
+  float* sL = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(sDQ) + Cfg::kDqBytes);  // [2][64]
+  float* sD = sL + 2 * 64;                                         // [2][64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * 64);
+  uint64_t* kv_full = bars;
+  uint64_t* qdo_full = bars + 1;    // [2]
+  uint64_t* qdo_empty = bars + 3;   // [2]
+  uint64_t* s_full = bars + 5;      // [2]
+  uint64_t* pds_full = bars + 7;    // [2]
+  uint64_t* pds_free = bars + 9;    // [2]
+  uint64_t* dq_full = bars + 11;    // [2]
+  uint64_t* dq_free = bars + 13;    // [2]
+  uint64_t* kdv_full = bars + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kvb = blockIdx.x;
+  const int b = blockIdx.y / ht, h = blockIdx.y % ht;
+  const int dt = ht * HD;
+  const int row0 = b * s;
+  const int kv0 = kvb * 128;
+  const int qt_first = kv0 / 64;          // 64-row query tiles at and after the diagonal
+  const int n_it = s / 64 - qt_first;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tm_kv);
+    ptx::tma_prefetch_desc(&tm_q);
+    ptx::tma_prefetch_desc(&tm_do);
+    ptx::mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&qdo_full[i], 1);
+      ptx::mbar_init(&qdo_empty[i], 1);
+      ptx::mbar_init(&s_full[i], 1);
+      ptx::mbar_init(&pds_full[i], 8);
+      ptx::mbar_init(&pds_free[i], 1);
+      ptx::mbar_init(&dq_full[i], 1);
+      ptx::mbar_init(&dq_free[i], 8);
+    }
+    ptx::mbar_init(kdv_full, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 256 + HD;  // tS/tdP: [2][64]
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(kv_full, 2 * Cfg::kKVBytes);
+      for (int c = 0; c < NC; ++c) {
+        ptx::tma_load_2d(sK + c * TB, &tm_kv, kv_full, dt + h * HD + 64 * c, row0 + kv0);
+        ptx::tma_load_2d(sV + c * TB, &tm_kv, kv_full, 2 * dt + h * HD + 64 * c, row0 + kv0);
+      }
+      for (int j = 0; j < n_it; ++j) {
+        const int bb = j & 1;
+        const int q0 = (qt_first + j) * 64;
+        WAIT(&qdo_empty[bb], ((j >> 1) & 1) ^ 1, 40);
+        ptx::mbar_arrive_expect_tx(&qdo_full[bb], 2 * Cfg::kQBytes);
+        for (int c = 0; c < NC; ++c) {
+          ptx::tma_load_2d(sQ + bb * Cfg::kQBytes + c * 8192, &tm_q, &qdo_full[bb], h * HD + 64 * c, row0 + q0);
+          ptx::tma_load_2d(sdO + bb * Cfg::kQBytes + c * 8192, &tm_do, &qdo_full[bb], h * HD + 64 * c, row0 + q0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 64, false, false);   // S^T, dP^T
+      constexpr uint32_t id_acc = ptx::idesc_bf16_f32(128, HD, false, true);  // dV, dK
+      constexpr uint32_t id_dq = ptx::idesc_bf16_f32(HD, 64, true, true);     // dQ^T
+      const uint32_t aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
+      WAIT(kv_full, 0, 41);
+      auto stage2 = [&](int i) {
+        const int bb = i & 1;
+        WAIT(&pds_full[bb], (i >> 1) & 1, 42);
+        ptx::tc_fence_after();
+        const uint32_t aQ = ptx::smem_u32(sQ + bb * Cfg::kQBytes), adO = ptx::smem_u32(sdO + bb * Cfg::kQBytes);
+        const uint32_t aP = ptx::smem_u32(sPT + bb * Cfg::kPBytes), adS = ptx::smem_u32(sdST + bb * Cfg::kPBytes);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {  // K = 64 query rows
+          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+          ptx::mma_bf16_ss(tdV, ptx::smem_desc_sw128(aP + kk * 32, 16, 1024),
+                           ptx::smem_desc_sw128(adO + kk * 2048, 8192, 1024), id_acc, acc);
+          ptx::mma_bf16_ss(tdK, ptx::smem_desc_sw128(adS + kk * 32, 16, 1024),
+                           ptx::smem_desc_sw128(aQ + kk * 2048, 8192, 1024), id_acc, acc);
+        }
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)  // K = 128 kv rows
+          ptx::mma_bf16_ss(tS + bb * 64, ptx::smem_desc_sw128(aK + kk * 2048, TB, 1024),
+                           ptx::smem_desc_sw128(adS + kk * 2048, TB, 1024), id_dq, kk > 0 ? 1u : 0u);
+        ptx::mma_commit(&dq_full[bb]);
+        ptx::mma_commit(&qdo_empty[bb]);
+        ptx::mma_commit(&pds_free[bb]);
+      };
+      for (int j = 0; j < n_it; ++j) {
+        const int bb = j & 1;
+        WAIT(&qdo_full[bb], (j >> 1) & 1, 43);
+        if (j >= 2) WAIT(&dq_free[bb], ((j >> 1) - 1) & 1, 44);  // dQ^T_{j-2} read out of tS[bb]
+        ptx::tc_fence_after();
+        const uint32_t aQ = ptx::smem_u32(sQ + bb * Cfg::kQBytes), adO = ptx::smem_u32(sdO + bb * Cfg::kQBytes);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t ak = (kk / 4) * TB + (kk % 4) * 32, aq = (kk / 4) * 8192 + (kk % 4) * 32;
+          ptx::mma_bf16_ss(tS + bb * 64, ptx::smem_desc_sw128(aK + ak, 16, 1024),
+                           ptx::smem_desc_sw128(aQ + aq, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+          ptx::mma_bf16_ss(tdP + bb * 64, ptx::smem_desc_sw128(aV + ak, 16, 1024),
+                           ptx::smem_desc_sw128(adO + aq, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+        }
+        ptx::mma_commit(&s_full[bb]);
+        if (j > 0) stage2(j - 1);
+      }
+      stage2(n_it - 1);
+      ptx::mma_commit(kdv_full);
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;   // which 32 query columns / 32-of-64 dQ columns
+    const int r = quarter * 32 + lane;  // TMEM lane: kv row (S^T, dP^T, dK, dV) or head dim (dQ^T)
+    const uint32_t lb = static_cast<uint32_t>(quarter * 32) << 16;
+    const int tid = threadIdx.x - 64;
+    const float* gL = lse + (static_cast<size_t>(b) * ht + h) * s;
+    const float* gD = Dg + (static_cast<size_t>(b) * ht + h) * s;
+    // dQ_i flush: TMEM (lane = head dim, column = query) -> smem staging [hd/32][q][32] (one
+    // 128B row per warp store) -> one TMA bulk reduce-add per 32-wide head-dim box into dq_acc.
+    auto readout = [&](int i) {
+      const int bb = i & 1;
+      const int q0 = (qt_first + i) * 64;
+      WAIT(&dq_full[bb], (i >> 1) & 1, 45);
+      ptx::tc_fence_after();
+      uint32_t v[32];
+      ptx::tmem_ld_32x32b_x32(tS + lb + bb * 64 + half * 32, v);
+      ptx::tmem_ld_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&dq_free[bb]);
+      if (tid == 0) ptx::bulk_wait_read0();  // previous flush has left the staging buffer
+      named_sync(2, 256);
+      float* box = sDQ + quarter * (64 * 32) + (half * 32) * 32 + lane;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) box[e * 32] = __uint_as_float(v[e]);
+      ptx::fence_proxy_async();
+      named_sync(2, 256);
+      if (tid == 0) {
+        for (int bx = 0; bx < HD / 32; ++bx)
+          ptx::tma_reduce_add_2d(&tm_dq, sDQ + bx * (64 * 32), h * HD + bx * 32, row0 + q0);
+        ptx::bulk_commit();
+      }
+    };
+    for (int j = 0; j < n_it; ++j) {
+      const int bb = j & 1;
+      const int q0 = (qt_first + j) * 64;
+      if (tid < 64) sL[bb * 64 + tid] = gL[q0 + tid];
+      else if (tid < 128) sD[bb * 64 + tid - 64] = gD[q0 + tid - 64];
+      named_sync(1, 256);
+      WAIT(&s_full[bb], (j >> 1) & 1, 46);
+      ptx::tc_fence_after();
+      const int qc = half * 32;
+      uint32_t sv[32], dv[32];
+      ptx::tmem_ld_32x32b_x32(tS + lb + bb * 64 + qc, sv);
+      ptx::tmem_ld_32x32b_x32(tdP + lb + bb * 64 + qc, dv);
+      ptx::tmem_ld_wait();
+      const float4* L4 = reinterpret_cast<const float4*>(sL + bb * 64 + qc);
+      const float4* D4 = reinterpret_cast<const float4*>(sD + bb * 64 + qc);
+      uint32_t pk[16], dk[16];
+#pragma unroll
+      for (int e4 = 0; e4 < 8; ++e4) {
+        const float4 l4 = L4[e4], d4 = D4[e4];
+        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dvv[4] = {d4.x, d4.y, d4.z, d4.w};
+        float pp[4], ds[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          pp[k] = ex2(fmaf(__uint_as_float(sv[4 * e4 + k]), scale_log2, -lv[k]));
+          ds[k] = pp[k] * (__uint_as_float(dv[4 * e4 + k]) - dvv[k]);
+        }
+        pk[2 * e4] = ptx::pack_bf16(pp[0], pp[1]);
+        pk[2 * e4 + 1] = ptx::pack_bf16(pp[2], pp[3]);
+        dk[2 * e4] = ptx::pack_bf16(ds[0], ds[1]);
+        dk[2 * e4 + 1] = ptx::pack_bf16(ds[2], ds[3]);
+      }
+      if (q0 + qc < kv0 + r) {  // near the diagonal: queries before this kv row see nothing
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (q0 + qc + e < kv0 + r) {
+            pk[e / 2] &= (e & 1) ? 0x0000FFFFu : 0xFFFF0000u;
+            dk[e / 2] &= (e & 1) ? 0x0000FFFFu : 0xFFFF0000u;
+          }
+      }
+      WAIT(&pds_free[bb], ((j >> 1) & 1) ^ 1, 47);  // stage 2 of tile j-2 is done with buffer bb
+      uint8_t* prow = sPT + bb * Cfg::kPBytes + r * 128;
+      uint8_t* drow = sdST + bb * Cfg::kPBytes + r * 128;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int off = ((half * 4 + u) ^ (r & 7)) * 16;
+        *reinterpret_cast<uint4*>(prow + off) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        *reinterpret_cast<uint4*>(drow + off) = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+      }
+      ptx::fence_proxy_async();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&pds_full[bb]);
+      if (j > 0) readout(j - 1);
+    }
+    readout(n_it - 1);
+    if (tid == 0) ptx::bulk_wait0();  // dQ reductions complete before the CTA retires
+    // dK (scaled) and dV rows of this KV block
+    WAIT(kdv_full, 0, 48);
+    ptx::tc_fence_after();
+    __nv_bfloat16* krow = dqkv + static_cast<size_t>(row0 + kv0 + r) * 3 * dt + dt + h * HD;
+    __nv_bfloat16* vrow = krow + dt;
+    constexpr int NCH = HD / 32;
+#pragma unroll 1
+    for (int c = half * (NCH / 2); c < (half + 1) * (NCH / 2); ++c) {
+      uint32_t kv[32], vv[32];
+      ptx::tmem_ld_32x32b_x32(tdK + lb + c * 32, kv);
+      ptx::tmem_ld_32x32b_x32(tdV + lb + c * 32, vv);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 a, bb2;
+        a.x = ptx::pack_bf16(__uint_as_float(kv[8 * q]) * scale, __uint_as_float(kv[8 * q + 1]) * scale);
+        a.y = ptx::pack_bf16(__uint_as_float(kv[8 * q + 2]) * scale, __uint_as_float(kv[8 * q + 3]) * scale);
+        a.z = ptx::pack_bf16(__uint_as_float(kv[8 * q + 4]) * scale, __uint_as_float(kv[8 * q + 5]) * scale);
+        a.w = ptx::pack_bf16(__uint_as_float(kv[8 * q + 6]) * scale, __uint_as_float(kv[8 * q + 7]) * scale);
+        bb2.x = ptx::pack_bf16(__uint_as_float(vv[8 * q]), __uint_as_float(vv[8 * q + 1]));
+        bb2.y = ptx::pack_bf16(__uint_as_float(vv[8 * q + 2]), __uint_as_float(vv[8 * q + 3]));
+        bb2.z = ptx::pack_bf16(__uint_as_float(vv[8 * q + 4]), __uint_as_float(vv[8 * q + 5]));
+        bb2.w = ptx::pack_bf16(__uint_as_float(vv[8 * q + 6]), __uint_as_float(vv[8 * q + 7]));
+        reinterpret_cast<uint4*>(krow + c * 32)[q] = a;
+        reinterpret_cast<uint4*>(vrow + c * 32)[q] = bb2;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int HD>
+int bwd_tc2(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* D,
+            float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st) {
+  using Cfg = TcBwd2Cfg<HD>;
+  static bool init = false;
+  if (!init) {
+    if (cudaFuncSetAttribute(fa_bwd_tc2_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
+        cudaSuccess)
+      return 3;
+    init = true;
+  }
+  const int dt = a.heads * HD;
+  const uint64_t M = static_cast<uint64_t>(a.batch) * a.seq;
+  CUtensorMap tkv, tq, tdo, tdq;
+  if (!make_tmap_bf16(&tkv, qkv, 3 * static_cast<uint64_t>(dt), M, 3 * dt, 64, 128)) return 3;
+  if (!make_tmap_bf16(&tq, qkv, 3 * static_cast<uint64_t>(dt), M, 3 * dt, 64, 64)) return 3;
+  if (!make_tmap_bf16(&tdo, dout, static_cast<uint64_t>(dt), M, dt, 64, 64)) return 3;
+  if (!make_tmap_f32(&tdq, dq_acc, static_cast<uint64_t>(dt), M, dt, 32, 64)) return 3;
+  dim3 grid(a.seq / 128, a.batch * a.heads);
+  const float scale = 1.f / sqrtf(static_cast<float>(HD));
+  fa_bwd_tc2_kernel<HD><<<grid, 320, Cfg::kSmem, st>>>(tkv, tq, tdo, tdq, lse, D, dq_acc, dqkv, a.seq, a.heads,
+                                                        scale * kLog2e, scale);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
 template <int HD>
 int bwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* D,
            float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st) {
@@ -634,7 +934,7 @@ int flash_attn_bwd_tc_main(const AttnShape& a, const __nv_bfloat16* qkv, const _
   if (a.seq % 128 != 0) return 1;
   switch (a.head_dim) {
     case 64: return bwd_tc<64>(a, qkv, dout, lse, D, dq_acc, dqkv, st);
-    case 128: return bwd_tc<128>(a, qkv, dout, lse, D, dq_acc, dqkv, st);
+    case 128: return bwd_tc2<128>(a, qkv, dout, lse, D, dq_acc, dqkv, st);
     default: return 1;
   }
 }
