@@ -245,7 +245,7 @@ void Stage::allocate() {
     row_loss_ = static_cast<float*>(alloc(M * 4));
   }
   loss_acc_ = static_cast<float*>(alloc(4));
-  overlap_rs_ = cfg_.dp > 1;
+  overlap_rs_ = true;  // per-bucket RS -> Adam -> AG pipelined on a side stream during backward
   if (overlap_rs_) {
     cudaStreamCreateWithFlags(&comm_st_, cudaStreamNonBlocking);
     bucket_ev_.resize(buckets_.size());
@@ -606,37 +606,36 @@ void Stage::backward_op(int mb, bf16* dh) {
 }
 
 // ------------------------------------------------------------------------------ step
-void Stage::optimizer_step() {
+// Adam on this rank's slice of one bucket, on `st` (fp32 master/m/v, writes the bf16 copy).
+void Stage::adam_bucket(int bucket, cudaStream_t st) {
+  const Bucket& b = buckets_[bucket];
+  const int64_t n = b.len / cfg_.dp;
+  if (!n) return;
   AdamArgs a;
   a.lr = opts_.lr, a.beta1 = opts_.beta1, a.beta2 = opts_.beta2, a.eps = opts_.eps, a.weight_decay = opts_.weight_decay;
   a.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(opts_.beta1), step_no_));
   a.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(opts_.beta2), step_no_));
-  KScope prof(this, K_ADAM, 0, 30.0 * shard_);
-  if (cfg_.dp == 1) {  // owned slices == whole buckets == the flat buffer: one launch
-    a.n = P_, a.master = master_, a.m = adam_m_, a.v = adam_v_, a.grad = grads_, a.param = params_;
-    ck(adam_step(a, st_), "adam");
-    return;
-  }
-  for (const Bucket& b : buckets_) {
-    const int64_t n = b.len / cfg_.dp;
-    if (!n) continue;
-    const int64_t own = b.off + comms_.me.d * n;
-    a.n = n, a.master = master_ + b.master_off, a.m = adam_m_ + b.master_off, a.v = adam_v_ + b.master_off;
-    a.grad = grads_ + own, a.param = params_ + own;
-    ck(adam_step(a, st_), "adam");
-  }
+  const int64_t own = b.off + comms_.me.d * n;
+  a.n = n, a.master = master_ + b.master_off, a.m = adam_m_ + b.master_off, a.v = adam_v_ + b.master_off;
+  a.grad = grads_ + own, a.param = params_ + own;
+  ck(adam_step(a, st), "adam");
 }
 
-// Overlapped ZeRO-1 reduce-scatter: the bucket's gradients are final on the compute stream; the
-// comm stream waits for them and reduce-scatters in place while backward continues.
+// The bucket's gradients are final on the compute stream (last microbatch): on the side stream,
+// reduce-scatter them over DP (in place), run Adam on the owned slice and allgather the updated
+// bf16 slices — all while backward continues with earlier layers (whose parameters are
+// untouched by this bucket's update).
 void Stage::grads_ready(int bucket) {
-  if (!overlap_rs_) return;
   const Bucket& b = buckets_[bucket];
   if (!b.len) return;
   cudaEventRecord(bucket_ev_[bucket], st_);
   cudaStreamWaitEvent(comm_st_, bucket_ev_[bucket], 0);
   try {
-    comms_.dp_reduce_scatter_f32(grads_ + b.off, b.len / cfg_.dp, comm_st_);
+    if (bucket == 0 && cfg_.pp > 1 && (first_ || last_))
+      comms_.emb_allreduce_f32(grads_ + slot_offset(0), static_cast<size_t>(Vt_) * d_, comm_st_);
+    if (cfg_.dp > 1) comms_.dp_reduce_scatter_f32(grads_ + b.off, b.len / cfg_.dp, comm_st_);
+    adam_bucket(bucket, comm_st_);
+    if (cfg_.dp > 1) comms_.dp_allgather_bf16(params_ + b.off, b.len / cfg_.dp, comm_st_);
   } catch (const CommError& e) {
     throw StepError{e.code, e.msg};
   }
@@ -690,26 +689,11 @@ void Stage::step() {
       ++launches_;
       comms_.pp_exchange(pending, pending_peer, nullptr, -1, n_act, st_);
     }
-    cudaStream_t emb_st = overlap_rs_ ? comm_st_ : st_;
-    if (overlap_rs_) {
-      cudaEventRecord(bucket_ev_[0], st_);
-      cudaStreamWaitEvent(comm_st_, bucket_ev_[0], 0);
-    }
-    if (cfg_.pp > 1 && (first_ || last_))
-      comms_.emb_allreduce_f32(grads_ + slot_offset(0), static_cast<size_t>(Vt_) * d_, emb_st);
-    if (overlap_rs_) {
-      {
-        KScope prof(this, K_COMM_DP);
-        if (buckets_[0].len) comms_.dp_reduce_scatter_f32(grads_ + buckets_[0].off, buckets_[0].len / cfg_.dp, comm_st_);
-        cudaEventRecord(comm_done_, comm_st_);
-        cudaStreamWaitEvent(st_, comm_done_, 0);  // the compute stream waits for all reduce-scatters
-      }
-    }
-    optimizer_step();
-    if (cfg_.dp > 1) {
-      KScope prof(this, K_COMM_DP);
-      for (const Bucket& b : buckets_)
-        if (b.len) comms_.dp_allgather_bf16(params_ + b.off, b.len / cfg_.dp, st_);
+    grads_ready(0);  // embeddings (tied wte: after the first/last-stage allreduce)
+    {
+      KScope prof(this, K_ADAM);  // exposed tail of the side-stream optimizer pipeline
+      cudaEventRecord(comm_done_, comm_st_);
+      cudaStreamWaitEvent(st_, comm_done_, 0);
     }
     comms_.world_allreduce_f32(loss_acc_, 1, st_);
   } catch (const CommError& e) {

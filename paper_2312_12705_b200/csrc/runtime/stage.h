@@ -129,7 +129,7 @@ class Stage {
   void layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2);
   void head_and_loss(int slot, bool with_grad);
   void head_bwd(bf16* dh_out);
-  void optimizer_step();
+  void adam_bucket(int bucket, cudaStream_t st);
   void grads_ready(int bucket);  // last microbatch's grads of `bucket` final: start its reduce-scatter
   void prepare_tokens(int mb, int slot);
 
