@@ -408,7 +408,8 @@ int gemm_bf16(const GemmParams& p, cudaStream_t stream) {
   // CTA pairs (256 x 256 tiles) when the problem yields at least one full wave of pairs;
   // otherwise single-CTA 128 x BN tiles with the widest BN that still fills the machine.
   const bool pair_ok = p.M % 256 == 0 && p.N % 256 == 0;
-  const bool pair_wave = pair_ok && (p.M / 256) * (p.N / 256) >= num_sms() / 2;
+  // >= ~85% of the pairs busy in a single wave beats 1.7 waves of single-CTA tiles
+  const bool pair_wave = pair_ok && (p.M / 256) * (p.N / 256) * 8 >= (num_sms() / 2) * 7 - 8;
   if (g_force_cg == 2 ? pair_ok : (g_force_cg == 0 && pair_wave)) return dispatch_epi<256, 2>(p, stream);
   const bool n256 = (p.N % 256 == 0) && (p.M / kBM) * (p.N / 256) >= num_sms();
   if (n256) return dispatch_epi<256, 1>(p, stream);
