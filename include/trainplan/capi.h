@@ -72,6 +72,10 @@ int tp_validate(const tp_model_spec* m, const tp_parallel_config* c, int num_nod
 /* Per-device pipeline order (pipesim.cpp:31-91): kind 0 GPipe, 1 1F1B, 2 interleaved. Writes
  * up to cap ops as (backward, microbatch, chunk) triples; *n = op count. */
 int tp_pipeline_order(int kind, int p, int m, int v, int device, int* ops, int cap, int* n);
+/* Executable per-device plan Stage::step() runs for that order (runtime/pipe_exec.h): 6 ints per
+ * action = {kind 0 fwd / 1 bwd, microbatch, chunk, activation slot, gradient buffer, flags}
+ * (flags: 1 recv input, 2 send output, 4 LM head now, 8 deferred LM head, 16 last microbatch). */
+int tp_pipeline_actions(int p, int m, int v, int device, int dh_ring, int forward_only, int* out, int cap, int* n);
 /* Rank layout (perf.cpp:15-20): rank = t + tp*(p + pp*d). out = {t, p, d}. */
 int tp_rank_coords(int rank, int tp, int pp, int dp, int out[3]);
 

@@ -75,6 +75,7 @@ SIGNATURES: dict[str, tuple] = {
     "tp_model_flops": (_i, [C.POINTER(ModelSpec), C.c_int64, _i, _i, C.POINTER(C.c_double)]),
     "tp_validate": (_i, [C.POINTER(ModelSpec), C.POINTER(ParallelConfig), _i, _i, _i, C.POINTER(Validation)]),
     "tp_pipeline_order": (_i, [_i, _i, _i, _i, _i, C.POINTER(_i), _i, C.POINTER(_i)]),
+    "tp_pipeline_actions": (_i, [_i, _i, _i, _i, _i, _i, C.POINTER(_i), _i, C.POINTER(_i)]),
     "tp_rank_coords": (_i, [_i, _i, _i, _i, C.POINTER(_i)]),
     "tp_gemm_bf16": (_i, [_i, _i, _i, _vp, _i, _i, _vp, _i, _i, _vp, _i, _i, _vp, _vp, _vp, _i, _i, _vp]),
     "tp_gemm_force_cta_group": (_i, [_i]),
@@ -175,6 +176,19 @@ def pipeline_order(kind: int, p: int, m: int, v: int, device: int) -> list[tuple
     n = _i()
     check(load().tp_pipeline_order(kind, p, m, v, device, buf, cap, C.byref(n)))
     return [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]) for i in range(n.value)]
+
+
+PA_RECV, PA_SEND, PA_HEAD, PA_HEAD_LATE, PA_LAST_MB = 1, 2, 4, 8, 16
+
+
+def pipeline_actions(p: int, m: int, v: int, device: int, dh_ring: int = 2, forward_only: bool = False) -> list[dict]:
+    """The executable plan Stage::step() runs on `device` (runtime/pipe_exec.h)."""
+    cap = 2 * m * v + 8
+    buf = (_i * (6 * cap))()
+    n = _i()
+    check(load().tp_pipeline_actions(p, m, v, device, dh_ring, int(forward_only), buf, cap, C.byref(n)))
+    keys = ("kind", "mb", "chunk", "slot", "dh", "flags")
+    return [dict(zip(keys, buf[6 * i:6 * i + 6])) for i in range(n.value)]
 
 
 def rank_coords(rank: int, tp: int, pp: int, dp: int) -> tuple[int, int, int]:

@@ -186,7 +186,9 @@ void validate_kernels(const ModelSpec& model, const ParallelConfig& cfg, Validat
   if (cfg.precision != Precision::BF16)
     hard("precision", "the B200 step computes in bf16 (fp32 master weights and grads)");
   if (cfg.zero_stage > 1) hard("zero_stage", "ZeRO stages 2/3 are out of scope (north_star: ZeRO-1)");
-  if (cfg.interleave_v != 1) hard("interleave_v", "interleaved 1F1B is not executed yet");
+  if (cfg.interleave_v > 1 && cfg.pp < 2) hard("interleave_v", "interleave_v > 1 needs pipeline parallelism (pp >= 2)");
+  if (cfg.interleave_v > 1 && cfg.pp >= 1 && model.num_layers % (cfg.pp * cfg.interleave_v) != 0)
+    hard("interleave_v", "num_layers must be divisible by pp*interleave_v (equal model chunks)");
 }
 
 RankCoords rank_coords(int rank, const ParallelConfig& c) {

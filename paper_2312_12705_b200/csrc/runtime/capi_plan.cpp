@@ -3,6 +3,7 @@
 #include <exception>
 #include <stdexcept>
 
+#include "runtime/pipe_exec.h"
 #include "runtime/status.h"
 #include "trainplan/capi.h"
 #include "trainplan/core.hpp"
@@ -101,6 +102,18 @@ int tp_pipeline_order(int kind, int p, int m, int v, int device, int* ops, int c
       ops[3 * i] = order[i].backward ? 1 : 0;
       ops[3 * i + 1] = order[i].microbatch;
       ops[3 * i + 2] = order[i].chunk;
+    }
+  });
+}
+
+int tp_pipeline_actions(int p, int m, int v, int device, int dh_ring, int forward_only, int* out, int cap, int* n) {
+  return guarded("tp_pipeline_actions", [&] {
+    auto acts = gptb200::pipeline_actions(p, m, v, device, dh_ring, forward_only != 0);
+    *n = static_cast<int>(acts.size());
+    for (int i = 0; i < *n && i < cap; ++i) {
+      const auto& a = acts[i];
+      int* o = out + 6 * i;
+      o[0] = a.kind, o[1] = a.microbatch, o[2] = a.chunk, o[3] = a.slot, o[4] = a.dh, o[5] = a.flags;
     }
   });
 }

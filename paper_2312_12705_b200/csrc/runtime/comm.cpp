@@ -9,7 +9,10 @@ void nccl_check(ncclResult_t r, const char* what) {
 }
 
 Comms::~Comms() {
-  for (ncclComm_t* c : {&emb_comm, &dp_comm, &pp_comm, &tp_comm, &world_comm})
+  // ncclCommDestroy synchronises with the peers: destroy in creation order on every rank
+  for (ncclComm_t& c : links_in_order) ncclCommDestroy(c);
+  links_in_order.clear();
+  for (ncclComm_t* c : {&emb_comm, &dp_comm, &tp_comm, &world_comm})
     if (*c) {
       ncclCommDestroy(*c);
       *c = nullptr;
@@ -29,7 +32,19 @@ void Comms::init(const trainplan::ParallelConfig& cfg, int rank_, int world_, co
     nccl_check(ncclCommSplit(world_comm, color, key, out, nullptr), what);
   };
   split(me.p + pp * me.d, me.t, &tp_comm, "split tp");
-  split(me.t + tp * me.d, me.p, &pp_comm, "split pp");
+  if (pp > 1) {
+    for (int dir = 0; dir < 2; ++dir)
+      for (int k = 0; k < pp; ++k) {
+        const int dst = dir == 0 ? (k + 1) % pp : (k + pp - 1) % pp;
+        const bool wrap = dir == 0 ? k == pp - 1 : k == 0;
+        if (wrap && cfg.interleave_v == 1) continue;  // same decision on every rank
+        ncclComm_t unused = nullptr;
+        ncclComm_t* out = me.p == k ? &link_send[dir] : (me.p == dst ? &link_recv[dir] : &unused);
+        const bool member = me.p == k || me.p == dst;
+        split(member ? me.t + tp * me.d : NCCL_SPLIT_NOCOLOR, me.p == k ? 0 : 1, out, "split pipeline link");
+        if (member) links_in_order.push_back(*out);
+      }
+  }
   split(me.t + tp * me.p, me.d, &dp_comm, "split dp");
   const bool edge = pp > 1 && (me.p == 0 || me.p == pp - 1);
   split(edge ? me.t + tp * me.d : NCCL_SPLIT_NOCOLOR, me.p, &emb_comm, "split emb");
@@ -70,13 +85,14 @@ void Comms::world_allreduce_f32(float* buf, size_t n, cudaStream_t st) const {
   nccl_check(ncclAllReduce(buf, buf, n, ncclFloat, ncclSum, world_comm, st), "world allreduce");
 }
 
-void Comms::pp_exchange(const void* send, int send_peer, void* recv, int recv_peer, size_t n,
-                        cudaStream_t st) const {
-  if (pp == 1 || (!send && !recv)) return;
-  nccl_check(ncclGroupStart(), "group start");
-  if (send) nccl_check(ncclSend(send, n, ncclBfloat16, send_peer, pp_comm, st), "pp send");
-  if (recv) nccl_check(ncclRecv(recv, n, ncclBfloat16, recv_peer, pp_comm, st), "pp recv");
-  nccl_check(ncclGroupEnd(), "group end");
+void Comms::pp_send(const void* buf, size_t n, int dir, cudaStream_t st) const {
+  if (!link_send[dir]) throw CommError{TP_ERR_INVALID, "pipeline send on a missing link"};
+  nccl_check(ncclSend(buf, n, ncclBfloat16, 1, link_send[dir], st), "pp send");
+}
+
+void Comms::pp_recv(void* buf, size_t n, int dir, cudaStream_t st) const {
+  if (!link_recv[dir]) throw CommError{TP_ERR_INVALID, "pipeline recv on a missing link"};
+  nccl_check(ncclRecv(buf, n, ncclBfloat16, 0, link_recv[dir], st), "pp recv");
 }
 
 }  // namespace gptb200

@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <string>
+#include <vector>
 
 #include "trainplan/core.hpp"
 
@@ -32,7 +33,12 @@ class Comms {
   int tp = 1, pp = 1, dp = 1;
   ncclComm_t world_comm = nullptr;
   ncclComm_t tp_comm = nullptr;   // ranks sharing (p, d), ordered by t
-  ncclComm_t pp_comm = nullptr;   // ranks sharing (t, d), ordered by p
+  // Pipeline ring links, one 2-rank communicator per (link, direction) so every FIFO carries one
+  // kind of message and is driven from one stream: [0] activations p -> p+1, [1] gradients p -> p-1
+  // (mod pp; the wrap links pp-1 -> 0 / 0 -> pp-1 exist only for interleaved schedules).
+  ncclComm_t link_send[2] = {nullptr, nullptr};
+  ncclComm_t link_recv[2] = {nullptr, nullptr};
+  std::vector<ncclComm_t> links_in_order;  // creation order (identical on all ranks) for teardown
   ncclComm_t dp_comm = nullptr;   // ranks sharing (t, p), ordered by d
   ncclComm_t emb_comm = nullptr;  // first & last stage of (t, d) when pp > 1 (tied embedding)
 
@@ -43,9 +49,10 @@ class Comms {
   void dp_allgather_bf16(void* buf, size_t n_per_rank, cudaStream_t st) const;       // in place
   void emb_allreduce_f32(float* buf, size_t n, cudaStream_t st) const;
   void world_allreduce_f32(float* buf, size_t n, cudaStream_t st) const;
-  // Pipeline p2p inside one ncclGroup: optional send to stage p+dir_send, optional recv.
-  void pp_exchange(const void* send, int send_peer_stage, void* recv, int recv_peer_stage,
-                   size_t n_bf16, cudaStream_t st) const;
+  // Pipeline p2p over the ring links: dir 0 = activations (to p+1 / from p-1), dir 1 = gradients
+  // (to p-1 / from p+1).
+  void pp_send(const void* buf, size_t n_bf16, int dir, cudaStream_t st) const;
+  void pp_recv(void* buf, size_t n_bf16, int dir, cudaStream_t st) const;
 };
 
 void nccl_check(ncclResult_t r, const char* what);

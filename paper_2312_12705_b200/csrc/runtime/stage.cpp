@@ -8,6 +8,8 @@
 #include "runtime/stage.h"
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels/attention.h"
@@ -74,8 +76,9 @@ Stage::Stage(const trainplan::ModelSpec& model, const trainplan::ParallelConfig&
   d_ = model.hidden_size;
   V_ = model.vocab_size;
   s_ = model.seq_length;
-  Ll_ = L_ / cfg.pp;
-  layer0_ = comms_.me.p * Ll_;
+  v_ = std::max(cfg.interleave_v, 1);
+  Lc_ = L_ / (cfg.pp * v_);
+  Ll_ = Lc_ * v_;
   dt_ = d_ / cfg.tp;
   ht_ = model.num_heads / cfg.tp;
   hd_ = d_ / model.num_heads;
@@ -86,13 +89,25 @@ Stage::Stage(const trainplan::ModelSpec& model, const trainplan::ParallelConfig&
   first_ = comms_.me.p == 0;
   last_ = comms_.me.p == cfg.pp - 1;
   ckpt_ = cfg.checkpoint_activations;
-  nslots_ = std::min(m_, cfg.pp - comms_.me.p);
+  plan_ = pipeline_actions(cfg.pp, m_, v_, comms_.me.p, kDhRing, false);
+  eval_plan_ = pipeline_actions(cfg.pp, m_, v_, comms_.me.p, kDhRing, true);
+  nslots_ = pipeline_slots(plan_);
   build_layout();
   allocate();
 }
 
 Stage::~Stage() {
   if (st_) cudaStreamSynchronize(st_);
+  for (int i = 0; i < 2; ++i)
+    if (send_st_[i]) {
+      cudaStreamSynchronize(send_st_[i]);
+      cudaStreamDestroy(send_st_[i]);
+      cudaEventDestroy(send_done_ev_[i]);
+    }
+  for (auto& e : slot_send_ev_) cudaEventDestroy(e);
+  for (auto& e : dh_send_ev_)
+    if (e) cudaEventDestroy(e);
+  if (op_ev_) cudaEventDestroy(op_ev_);
   if (comm_st_) {
     cudaStreamSynchronize(comm_st_);
     for (auto& e : bucket_ev_) cudaEventDestroy(e);
@@ -162,7 +177,7 @@ void Stage::build_layout() {
   if (first_) add(1, s_, d, s_, 0, 0, 0, d, std_base, 0.f);
   close_bucket();  // bucket 0: embeddings (possibly empty)
   for (int l = 0; l < Ll_; ++l) {
-    const int b = 2 + kPerLayer * (layer0_ + l);
+    const int b = 2 + kPerLayer * glayer(l);
     add(b + LN1G, d, 1, d, 0, 0, 0, 1, 0.f, 1.f);
     add(b + LN1B, d, 1, d, 0, 0, 0, 1, 0.f, 0.f);
     add(b + WQKV, 3 * dt, d, dt, d, t * dt, 0, d, std_base, 0.f);
@@ -212,10 +227,10 @@ void Stage::allocate() {
   };
   slots_act_.resize(nslots_);
   for (auto& S : slots_act_) {
-    S.h.resize(Ll_ + 1);
+    S.h.resize(Lc_ + 1);
     for (auto& h : S.h) h = static_cast<bf16*>(alloc(M * d * 2));
     if (!ckpt_) {
-      S.acts.resize(Ll_);
+      S.acts.resize(Lc_);
       for (auto& A : S.acts) layer_acts(A);
     }
     S.inputs = static_cast<int32_t*>(alloc(M * 4));
@@ -223,8 +238,7 @@ void Stage::allocate() {
   }
   if (ckpt_) layer_acts(scratch_);
   tmp_md_ = static_cast<bf16*>(alloc(M * d * 2));
-  dh_[0] = static_cast<bf16*>(alloc(M * d * 2));
-  dh_[1] = static_cast<bf16*>(alloc(M * d * 2));
+  for (auto& b : dh_) b = static_cast<bf16*>(alloc(M * d * 2));
   dy_ = static_cast<bf16*>(alloc(M * d * 2));
   du_ = static_cast<bf16*>(alloc(M * 4 * dt * 2));
   dm_ = static_cast<bf16*>(alloc(M * d * 2));
@@ -245,6 +259,16 @@ void Stage::allocate() {
     row_loss_ = static_cast<float*>(alloc(M * 4));
   }
   loss_acc_ = static_cast<float*>(alloc(4));
+  if (cfg_.pp > 1) {
+    for (int i = 0; i < 2; ++i) {
+      cudaStreamCreateWithFlags(&send_st_[i], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&send_done_ev_[i], cudaEventDisableTiming);
+    }
+    slot_send_ev_.resize(nslots_);
+    for (auto& e : slot_send_ev_) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    for (auto& e : dh_send_ev_) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&op_ev_, cudaEventDisableTiming);
+  }
   overlap_rs_ = true;  // per-bucket RS -> Adam -> AG pipelined on a side stream during backward
   if (overlap_rs_) {
     cudaStreamCreateWithFlags(&comm_st_, cudaStreamNonBlocking);
@@ -260,18 +284,18 @@ const ParamSlot* Stage::slot(int tid) const {
 }
 
 Stage::LayerW Stage::w(int l) const {
-  const int b = 2 + kPerLayer * (layer0_ + l);
+  const int b = 2 + kPerLayer * glayer(l);
   auto p = [&](int j) { return params_ + slot(b + j)->offset; };
   return {p(LN1G), p(LN1B), p(WQKV), p(BQKV), p(WO), p(BO), p(LN2G), p(LN2B), p(W1), p(B1), p(W2), p(B2)};
 }
 
 Stage::LayerG Stage::gr(int l) const {
-  const int b = 2 + kPerLayer * (layer0_ + l);
+  const int b = 2 + kPerLayer * glayer(l);
   auto p = [&](int j) { return grads_ + slot(b + j)->offset; };
   return {p(LN1G), p(LN1B), p(WQKV), p(BQKV), p(WO), p(BO), p(LN2G), p(LN2B), p(W1), p(B1), p(W2), p(B2)};
 }
 
-LayerActs& Stage::acts_for(int slot, int l) { return ckpt_ ? scratch_ : slots_act_[slot].acts[l]; }
+LayerActs& Stage::acts_for(int slot, int l) { return ckpt_ ? scratch_ : slots_act_[slot].acts[l % Lc_]; }
 
 void Stage::init_params() {
   cudaMemsetAsync(grads_, 0, P_ * sizeof(float), st_);
@@ -364,9 +388,10 @@ static DropKey drop_key(const TrainOptions& o, int step, int layer, int site, in
   return k;
 }
 
-void Stage::layer_fwd(int l, LayerActs& A, const bf16* hin, bf16* hout, bool fuse_next, int slot) {
-  const int lg = layer0_ + l;
+void Stage::layer_fwd(int l, LayerActs& A, const bf16* hin, bf16* hout, int slot) {
+  const int lg = glayer(l);
   const LayerW W = w(l);
+  const bool next_in_chunk = (l + 1) % Lc_ != 0;
   const int64_t sample0 = static_cast<int64_t>(comms_.me.d) * (cfg_.gbs / cfg_.dp) +
                           static_cast<int64_t>(cur_mb_) * mbs_;
   gemm_fwd(A.a, W.wqkv, W.bqkv, A.qkv, M_, 3 * dt_, d_);
@@ -393,8 +418,8 @@ void Stage::layer_fwd(int l, LayerActs& A, const bf16* hin, bf16* hout, bool fus
   r2.y = tmp_md_, r2.bias = W.b2, r2.resid = A.hmid;
   r2.drop = drop_key(opts_, step_no_, lg, 1, sample0, s_, d_);
   r2.h_out = hout;
-  if (fuse_next) {
-    if (l + 1 < Ll_) {
+  if (next_in_chunk || last_vs(l / Lc_)) {
+    if (next_in_chunk) {
       LayerActs& N = acts_for(slot, l + 1);
       const LayerW Wn = w(l + 1);
       r2.gamma = Wn.ln1g, r2.beta = Wn.ln1b, r2.ln_out = N.a, r2.mean = N.mu1, r2.rstd = N.rs1;
@@ -411,7 +436,7 @@ void Stage::layer_fwd(int l, LayerActs& A, const bf16* hin, bf16* hout, bool fus
 }
 
 void Stage::layer_recompute(int l, LayerActs& A, const bf16* hin) {
-  const int lg = layer0_ + l;
+  const int lg = glayer(l);
   const LayerW W = w(l);
   const int64_t sample0 = static_cast<int64_t>(comms_.me.d) * (cfg_.gbs / cfg_.dp) +
                           static_cast<int64_t>(cur_mb_) * mbs_;
@@ -452,17 +477,17 @@ void Stage::tp_allreduce(bf16* buf) {
   }
 }
 
-void Stage::forward_op(int mb, bool with_loss) {
+void Stage::forward_op(int mb, int c, int slot, bool head_now) {
   cur_mb_ = mb;
-  const int slot = mb % nslots_;
   Slot& S = slots_act_[slot];
-  if (first_ || last_) prepare_tokens(mb, slot);
-  LayerActs& A0 = acts_for(slot, 0);
-  const LayerW W0 = w(0);
+  if (first_vs(c) || last_vs(c)) prepare_tokens(mb, slot);
+  const int l0 = c * Lc_;
+  LayerActs& A0 = acts_for(slot, l0);
+  const LayerW W0 = w(l0);
   ResidLnArgs r;
   r.rows = M_, r.d = d_, r.seq = s_;
   r.gamma = W0.ln1g, r.beta = W0.ln1b, r.ln_out = A0.a, r.mean = A0.mu1, r.rstd = A0.rs1;
-  if (first_) {
+  if (first_vs(c)) {
     ck(embed_lookup(S.inputs, M_, params_ + slot_offset(0), comms_.me.t * Vt_, Vt_, d_, tmp_md_, st_), "embed");
     tp_allreduce(tmp_md_);
     const int64_t sample0 = static_cast<int64_t>(comms_.me.d) * (cfg_.gbs / cfg_.dp) + static_cast<int64_t>(mb) * mbs_;
@@ -476,11 +501,24 @@ void Stage::forward_op(int mb, bool with_loss) {
     KScope prof(this, K_NORM, 0, 8.0 * M_ * d_);
     ck(resid_ln_fwd(r, st_), "embed+ln1");
   }
-  for (int l = 0; l < Ll_; ++l) layer_fwd(l, acts_for(slot, l), S.h[l], S.h[l + 1], (l + 1 < Ll_) || last_, slot);
-  if (last_) head_and_loss(slot, with_loss);
+  for (int l = 0; l < Lc_; ++l) layer_fwd(l0 + l, acts_for(slot, l0 + l), S.h[l], S.h[l + 1], slot);
+  if (last_vs(c) && head_now) head_and_loss(slot);
 }
 
-void Stage::head_and_loss(int slot, bool /*with_grad*/) {
+void Stage::final_ln(const bf16* h) {
+  ResidLnArgs r;
+  r.rows = M_, r.d = d_, r.seq = s_;
+  r.resid = h;
+  r.gamma = params_ + slot_offset(2 + kPerLayer * L_);
+  r.beta = params_ + slot_offset(2 + kPerLayer * L_ + 1);
+  r.ln_out = hf_, r.mean = muf_, r.rstd = rsf_;
+  KScope prof(this, K_NORM, 0, 4.0 * M_ * d_);
+  ck(resid_ln_fwd(r, st_), "final ln");
+}
+
+// hf_ (final LN output of this microbatch) -> vocab-parallel logits -> CE; logits_ is left holding
+// the loss-scaled softmax - onehot for head_bwd.
+void Stage::head_and_loss(int slot) {
   Slot& S = slots_act_[slot];
   gemm_fwd(hf_, params_ + slot_offset(0), nullptr, logits_, M_, Vt_, d_);
   ck(xent_stats(logits_, M_, Vt_, S.labels, comms_.me.t * Vt_, xstats_, st_), "xent stats");
@@ -503,7 +541,7 @@ void Stage::head_bwd(bf16* dh) {
 }
 
 void Stage::layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2) {
-  const int lg = layer0_ + l;
+  const int lg = glayer(l);
   const LayerW W = w(l);
   const LayerG G = gr(l);
   const bool drop_on = opts_.dropout > 0.f;
@@ -550,11 +588,11 @@ void Stage::layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2)
   c.x = hin, c.dy = dm_, c.resid_grad = dh, c.gamma = W.ln1g, c.mean = A.mu1, c.rstd = A.rs1;
   c.dx = dh;
   c.dgamma = G.ln1g, c.dbeta = G.ln1b, c.workspace = ws_;
-  if (l > 0) {  // preceding branch: MLP of layer l-1 on this stage
+  if (l % Lc_ > 0) {  // preceding branch: MLP of layer l-1 in this chunk
     c.drop = drop_key(opts_, step_no_, lg - 1, 1, sample0, s_, d_);
     c.dxd = drop_on ? dy_ : dh;
     c.dbias = gr(l - 1).b2;
-  } else if (first_) {  // preceding branch: embedding dropout
+  } else if (first_vs(l / Lc_)) {  // preceding branch: embedding dropout
     c.drop = drop_key(opts_, step_no_, kEmbedLayer, 2, sample0, s_, d_);
     c.dxd = drop_on ? dy_ : dh;
   }
@@ -564,27 +602,28 @@ void Stage::layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2)
   }
 }
 
-void Stage::backward_op(int mb, bf16* dh) {
+void Stage::backward_op(int mb, int c, int slot, bf16* dh, bool head_late) {
   cur_mb_ = mb;
-  const int slot = mb % nslots_;
   Slot& S = slots_act_[slot];
   const bool drop_on = opts_.dropout > 0.f;
+  const int l_last = (c + 1) * Lc_ - 1;
   const int64_t sample0 = static_cast<int64_t>(comms_.me.d) * (cfg_.gbs / cfg_.dp) + static_cast<int64_t>(mb) * mbs_;
   LnBwdArgs b;
   b.rows = M_, b.d = d_, b.workspace = ws_;
-  b.drop = drop_key(opts_, step_no_, layer0_ + Ll_ - 1, 1, sample0, s_, d_);
+  b.drop = drop_key(opts_, step_no_, glayer(l_last), 1, sample0, s_, d_);
   b.dxd = drop_on ? dy_ : dh;
-  b.dbias = gr(Ll_ - 1).b2;
-  if (last_) {
-    if (ckpt_) {
-      // hf_ / logits_ are still those of this microbatch (1F1B: F(k) is followed by B(k))
+  b.dbias = gr(l_last).b2;
+  if (last_vs(c)) {
+    if (head_late) {  // another microbatch's forward ran since ours: rebuild the head input
+      final_ln(S.h[Lc_]);
+      head_and_loss(slot);
     }
     head_bwd(dh);
     const int f = 2 + kPerLayer * L_;
-    b.x = S.h[Ll_], b.dy = tmp_md_, b.gamma = params_ + slot_offset(f), b.mean = muf_, b.rstd = rsf_;
+    b.x = S.h[Lc_], b.dy = tmp_md_, b.gamma = params_ + slot_offset(f), b.mean = muf_, b.rstd = rsf_;
     b.dx = dh, b.dgamma = grads_ + slot_offset(f), b.dbeta = grads_ + slot_offset(f + 1);
   } else {
-    b.resid_grad = dh;  // received gradient of the stage output
+    b.resid_grad = dh;  // received gradient of the chunk output
     b.dx = nullptr;
     if (!drop_on) b.dxd = nullptr;
   }
@@ -592,13 +631,14 @@ void Stage::backward_op(int mb, bf16* dh) {
     KScope prof(this, K_NORM, 0, 10.0 * M_ * d_);
     ck(ln_bwd(b, st_), "final ln / stage-boundary bwd");
   }
-  for (int l = Ll_ - 1; l >= 0; --l) {
-    LayerActs& A = acts_for(slot, l);
-    if (ckpt_) layer_recompute(l, A, S.h[l]);
-    layer_bwd(l, A, S.h[l], dh, drop_on ? dy_ : dh);
-    if (in_last_bwd_) grads_ready(layer_bucket_[l]);
+  for (int l = Lc_ - 1; l >= 0; --l) {
+    const int li = c * Lc_ + l;
+    LayerActs& A = acts_for(slot, li);
+    if (ckpt_) layer_recompute(li, A, S.h[l]);
+    layer_bwd(li, A, S.h[l], dh, drop_on ? dy_ : dh);
+    if (in_last_bwd_) grads_ready(layer_bucket_[li]);
   }
-  if (first_) {
+  if (first_vs(c)) {
     const bf16* g = drop_on ? dy_ : dh;
     ck(embed_bwd(S.inputs, M_, g, comms_.me.t * Vt_, Vt_, d_, s_, grads_ + slot_offset(0), grads_ + slot_offset(1), st_),
        "embed bwd");
@@ -641,54 +681,60 @@ void Stage::grads_ready(int bucket) {
   }
 }
 
+// Pipeline p2p of one plan action (runtime/pipe_exec.h): receive on the compute stream before the
+// op; send on the direction's side stream after it, recording the buffer's send-done event.
+void Stage::pp_recv(void* buf, int dir) {
+  ++launches_;
+  KScope prof(this, K_COMM_PP);
+  comms_.pp_recv(buf, static_cast<size_t>(M_) * d_, dir, st_);
+}
+
+void Stage::pp_send(const void* buf, int dir, cudaEvent_t done) {
+  ++launches_;
+  cudaEventRecord(op_ev_, st_);
+  cudaStreamWaitEvent(send_st_[dir], op_ev_, 0);
+  comms_.pp_send(buf, static_cast<size_t>(M_) * d_, dir, send_st_[dir]);
+  cudaEventRecord(done, send_st_[dir]);
+}
+
+void Stage::run_action(const PipeAction& a) {
+  static const bool trace = std::getenv("GPTB200_TRACE_PIPE") != nullptr;
+  if (trace)
+    std::fprintf(stderr, "[stage %d] %s mb %d chunk %d slot %d dh %d flags %d\n", comms_.me.p,
+                 a.kind == PA_FWD ? "F" : "B", a.microbatch, a.chunk, a.slot, a.dh, a.flags);
+  if (a.kind == PA_FWD) {
+    Slot& S = slots_act_[a.slot];
+    if (cfg_.pp > 1) cudaStreamWaitEvent(st_, slot_send_ev_[a.slot], 0);  // h[Lc] of the slot's last use sent
+    if (a.flags & PA_RECV) pp_recv(S.h[0], 0);
+    forward_op(a.microbatch, a.chunk, a.slot, (a.flags & PA_HEAD) != 0);
+    if (a.flags & PA_SEND) pp_send(S.h[Lc_], 0, slot_send_ev_[a.slot]);
+  } else {
+    bf16* dh = dh_[a.dh];
+    if (cfg_.pp > 1) cudaStreamWaitEvent(st_, dh_send_ev_[a.dh], 0);
+    if (a.flags & PA_RECV) pp_recv(dh, 1);
+    in_last_bwd_ = (a.flags & PA_LAST_MB) != 0;
+    backward_op(a.microbatch, a.chunk, a.slot, dh, (a.flags & PA_HEAD_LATE) != 0);
+    in_last_bwd_ = false;
+    if (a.flags & PA_SEND) pp_send(dh, 1, dh_send_ev_[a.dh]);
+  }
+}
+
+void Stage::join_sends() {
+  for (int i = 0; i < 2; ++i)
+    if (send_st_[i]) {
+      cudaEventRecord(send_done_ev_[i], send_st_[i]);
+      cudaStreamWaitEvent(st_, send_done_ev_[i], 0);
+    }
+}
+
 void Stage::step() {
   ++step_no_;
   launches_ = 0;
   cudaMemsetAsync(grads_, 0, P_ * sizeof(float), st_);
   cudaMemsetAsync(loss_acc_, 0, sizeof(float), st_);
-  const auto ops = trainplan::pipeline_order(ScheduleKind::OneF1B, cfg_.pp, m_, 1, comms_.me.p);
-  const int last_bwd_mb = ops.back().microbatch;
-  const size_t n_act = static_cast<size_t>(M_) * d_;
-  const void* pending = nullptr;
-  int pending_peer = -1, dh_idx = 0;
   try {
-    for (const PipeOp& op : ops) {
-      void* recv = nullptr;
-      int recv_peer = -1;
-      if (!op.backward && !first_) {
-        recv = slots_act_[op.microbatch % nslots_].h[0];
-        recv_peer = comms_.me.p - 1;
-      } else if (op.backward && !last_) {
-        recv = dh_[dh_idx];
-        recv_peer = comms_.me.p + 1;
-      }
-      if (pending || recv) {
-        ++launches_;
-        KScope prof(this, K_COMM_PP);
-        comms_.pp_exchange(pending, pending_peer, recv, recv_peer, n_act, st_);
-      }
-      pending = nullptr;
-      if (!op.backward) {
-        forward_op(op.microbatch, true);
-        if (!last_) {
-          pending = slots_act_[op.microbatch % nslots_].h[Ll_];
-          pending_peer = comms_.me.p + 1;
-        }
-      } else {
-        in_last_bwd_ = op.microbatch == last_bwd_mb;
-        backward_op(op.microbatch, dh_[dh_idx]);
-        in_last_bwd_ = false;
-        if (!first_) {
-          pending = dh_[dh_idx];
-          pending_peer = comms_.me.p - 1;
-        }
-        dh_idx ^= 1;
-      }
-    }
-    if (pending) {
-      ++launches_;
-      comms_.pp_exchange(pending, pending_peer, nullptr, -1, n_act, st_);
-    }
+    for (const PipeAction& a : plan_) run_action(a);
+    join_sends();
     grads_ready(0);  // embeddings (tied wte: after the first/last-stage allreduce)
     {
       KScope prof(this, K_ADAM);  // exposed tail of the side-stream optimizer pipeline
@@ -710,13 +756,9 @@ float Stage::read_loss() {
 
 float Stage::eval_loss() {
   cudaMemsetAsync(loss_acc_, 0, sizeof(float), st_);
-  const size_t n_act = static_cast<size_t>(M_) * d_;
   try {
-    for (int mb = 0; mb < m_; ++mb) {
-      if (!first_) comms_.pp_exchange(nullptr, -1, slots_act_[mb % nslots_].h[0], comms_.me.p - 1, n_act, st_);
-      forward_op(mb, true);
-      if (!last_) comms_.pp_exchange(slots_act_[mb % nslots_].h[Ll_], comms_.me.p + 1, nullptr, -1, n_act, st_);
-    }
+    for (const PipeAction& a : eval_plan_) run_action(a);
+    join_sends();
     comms_.world_allreduce_f32(loss_acc_, 1, st_);
   } catch (const CommError& e) {
     throw StepError{e.code, e.msg};

@@ -13,6 +13,7 @@
 
 #include "kernels/ops.h"
 #include "runtime/comm.h"
+#include "runtime/pipe_exec.h"
 #include "trainplan/core.hpp"
 
 namespace gptb200 {
@@ -122,16 +123,22 @@ class Stage {
   LayerG gr(int l) const;
   LayerActs& acts_for(int slot, int l);
 
-  void forward_op(int mb, bool with_loss);
-  void backward_op(int mb, bf16* dh);
-  void layer_fwd(int l, LayerActs& A, const bf16* hin, bf16* hout, bool fuse_next_ln, int slot);
+  // One pipeline op on chunk c (layers [c*Lc, (c+1)*Lc) of this device; virtual stage c*pp + p).
+  void forward_op(int mb, int c, int slot, bool head_now);
+  void backward_op(int mb, int c, int slot, bf16* dh, bool head_late);
+  void layer_fwd(int li, LayerActs& A, const bf16* hin, bf16* hout, int slot);
   void layer_recompute(int l, LayerActs& A, const bf16* hin);
   void layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2);
-  void head_and_loss(int slot, bool with_grad);
+  void head_and_loss(int slot);
+  void final_ln(const bf16* h);  // final LayerNorm of the last virtual stage into hf_/muf_/rsf_
   void head_bwd(bf16* dh_out);
   void adam_bucket(int bucket, cudaStream_t st);
   void grads_ready(int bucket);  // last microbatch's grads of `bucket` final: start its reduce-scatter
   void prepare_tokens(int mb, int slot);
+  void run_action(const PipeAction& a);
+  void pp_recv(void* buf, int dir);
+  void pp_send(const void* buf, int dir, cudaEvent_t done);
+  void join_sends();
 
   void gemm_fwd(const bf16* X, const bf16* W, const bf16* bias, bf16* Y, int M, int N, int K, int epi = 0,
                 bf16* C2 = nullptr);
@@ -165,7 +172,11 @@ class Stage {
   size_t dev_bytes_ = 0;
 
   // shape
-  int L_ = 0, Ll_ = 0, layer0_ = 0, d_ = 0, dt_ = 0, ht_ = 0, hd_ = 0, V_ = 0, Vt_ = 0, s_ = 0;
+  // Ll_ local layers = v_ chunks of Lc_ layers; local layer li is global layer glayer(li).
+  int glayer(int li) const { return ((li / Lc_) * cfg_.pp + comms_.me.p) * Lc_ + li % Lc_; }
+  bool first_vs(int c) const { return first_ && c == 0; }
+  bool last_vs(int c) const { return last_ && c == v_ - 1; }
+  int L_ = 0, Ll_ = 0, Lc_ = 0, v_ = 1, d_ = 0, dt_ = 0, ht_ = 0, hd_ = 0, V_ = 0, Vt_ = 0, s_ = 0;
   int mbs_ = 1, M_ = 0, m_ = 1, nslots_ = 1;
   bool first_ = true, last_ = true, ckpt_ = false;
   int step_no_ = 0;
@@ -189,7 +200,14 @@ class Stage {
   std::vector<Slot> slots_act_;
   LayerActs scratch_;  // checkpointing recompute buffers
   int32_t* tokens_ = nullptr;
-  bf16 *tmp_md_ = nullptr, *dh_[2] = {nullptr, nullptr}, *dy_ = nullptr, *du_ = nullptr, *dm_ = nullptr,
+  // pipeline p2p: sends on one side stream per direction, buffer-reuse events
+  cudaStream_t send_st_[2] = {nullptr, nullptr};
+  cudaEvent_t op_ev_ = nullptr, send_done_ev_[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> slot_send_ev_;
+  cudaEvent_t dh_send_ev_[kDhRing] = {};
+  std::vector<PipeAction> plan_, eval_plan_;
+  bf16* dh_[kDhRing] = {};
+  bf16 *tmp_md_ = nullptr, *dy_ = nullptr, *du_ = nullptr, *dm_ = nullptr,
        *do_ = nullptr, *dqkv_ = nullptr;
   float *attn_D_ = nullptr, *dq_acc_ = nullptr, *ws_ = nullptr;
   bf16* hf_ = nullptr;

@@ -44,7 +44,7 @@ def main():
     nid = idf.read_bytes()
     spec = T.ModelSpec(c["L"], c["d"], c["a"], c["V"], c["s"])
     cfg = T.ParallelConfig(tp=c["tp"], pp=c["pp"], dp=c["dp"], mbs=c["mbs"], gbs=c["gbs"], zero_stage=1,
-                           checkpoint_activations=c.get("ckpt", 0))
+                           checkpoint_activations=c.get("ckpt", 0), interleave_v=c.get("v", 1))
     opts = T.TrainOptions(seed=1234, dropout=c.get("dropout", 0.0), lr=1e-3, weight_decay=0.01)
     sess = T.Session(spec, cfg, opts, rank=a.rank, world=a.world, device=a.rank, nccl_id=nid)
     sess.init_params()

@@ -44,12 +44,12 @@ def _slice(full, info):
     return full[np.ix_(grow, gcol)] if info["cols"] > 1 else full[grow]
 
 
-def run_layout(tp, pp, dp, L=2, d=256, a=4, V=1024, s=128, mbs=1, gbs=None, ckpt=0, dropout=0.0):
+def run_layout(tp, pp, dp, L=2, d=256, a=4, V=1024, s=128, mbs=1, gbs=None, ckpt=0, dropout=0.0, v=1):
     world = tp * pp * dp
     if _ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
     gbs = gbs or mbs * dp * 2
-    c = dict(L=L, d=d, a=a, V=V, s=s, tp=tp, pp=pp, dp=dp, mbs=mbs, gbs=gbs, ckpt=ckpt, dropout=dropout)
+    c = dict(L=L, d=d, a=a, V=V, s=s, tp=tp, pp=pp, dp=dp, mbs=mbs, gbs=gbs, ckpt=ckpt, dropout=dropout, v=v)
     with tempfile.TemporaryDirectory() as td:
         procs = [subprocess.Popen([sys.executable, str(ROOT / "tests" / "mp_worker.py"), "--cfg", json.dumps(c),
                                    "--rank", str(r), "--world", str(world), "--out", td],
@@ -144,6 +144,24 @@ def test_tp2_dp2_ckpt():
 
 def test_pp2_dp2():
     run_layout(tp=1, pp=2, dp=2, gbs=8)
+
+
+def test_pp2_interleaved_v2():
+    # 4 layers = 2 devices x 2 chunks: device 0 holds layers {0, 2}, device 1 {1, 3}
+    run_layout(tp=1, pp=2, dp=1, L=4, gbs=4, v=2)
+
+
+def test_pp2_interleaved_v2_dropout_late_head():
+    # m == p: every forward runs before the first backward, so the LM head is deferred
+    run_layout(tp=1, pp=2, dp=1, L=4, gbs=2, v=2, dropout=0.1)
+
+
+def test_tp2_pp2_interleaved_v2_ckpt():
+    run_layout(tp=2, pp=2, dp=1, L=4, gbs=4, v=2, ckpt=1)
+
+
+def test_pp2_dp2_interleaved_v2():
+    run_layout(tp=1, pp=2, dp=2, L=4, gbs=8, v=2)
 
 
 def test_config1_tp2_pp2_dp2():
