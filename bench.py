@@ -50,6 +50,8 @@ WORKLOADS = {
     # BASELINE config 4: 175B-shape layer slice (8 layers) TP4 x PP2 1F1B, m = 16, checkpointing.
     "gpt-175b-slice-tp4pp2": (8, 12288, 96, 51200, 2048, 1, 4, 2, True, 0.1, 16),
     "gpt-175b-slice-tp4": (4, 12288, 96, 51200, 2048, 1, 4, 1, True, 0.1, 8),
+    # the same slice's pipeline on 4 GPUs (TP2 x PP2; --interleave 2 for the interleaved 1F1B).
+    "gpt-175b-slice-tp2pp2": (8, 12288, 96, 51200, 2048, 1, 2, 2, True, 0.1, 16),
     # BASELINE config 5: 1T-shape layer slice (4 layers, 160 heads, hd 160) TP8 / TP4 x PP2.
     "gpt-1t-slice-tp8": (4, 25600, 160, 51200, 2048, 1, 8, 1, True, 0.1, 8),
     "gpt-1t-slice-tp4pp2": (4, 25600, 160, 51200, 2048, 1, 4, 2, True, 0.1, 8),
@@ -187,7 +189,7 @@ def workload_config(args, world):
     dp = max(world // (tp * pp), 1)
     return {"workload": f"{args.workload}: GPT L{L} d{d} a{a} V{V} s{s}, fwd+bwd+ZeRO-1 Adam step",
             "global_batch": mbs * nmb * dp, "seq_len": s, "micro_batch": mbs, "microbatches": nmb,
-            "parallelism": f"tp{tp}.pp{pp}.dp{dp}",
+            "parallelism": f"tp{tp}.pp{pp}.dp{dp}" + (f".v{args.interleave}" if args.interleave > 1 else ""),
             "zero_stage": 1, "activation_checkpointing": ckpt, "hidden_dropout": drop, "attention_dropout": 0.0,
             "flash_attention": True, "grad_accum_dtype": "fp32",
             "l2": "per-step working set (tens of GB) far larger than the 126 MB L2; no flush needed"}
@@ -202,6 +204,7 @@ def main():
     ap.add_argument("--workload", default="gpt-1.4b", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--interleave", type=int, default=1, help="model chunks per pipeline stage (interleaved 1F1B)")
     args = ap.parse_args()
     rank, local, world = env_rank()
     if world != args.gpus:
@@ -219,7 +222,8 @@ def main():
     dp = world // (tp * pp)
     gbs = mbs * nmb * dp
     spec = T.ModelSpec(L, d, a, V, s)
-    cfg = T.ParallelConfig(tp=tp, pp=pp, dp=dp, mbs=mbs, gbs=gbs, zero_stage=1, checkpoint_activations=int(ckpt))
+    cfg = T.ParallelConfig(tp=tp, pp=pp, dp=dp, mbs=mbs, gbs=gbs, zero_stage=1, checkpoint_activations=int(ckpt),
+                           interleave_v=args.interleave)
     opts = T.TrainOptions(seed=1234, dropout=drop, lr=1e-4, weight_decay=0.0)
     nid = share_nccl_id(rank, world)
     sess = T.Session(spec, cfg, opts, rank=rank, world=world, device=local, nccl_id=nid)

@@ -188,6 +188,13 @@ typedef struct tp_kernel_times {
 int tp_session_time_steps(tp_session* s, int steps, int profile, float* ms, tp_kernel_times* kt);
 /* Max over all ranks of *v (NCCL on the world communicator); identity when world == 1. */
 int tp_session_allreduce_max(tp_session* s, float* v);
+/* TP allreduce of one [mbs*s, d] bf16 activation buffer (the Megatron f/g operator), for tests and
+ * microbenchmarks: mode 0 = automatic (NVLS in-switch reduction kernel when the TP group is one
+ * multicast domain), 1 = ncclAllReduce. in/out are mbs*s*d bf16 bit patterns on the host. */
+int tp_session_debug_tp_allreduce(tp_session* s, const uint16_t* in, uint16_t* out, int mode);
+/* Average device ms per allreduce over `iters` (ctas 0 = default grid); *nvls = 1 if the
+ * session's TP group uses the NVLS kernel. */
+int tp_session_bench_tp_allreduce(tp_session* s, int iters, int mode, int ctas, float* ms, int* nvls);
 
 #ifdef __cplusplus
 }

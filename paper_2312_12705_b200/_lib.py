@@ -106,6 +106,8 @@ SIGNATURES: dict[str, tuple] = {
     "tp_session_buckets": (_i, [_vp, C.POINTER(_i64), _i, C.POINTER(_i)]),
     "tp_session_time_steps": (_i, [_vp, _i, _i, C.POINTER(_f), C.POINTER(KernelTimes)]),
     "tp_session_allreduce_max": (_i, [_vp, C.POINTER(_f)]),
+    "tp_session_debug_tp_allreduce": (_i, [_vp, _vp, _vp, _i]),
+    "tp_session_bench_tp_allreduce": (_i, [_vp, _i, _i, _i, C.POINTER(_f), C.POINTER(_i)]),
 }
 
 _lib = None
@@ -297,6 +299,19 @@ class Session:
         x = _f(v)
         check(self._lib.tp_session_allreduce_max(self.h, C.byref(x)))
         return x.value
+
+    def debug_tp_allreduce(self, x, mode: int = 0):
+        """x: uint16 bf16 bit patterns of one [mbs*s, d] buffer; returns the TP-summed buffer."""
+        import numpy as np
+        x = np.ascontiguousarray(x, dtype=np.uint16)
+        out = np.empty_like(x)
+        check(self._lib.tp_session_debug_tp_allreduce(self.h, x.ctypes.data, out.ctypes.data, mode))
+        return out
+
+    def bench_tp_allreduce(self, iters: int = 20, mode: int = 0, ctas: int = 0):
+        ms, nv = _f(), _i()
+        check(self._lib.tp_session_bench_tp_allreduce(self.h, iters, mode, ctas, C.byref(ms), C.byref(nv)))
+        return ms.value, bool(nv.value)
 
     def read_flat(self, which: int, offset: int, n: int):
         import numpy as np

@@ -28,6 +28,9 @@ COMMON = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
 _TORCH_NCCL = Path(sys.prefix) / "lib" / f"python{sys.version_info.major}.{sys.version_info.minor}" / \
     "site-packages" / "nvidia" / "nccl" / "lib"
 NCCL_DIR = _TORCH_NCCL if (_TORCH_NCCL / "libnccl.so.2").exists() else Path("/usr/lib/x86_64-linux-gnu")
+# headers of the same NCCL (2.28: symmetric windows + device API used by the NVLS TP kernels)
+if (NCCL_DIR.parent / "include" / "nccl_device.h").exists():
+    COMMON.insert(COMMON.index("-I/usr/local/cuda/include"), f"-I{NCCL_DIR.parent / 'include'}")
 LINK = ["-shared", "-lcudart", f"-L{NCCL_DIR}", "-l:libnccl.so.2", "-lgomp",
         "-Xlinker", f"-rpath={NCCL_DIR}", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
 

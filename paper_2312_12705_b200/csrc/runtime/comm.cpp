@@ -9,6 +9,10 @@ void nccl_check(ncclResult_t r, const char* what) {
 }
 
 Comms::~Comms() {
+  if (tp_nvls) {
+    nvls_destroy(tp_nvls, tp_comm);
+    tp_nvls = nullptr;
+  }
   // ncclCommDestroy synchronises with the peers: destroy in creation order on every rank
   for (ncclComm_t& c : links_in_order) ncclCommDestroy(c);
   links_in_order.clear();
@@ -50,8 +54,20 @@ void Comms::init(const trainplan::ParallelConfig& cfg, int rank_, int world_, co
   split(edge ? me.t + tp * me.d : NCCL_SPLIT_NOCOLOR, me.p, &emb_comm, "split emb");
 }
 
-void Comms::tp_allreduce_bf16(void* buf, size_t n, cudaStream_t st) const {
+void* Comms::init_tp_symmetric(size_t bytes) {
+  if (tp == 1) return nullptr;
+  tp_nvls = nvls_create(tp_comm, bytes, 148);
+  return nvls_base(tp_nvls);
+}
+
+void Comms::tp_allreduce_bf16(void* buf, size_t n, cudaStream_t st, int mode) const {
   if (tp == 1) return;
+  if (mode == 0 && tp_nvls) {
+    const int r = nvls_allreduce_bf16(tp_nvls, buf, n, st, tp_nvls_ctas);
+    if (r == 0) return;
+    if (r == 2) throw CommError{TP_ERR_CUDA, "NVLS allreduce launch failed"};
+    // r == 1: buffer outside the window -> NCCL
+  }
   nccl_check(ncclAllReduce(buf, buf, n, ncclBfloat16, ncclSum, tp_comm, st), "tp allreduce");
 }
 

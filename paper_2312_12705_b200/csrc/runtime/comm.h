@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include "kernels/tp_nvls.h"
 #include "trainplan/core.hpp"
 
 namespace gptb200 {
@@ -42,8 +43,15 @@ class Comms {
   ncclComm_t dp_comm = nullptr;   // ranks sharing (t, p), ordered by d
   ncclComm_t emb_comm = nullptr;  // first & last stage of (t, d) when pp > 1 (tied embedding)
 
+  // NVLS symmetric window on the TP communicator (tp > 1 and one multicast domain); buffers
+  // carved from it are allreduced by the in-switch reduction kernel, others by ncclAllReduce.
+  NvlsContext* tp_nvls = nullptr;
+  void* init_tp_symmetric(size_t bytes);  // collective over TP; returns the window base or nullptr
+  int tp_nvls_ctas = 0;                    // 0 = default grid
+
   // Collectives on `st` (no-ops for singleton groups). Throw CommError on failure.
-  void tp_allreduce_bf16(void* buf, size_t n, cudaStream_t st) const;
+  // mode: 0 = automatic (NVLS kernel when buf is in the window), 1 = force ncclAllReduce.
+  void tp_allreduce_bf16(void* buf, size_t n, cudaStream_t st, int mode = 0) const;
   void tp_allgather_f32(const float* send, float* recv, size_t n_per_rank, cudaStream_t st) const;
   void dp_reduce_scatter_f32(float* buf, size_t n_per_rank, cudaStream_t st) const;  // in place
   void dp_allgather_bf16(void* buf, size_t n_per_rank, cudaStream_t st) const;       // in place

@@ -196,4 +196,15 @@ int tp_session_allreduce_max(tp_session* s, float* v) {
   return run("tp_session_allreduce_max", [&] { *v = s->stage->allreduce_max(*v); });
 }
 
+int tp_session_debug_tp_allreduce(tp_session* s, const uint16_t* in, uint16_t* out, int mode) {
+  return run("tp_session_debug_tp_allreduce", [&] { s->stage->debug_tp_allreduce(in, out, mode); });
+}
+
+int tp_session_bench_tp_allreduce(tp_session* s, int iters, int mode, int ctas, float* ms, int* nvls) {
+  return run("tp_session_bench_tp_allreduce", [&] {
+    *ms = s->stage->bench_tp_allreduce(iters, mode, ctas);
+    *nvls = s->stage->tp_uses_nvls() ? 1 : 0;
+  });
+}
+
 }  // extern "C"

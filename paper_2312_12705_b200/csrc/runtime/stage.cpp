@@ -237,7 +237,13 @@ void Stage::allocate() {
     S.labels = static_cast<int32_t*>(alloc(M * 4));
   }
   if (ckpt_) layer_acts(scratch_);
-  tmp_md_ = static_cast<bf16*>(alloc(M * d * 2));
+  // The two TP-allreduced buffers live in the NVLS symmetric window when the TP group has one.
+  if (void* sym = comms_.init_tp_symmetric(2 * M * d * 2)) {
+    tmp_md_ = static_cast<bf16*>(sym);
+    dm_ = tmp_md_ + M * d;
+  } else {
+    tmp_md_ = static_cast<bf16*>(alloc(M * d * 2));
+    }
   for (auto& b : dh_) b = static_cast<bf16*>(alloc(M * d * 2));
   dy_ = static_cast<bf16*>(alloc(M * d * 2));
   du_ = static_cast<bf16*>(alloc(M * 4 * dt * 2));
@@ -870,6 +876,42 @@ float Stage::time_steps(int steps, bool profile, KernelTimes* kt) {
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   return ms;
+}
+
+void Stage::debug_tp_allreduce(const uint16_t* in, uint16_t* out, int mode) {
+  const size_t n = static_cast<size_t>(M_) * d_;
+  cudaMemcpyAsync(tmp_md_, in, n * 2, cudaMemcpyHostToDevice, st_);
+  try {
+    comms_.tp_allreduce_bf16(tmp_md_, n, st_, mode);
+  } catch (const CommError& e) {
+    throw StepError{e.code, e.msg};
+  }
+  cudaMemcpyAsync(out, tmp_md_, n * 2, cudaMemcpyDeviceToHost, st_);
+  sync();
+}
+
+float Stage::bench_tp_allreduce(int iters, int mode, int ctas) {
+  const size_t n = static_cast<size_t>(M_) * d_;
+  comms_.tp_nvls_ctas = ctas;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  try {
+    for (int i = 0; i < 3; ++i) comms_.tp_allreduce_bf16(tmp_md_, n, st_, mode);
+    cudaEventRecord(a, st_);
+    for (int i = 0; i < iters; ++i) comms_.tp_allreduce_bf16(tmp_md_, n, st_, mode);
+    cudaEventRecord(b, st_);
+  } catch (const CommError& e) {
+    comms_.tp_nvls_ctas = 0;
+    throw StepError{e.code, e.msg};
+  }
+  sync();
+  comms_.tp_nvls_ctas = 0;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return ms / std::max(iters, 1);
 }
 
 float Stage::allreduce_max(float v) {

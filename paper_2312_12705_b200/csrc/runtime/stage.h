@@ -101,6 +101,11 @@ class Stage {
   // With profile, every launch is bracketed too and summed per KernelClass into *kt.
   float time_steps(int steps, bool profile, KernelTimes* kt);
   float allreduce_max(float v);
+  // TP allreduce of the [M, d] bf16 activation buffer (test / microbenchmark hooks).
+  // mode 0 = automatic (NVLS when available), 1 = ncclAllReduce. in/out: M*d bf16 bit patterns.
+  void debug_tp_allreduce(const uint16_t* in, uint16_t* out, int mode);
+  float bench_tp_allreduce(int iters, int mode, int ctas);
+  bool tp_uses_nvls() const { return comms_.tp_nvls != nullptr; }
 
  private:
   struct LayerW {
