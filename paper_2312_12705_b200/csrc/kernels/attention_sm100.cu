@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // all 32 lanes: uniform descriptors, one elected lane issues
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBM, kBN, false, false);
       constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(kBM, HD, false, true);
       const uint32_t q_addr = ptx::smem_u32(sQ), p_addr = ptx::smem_u32(sP);
@@ -162,10 +162,10 @@ __global__ void __launch_bounds__(320, 1)
         for (int kk = 0; kk < kBN / 16; ++kk) {
           const uint64_t a = ptx::smem_desc_sw128(pa + (kk / 4) * Cfg::kTileBytes + (kk % 4) * 32, 16, 1024);
           const uint64_t bd = ptx::smem_desc_sw128(v_addr + kk * 2048, Cfg::kTileBytes, 1024);
-          ptx::mma_bf16_ss(tO, a, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          ptx::mma_bf16_ss_w(tO, a, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
-        ptx::mma_commit(&pv_done[pb]);
-        ptx::mma_commit(&v_empty[st]);
+        ptx::mma_commit_w(&pv_done[pb]);
+        ptx::mma_commit_w(&v_empty[st]);
       };
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j % ST, buf = j & 1;
@@ -176,11 +176,11 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk / 4) * Cfg::kTileBytes + (kk % 4) * 32;
-          ptx::mma_bf16_ss(tmem + buf * kBN, ptx::smem_desc_sw128(q_addr + off, 16, 1024),
+          ptx::mma_bf16_ss_w(tmem + buf * kBN, ptx::smem_desc_sw128(q_addr + off, 16, 1024),
                            ptx::smem_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
         }
-        ptx::mma_commit(&s_full[buf]);
-        ptx::mma_commit(&k_empty[st]);
+        ptx::mma_commit_w(&s_full[buf]);
+        ptx::mma_commit_w(&k_empty[st]);
         if (j > 0) issue_pv(j - 1);
       }
       issue_pv(n_tiles - 1);
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // all 32 lanes: uniform descriptors, one elected lane issues
       constexpr uint32_t id_sq = ptx::idesc_bf16_f32(128, 128, false, false);  // S^T, dP^T
       constexpr uint32_t id_acc = ptx::idesc_bf16_f32(128, HD, false, true);   // dV, dK
       constexpr uint32_t id_dq = ptx::idesc_bf16_f32(128, HD, true, true);     // dQ
@@ -433,12 +433,12 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk / 4) * TB + (kk % 4) * 32;
-          ptx::mma_bf16_ss(tS, ptx::smem_desc_sw128(aK + off, 16, 1024), ptx::smem_desc_sw128(aQ + off, 16, 1024),
+          ptx::mma_bf16_ss_w(tS, ptx::smem_desc_sw128(aK + off, 16, 1024), ptx::smem_desc_sw128(aQ + off, 16, 1024),
                            id_sq, kk > 0 ? 1u : 0u);
-          ptx::mma_bf16_ss(tdP, ptx::smem_desc_sw128(aV + off, 16, 1024), ptx::smem_desc_sw128(adO + off, 16, 1024),
+          ptx::mma_bf16_ss_w(tdP, ptx::smem_desc_sw128(aV + off, 16, 1024), ptx::smem_desc_sw128(adO + off, 16, 1024),
                            id_sq, kk > 0 ? 1u : 0u);
         }
-        ptx::mma_commit(sdp_full);
+        ptx::mma_commit_w(sdp_full);
         WAIT(pds_full, it & 1, 25);
         ptx::tc_fence_after();
 #pragma unroll
@@ -447,19 +447,19 @@ __global__ void __launch_bounds__(320, 1)
           const uint64_t bdo = ptx::smem_desc_sw128(adO + kk * 2048, TB, 1024);
           const uint64_t bq = ptx::smem_desc_sw128(aQ + kk * 2048, TB, 1024);
           const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
-          ptx::mma_bf16_ss(tdV, ptx::smem_desc_sw128(aPT + aoff, 16, 1024), bdo, id_acc, acc);
-          ptx::mma_bf16_ss(tdK, ptx::smem_desc_sw128(adST + aoff, 16, 1024), bq, id_acc, acc);
+          ptx::mma_bf16_ss_w(tdV, ptx::smem_desc_sw128(aPT + aoff, 16, 1024), bdo, id_acc, acc);
+          ptx::mma_bf16_ss_w(tdK, ptx::smem_desc_sw128(adST + aoff, 16, 1024), bq, id_acc, acc);
         }
 #pragma unroll
         for (int kk = 0; kk < 128 / 16; ++kk) {  // K = 128 kv rows
-          ptx::mma_bf16_ss(tS, ptx::smem_desc_sw128(adST + kk * 2048, TB, 1024),
+          ptx::mma_bf16_ss_w(tS, ptx::smem_desc_sw128(adST + kk * 2048, TB, 1024),
                            ptx::smem_desc_sw128(aK + kk * 2048, TB, 1024), id_dq, kk > 0 ? 1u : 0u);
         }
-        ptx::mma_commit(dq_full);
-        ptx::mma_commit(qdo_empty);
-        ptx::mma_commit(pds_free);
+        ptx::mma_commit_w(dq_full);
+        ptx::mma_commit_w(qdo_empty);
+        ptx::mma_commit_w(pds_free);
       }
-      ptx::mma_commit(kdv_full);
+      ptx::mma_commit_w(kdv_full);
     }
   } else {
     // 8 compute warps: warp w owns TMEM lane quarter (w & 3) and one half of the 128 query
@@ -591,6 +591,10 @@ __global__ void __launch_bounds__(320, 1)
 // exp/dS work on tile j overlaps the tensor core on tile j-1. TMEM: S^T|dQ^T (2x64) + dP^T
 // (2x64) + dV (128) + dK (128) = 512 columns. dQ^T rows are head-dim lanes: the flush into
 // dq_acc is one coalesced fp32 reduction per (query, 32 head dims) per warp.
+// 16 warps, register-rebalanced per warpgroup (setmaxnreg): WG0 = TMA producer (warp 0) + MMA
+// issuer (warp 1); WG1-2 = P/dS compute (TMEM lane quarter x 32-query half); WG3 = dQ flush, one
+// warp per 32 head dims, each staging its own [64 q][32 hd] box and issuing its own TMA
+// reduce-add, so the flush of tile j-1 runs concurrently with the P/dS math of tile j.
 template <int HD>
 struct TcBwd2Cfg {
   static constexpr int NC = HD / 64;
@@ -598,15 +602,14 @@ struct TcBwd2Cfg {
   static constexpr int kKVBytes = NC * kTileBytes;     // [128 kv][HD]
   static constexpr int kQBytes = NC * 64 * 128;        // [64 q][HD]
   static constexpr int kPBytes = 128 * 128;            // [128 kv][64 q]
-  static constexpr int kDqBytes = 64 * HD * 4;             // dQ staging: [HD/32 boxes][64 q][32 hd] fp32
-  static constexpr int kSmem = 2 * kKVBytes + 4 * kQBytes + 4 * kPBytes + kDqBytes + 4 * 64 * 4 + 1024 + 256;
+  static constexpr int QST = 3;                        // Q/dO (+ LSE/D) ring depth
+  static constexpr int kSmem = 2 * kKVBytes + 2 * QST * kQBytes + 4 * kPBytes + QST * 2 * 64 * 4 + 1024 + 256;
 };
 
 template <int HD>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(512, 1)
     fa_bwd_tc2_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
-                      const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_dq,
-                      const float* __restrict__ lse,
+                      const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse,
                       const float* __restrict__ Dg, float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv,
                       int s, int ht, float scale_log2, float scale) {
   using Cfg = TcBwd2Cfg<HD>;
@@ -615,24 +618,24 @@ __global__ void __launch_bounds__(320, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = smem;
   uint8_t* sV = sK + Cfg::kKVBytes;
-  uint8_t* sQ = sV + Cfg::kKVBytes;          // [2][NC][64][64]
-  uint8_t* sdO = sQ + 2 * Cfg::kQBytes;      // [2][NC][64][64]
-  uint8_t* sPT = sdO + 2 * Cfg::kQBytes;     // [2][128 kv][64 q]
+  constexpr int QST = Cfg::QST;
+  uint8_t* sQ = sV + Cfg::kKVBytes;          // [QST][NC][64][64]
+  uint8_t* sdO = sQ + QST * Cfg::kQBytes;    // [QST][NC][64][64]
+  uint8_t* sPT = sdO + QST * Cfg::kQBytes;   // [2][128 kv][64 q]
   uint8_t* sdST = sPT + 2 * Cfg::kPBytes;    // [2][128 kv][64 q]
-  float* sDQ = reinterpret_cast<float*>(sdST + 2 * Cfg::kPBytes);  // [HD/32][64][32]
-  float* sL = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(sDQ) + Cfg::kDqBytes);  // [2][64]
-  float* sD = sL + 2 * 64;                                         // [2][64]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * 64);
+  float* sL = reinterpret_cast<float*>(sdST + 2 * Cfg::kPBytes);  // [QST][64]
+  float* sD = sL + QST * 64;                                      // [QST][64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + QST * 64);
   uint64_t* kv_full = bars;
-  uint64_t* qdo_full = bars + 1;    // [2]
-  uint64_t* qdo_empty = bars + 3;   // [2]
-  uint64_t* s_full = bars + 5;      // [2]
-  uint64_t* pds_full = bars + 7;    // [2]
-  uint64_t* pds_free = bars + 9;    // [2]
-  uint64_t* dq_full = bars + 11;    // [2]
-  uint64_t* dq_free = bars + 13;    // [2]
-  uint64_t* kdv_full = bars + 15;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* qdo_full = bars + 1;            // [QST]
+  uint64_t* qdo_empty = qdo_full + QST;     // [QST]
+  uint64_t* s_full = qdo_empty + QST;       // [2]
+  uint64_t* pds_full = s_full + 2;          // [2]
+  uint64_t* pds_free = pds_full + 2;        // [2]
+  uint64_t* dq_full = pds_free + 2;         // [2]
+  uint64_t* dq_free = dq_full + 2;          // [2]
+  uint64_t* kdv_full = dq_free + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kdv_full + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int kvb = blockIdx.x;
@@ -648,14 +651,16 @@ __global__ void __launch_bounds__(320, 1)
     ptx::tma_prefetch_desc(&tm_q);
     ptx::tma_prefetch_desc(&tm_do);
     ptx::mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < QST; ++i) {
       ptx::mbar_init(&qdo_full[i], 1);
       ptx::mbar_init(&qdo_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&s_full[i], 1);
       ptx::mbar_init(&pds_full[i], 8);
       ptx::mbar_init(&pds_free[i], 1);
       ptx::mbar_init(&dq_full[i], 1);
-      ptx::mbar_init(&dq_free[i], 8);
+      ptx::mbar_init(&dq_free[i], 4);
     }
     ptx::mbar_init(kdv_full, 1);
     ptx::fence_mbar_init();
@@ -666,123 +671,126 @@ __global__ void __launch_bounds__(320, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 256 + HD;  // tS/tdP: [2][64]
+  const int wg = warp / 4;
+  if (wg == 0) ptx::setmaxnreg_dec<64>();
 
   if (warp == 0) {
     if (lane == 0) {
+      const float* gLq = lse + (static_cast<size_t>(b) * ht + h) * s;
+      const float* gDq = Dg + (static_cast<size_t>(b) * ht + h) * s;
       ptx::mbar_arrive_expect_tx(kv_full, 2 * Cfg::kKVBytes);
       for (int c = 0; c < NC; ++c) {
         ptx::tma_load_2d(sK + c * TB, &tm_kv, kv_full, dt + h * HD + 64 * c, row0 + kv0);
         ptx::tma_load_2d(sV + c * TB, &tm_kv, kv_full, 2 * dt + h * HD + 64 * c, row0 + kv0);
       }
       for (int j = 0; j < n_it; ++j) {
-        const int bb = j & 1;
+        const int sq = j % QST;
         const int q0 = (qt_first + j) * 64;
-        WAIT(&qdo_empty[bb], ((j >> 1) & 1) ^ 1, 40);
-        ptx::mbar_arrive_expect_tx(&qdo_full[bb], 2 * Cfg::kQBytes);
+        WAIT(&qdo_empty[sq], ((j / QST) & 1) ^ 1, 40);
+        ptx::mbar_arrive_expect_tx(&qdo_full[sq], 2 * Cfg::kQBytes + 2 * 64 * 4);
         for (int c = 0; c < NC; ++c) {
-          ptx::tma_load_2d(sQ + bb * Cfg::kQBytes + c * 8192, &tm_q, &qdo_full[bb], h * HD + 64 * c, row0 + q0);
-          ptx::tma_load_2d(sdO + bb * Cfg::kQBytes + c * 8192, &tm_do, &qdo_full[bb], h * HD + 64 * c, row0 + q0);
+          ptx::tma_load_2d(sQ + sq * Cfg::kQBytes + c * 8192, &tm_q, &qdo_full[sq], h * HD + 64 * c, row0 + q0);
+          ptx::tma_load_2d(sdO + sq * Cfg::kQBytes + c * 8192, &tm_do, &qdo_full[sq], h * HD + 64 * c, row0 + q0);
         }
+        // the tile's LSE and D rows ride on the same transaction
+        ptx::bulk_load(sL + sq * 64, gLq + q0, 64 * 4, &qdo_full[sq]);
+        ptx::bulk_load(sD + sq * 64, gDq + q0, 64 * 4, &qdo_full[sq]);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // all 32 lanes: uniform descriptors, one elected lane issues
       constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 64, false, false);   // S^T, dP^T
       constexpr uint32_t id_acc = ptx::idesc_bf16_f32(128, HD, false, true);  // dV, dK
       constexpr uint32_t id_dq = ptx::idesc_bf16_f32(HD, 64, true, true);     // dQ^T
       const uint32_t aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
       WAIT(kv_full, 0, 41);
       auto stage2 = [&](int i) {
-        const int bb = i & 1;
+        const int bb = i & 1, sq = i % QST;
         WAIT(&pds_full[bb], (i >> 1) & 1, 42);
         ptx::tc_fence_after();
-        const uint32_t aQ = ptx::smem_u32(sQ + bb * Cfg::kQBytes), adO = ptx::smem_u32(sdO + bb * Cfg::kQBytes);
+        const uint32_t aQ = ptx::smem_u32(sQ + sq * Cfg::kQBytes), adO = ptx::smem_u32(sdO + sq * Cfg::kQBytes);
         const uint32_t aP = ptx::smem_u32(sPT + bb * Cfg::kPBytes), adS = ptx::smem_u32(sdST + bb * Cfg::kPBytes);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {  // K = 64 query rows
           const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-          ptx::mma_bf16_ss(tdV, ptx::smem_desc_sw128(aP + kk * 32, 16, 1024),
+          ptx::mma_bf16_ss_w(tdV, ptx::smem_desc_sw128(aP + kk * 32, 16, 1024),
                            ptx::smem_desc_sw128(adO + kk * 2048, 8192, 1024), id_acc, acc);
-          ptx::mma_bf16_ss(tdK, ptx::smem_desc_sw128(adS + kk * 32, 16, 1024),
+          ptx::mma_bf16_ss_w(tdK, ptx::smem_desc_sw128(adS + kk * 32, 16, 1024),
                            ptx::smem_desc_sw128(aQ + kk * 2048, 8192, 1024), id_acc, acc);
         }
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // K = 128 kv rows
-          ptx::mma_bf16_ss(tS + bb * 64, ptx::smem_desc_sw128(aK + kk * 2048, TB, 1024),
+          ptx::mma_bf16_ss_w(tS + bb * 64, ptx::smem_desc_sw128(aK + kk * 2048, TB, 1024),
                            ptx::smem_desc_sw128(adS + kk * 2048, TB, 1024), id_dq, kk > 0 ? 1u : 0u);
-        ptx::mma_commit(&dq_full[bb]);
-        ptx::mma_commit(&qdo_empty[bb]);
-        ptx::mma_commit(&pds_free[bb]);
+        ptx::mma_commit_w(&dq_full[bb]);
+        ptx::mma_commit_w(&qdo_empty[sq]);
+        ptx::mma_commit_w(&pds_free[bb]);
       };
       for (int j = 0; j < n_it; ++j) {
-        const int bb = j & 1;
-        WAIT(&qdo_full[bb], (j >> 1) & 1, 43);
+        const int bb = j & 1, sq = j % QST;
+        WAIT(&qdo_full[sq], (j / QST) & 1, 43);
         if (j >= 2) WAIT(&dq_free[bb], ((j >> 1) - 1) & 1, 44);  // dQ^T_{j-2} read out of tS[bb]
         ptx::tc_fence_after();
-        const uint32_t aQ = ptx::smem_u32(sQ + bb * Cfg::kQBytes), adO = ptx::smem_u32(sdO + bb * Cfg::kQBytes);
+        const uint32_t aQ = ptx::smem_u32(sQ + sq * Cfg::kQBytes), adO = ptx::smem_u32(sdO + sq * Cfg::kQBytes);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t ak = (kk / 4) * TB + (kk % 4) * 32, aq = (kk / 4) * 8192 + (kk % 4) * 32;
-          ptx::mma_bf16_ss(tS + bb * 64, ptx::smem_desc_sw128(aK + ak, 16, 1024),
+          ptx::mma_bf16_ss_w(tS + bb * 64, ptx::smem_desc_sw128(aK + ak, 16, 1024),
                            ptx::smem_desc_sw128(aQ + aq, 16, 1024), id_s, kk > 0 ? 1u : 0u);
-          ptx::mma_bf16_ss(tdP + bb * 64, ptx::smem_desc_sw128(aV + ak, 16, 1024),
+          ptx::mma_bf16_ss_w(tdP + bb * 64, ptx::smem_desc_sw128(aV + ak, 16, 1024),
                            ptx::smem_desc_sw128(adO + aq, 16, 1024), id_s, kk > 0 ? 1u : 0u);
         }
-        ptx::mma_commit(&s_full[bb]);
+        ptx::mma_commit_w(&s_full[bb]);
         if (j > 0) stage2(j - 1);
       }
       stage2(n_it - 1);
-      ptx::mma_commit(kdv_full);
+      ptx::mma_commit_w(kdv_full);
     }
-  } else {
+  } else if (wg == 3) {
+    ptx::setmaxnreg_dec<64>();
+    // dQ_i flush: TMEM (lane = head dim, column = query) -> fp32 reductions into dq_acc; per
+    // query one warp instruction covers 32 consecutive head dims (one 128-byte L2 request).
     const int quarter = warp & 3;
-    const int half = (warp - 2) >> 2;   // which 32 query columns / 32-of-64 dQ columns
-    const int r = quarter * 32 + lane;  // TMEM lane: kv row (S^T, dP^T, dK, dV) or head dim (dQ^T)
     const uint32_t lb = static_cast<uint32_t>(quarter * 32) << 16;
-    const int tid = threadIdx.x - 64;
-    const float* gL = lse + (static_cast<size_t>(b) * ht + h) * s;
-    const float* gD = Dg + (static_cast<size_t>(b) * ht + h) * s;
-    // dQ_i flush: TMEM (lane = head dim, column = query) -> smem staging [hd/32][q][32] (one
-    // 128B row per warp store) -> one TMA bulk reduce-add per 32-wide head-dim box into dq_acc.
-    auto readout = [&](int i) {
+    for (int i = 0; i < n_it; ++i) {
       const int bb = i & 1;
       const int q0 = (qt_first + i) * 64;
+      float* dst = dq_acc + static_cast<size_t>(row0 + q0) * dt + h * HD + quarter * 32 + lane;
       WAIT(&dq_full[bb], (i >> 1) & 1, 45);
       ptx::tc_fence_after();
-      uint32_t v[32];
-      ptx::tmem_ld_32x32b_x32(tS + lb + bb * 64 + half * 32, v);
-      ptx::tmem_ld_wait();
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&dq_free[bb]);
-      if (tid == 0) ptx::bulk_wait_read0();  // previous flush has left the staging buffer
-      named_sync(2, 256);
-      float* box = sDQ + quarter * (64 * 32) + (half * 32) * 32 + lane;
 #pragma unroll
-      for (int e = 0; e < 32; ++e) box[e * 32] = __uint_as_float(v[e]);
-      ptx::fence_proxy_async();
-      named_sync(2, 256);
-      if (tid == 0) {
-        for (int bx = 0; bx < HD / 32; ++bx)
-          ptx::tma_reduce_add_2d(&tm_dq, sDQ + bx * (64 * 32), h * HD + bx * 32, row0 + q0);
-        ptx::bulk_commit();
+      for (int hq = 0; hq < 2; ++hq) {
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(tS + lb + bb * 64 + hq * 32, v);
+        ptx::tmem_ld_wait();
+        if (hq == 1) {
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&dq_free[bb]);
+        }
+#pragma unroll
+        for (int e = 0; e < 32; ++e) atomicAdd(dst + static_cast<size_t>(hq * 32 + e) * dt, __uint_as_float(v[e]));
       }
-    };
+    }
+  } else if (wg == 1 || wg == 2) {
+    ptx::setmaxnreg_inc<192>();
+    const int quarter = warp & 3;
+    const int half = wg - 1;            // which 32 query columns of the 64-row tile
+    const int r = quarter * 32 + lane;  // TMEM lane: kv row (S^T, dP^T, dK, dV)
+    const uint32_t lb = static_cast<uint32_t>(quarter * 32) << 16;
     for (int j = 0; j < n_it; ++j) {
-      const int bb = j & 1;
+      const int bb = j & 1, sq = j % QST;
       const int q0 = (qt_first + j) * 64;
-      if (tid < 64) sL[bb * 64 + tid] = gL[q0 + tid];
-      else if (tid < 128) sD[bb * 64 + tid - 64] = gD[q0 + tid - 64];
-      named_sync(1, 256);
       WAIT(&s_full[bb], (j >> 1) & 1, 46);
+      WAIT(&qdo_full[sq], (j / QST) & 1, 49);  // LSE / D rows of this tile (already complete)
       ptx::tc_fence_after();
       const int qc = half * 32;
       uint32_t sv[32], dv[32];
       ptx::tmem_ld_32x32b_x32(tS + lb + bb * 64 + qc, sv);
       ptx::tmem_ld_32x32b_x32(tdP + lb + bb * 64 + qc, dv);
       ptx::tmem_ld_wait();
-      const float4* L4 = reinterpret_cast<const float4*>(sL + bb * 64 + qc);
-      const float4* D4 = reinterpret_cast<const float4*>(sD + bb * 64 + qc);
+      const float4* L4 = reinterpret_cast<const float4*>(sL + sq * 64 + qc);
+      const float4* D4 = reinterpret_cast<const float4*>(sD + sq * 64 + qc);
       uint32_t pk[16], dk[16];
 #pragma unroll
       for (int e4 = 0; e4 < 8; ++e4) {
@@ -820,10 +828,7 @@ __global__ void __launch_bounds__(320, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&pds_full[bb]);
-      if (j > 0) readout(j - 1);
     }
-    readout(n_it - 1);
-    if (tid == 0) ptx::bulk_wait0();  // dQ reductions complete before the CTA retires
     // dK (scaled) and dV rows of this KV block
     WAIT(kdv_full, 0, 48);
     ptx::tc_fence_after();
@@ -872,14 +877,13 @@ int bwd_tc2(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* d
   }
   const int dt = a.heads * HD;
   const uint64_t M = static_cast<uint64_t>(a.batch) * a.seq;
-  CUtensorMap tkv, tq, tdo, tdq;
+  CUtensorMap tkv, tq, tdo;
   if (!make_tmap_bf16(&tkv, qkv, 3 * static_cast<uint64_t>(dt), M, 3 * dt, 64, 128)) return 3;
   if (!make_tmap_bf16(&tq, qkv, 3 * static_cast<uint64_t>(dt), M, 3 * dt, 64, 64)) return 3;
   if (!make_tmap_bf16(&tdo, dout, static_cast<uint64_t>(dt), M, dt, 64, 64)) return 3;
-  if (!make_tmap_f32(&tdq, dq_acc, static_cast<uint64_t>(dt), M, dt, 32, 64)) return 3;
   dim3 grid(a.seq / 128, a.batch * a.heads);
   const float scale = 1.f / sqrtf(static_cast<float>(HD));
-  fa_bwd_tc2_kernel<HD><<<grid, 320, Cfg::kSmem, st>>>(tkv, tq, tdo, tdq, lse, D, dq_acc, dqkv, a.seq, a.heads,
+  fa_bwd_tc2_kernel<HD><<<grid, 512, Cfg::kSmem, st>>>(tkv, tq, tdo, lse, D, dq_acc, dqkv, a.seq, a.heads,
                                                         scale * kLog2e, scale);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }

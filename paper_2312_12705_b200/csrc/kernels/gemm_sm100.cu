@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader CTA only)
-    if (lane == 0 && leader) {
+    if (leader) {  // all 32 lanes: uniform descriptors, one elected lane issues
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(kTileM, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
@@ -197,23 +197,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             else
               bdesc = ptx::smem_desc_sw128(sb + k * 32, 16, 1024);
             if constexpr (CG == 2)
-              ptx::mma_bf16_ss_cg2(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+              ptx::mma_bf16_ss_cg2_w(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
             else
-              ptx::mma_bf16_ss(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+              ptx::mma_bf16_ss_w(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
           }
           if constexpr (CG == 2)
-            ptx::mma_commit_cg2(&empty[stage]);
+            ptx::mma_commit_cg2_w(&empty[stage]);
           else
-            ptx::mma_commit(&empty[stage]);
+            ptx::mma_commit_w(&empty[stage]);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
         if constexpr (CG == 2)
-          ptx::mma_commit_cg2(&tfull[acc]);
+          ptx::mma_commit_cg2_w(&tfull[acc]);
         else
-          ptx::mma_commit(&tfull[acc]);
+          ptx::mma_commit_w(&tfull[acc]);
       }
     }
   } else {
