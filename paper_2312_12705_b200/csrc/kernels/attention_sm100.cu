@@ -93,7 +93,8 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* pv_done = p_full + PB;    // [PB]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + PB);
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // warp index via shfl: provably warp-uniform, so role branches are not treated as divergent
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
   const int qb = gridDim.x - 1 - blockIdx.x;  // heaviest causal blocks first
   const int b = blockIdx.y / ht, h = blockIdx.y % ht;
   const int dt = ht * HD;
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(320, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
   const uint32_t tO = tmem + 2 * kBN;
 
   if (warp == 0) {
@@ -369,7 +370,8 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* kdv_full = bars + 9;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // warp index via shfl: provably warp-uniform, so role branches are not treated as divergent
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
   const int kvb = blockIdx.x;
   const int b = blockIdx.y / ht, h = blockIdx.y % ht;
   const int dt = ht * HD;
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(320, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
   const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 256 + HD;
 
   if (warp == 0) {
@@ -637,7 +639,8 @@ __global__ void __launch_bounds__(512, 1)
   uint64_t* kdv_full = dq_free + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kdv_full + 1);
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // warp index via shfl: provably warp-uniform, so role branches are not treated as divergent
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
   const int kvb = blockIdx.x;
   const int b = blockIdx.y / ht, h = blockIdx.y % ht;
   const int dt = ht * HD;
@@ -669,7 +672,7 @@ __global__ void __launch_bounds__(512, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
   const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 256 + HD;  // tS/tdP: [2][64]
   const int wg = warp / 4;
   if (wg == 0) ptx::setmaxnreg_dec<64>();
@@ -702,14 +705,19 @@ __global__ void __launch_bounds__(512, 1)
       constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 64, false, false);   // S^T, dP^T
       constexpr uint32_t id_acc = ptx::idesc_bf16_f32(128, HD, false, true);  // dV, dK
       constexpr uint32_t id_dq = ptx::idesc_bf16_f32(HD, 64, true, true);     // dQ^T
-      const uint32_t aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
+      // Shared-window addresses from the symbol (provably warp-uniform, so descriptors stay in
+      // uniform registers): same layout as the generic pointers above.
+      const uint32_t u0 = (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + 1023u) & ~1023u;
+      const uint32_t aK = u0, aV = u0 + Cfg::kKVBytes;
+      const uint32_t aQ0 = u0 + 2 * Cfg::kKVBytes, adO0 = aQ0 + QST * Cfg::kQBytes;
+      const uint32_t aP0 = adO0 + QST * Cfg::kQBytes, adS0 = aP0 + 2 * Cfg::kPBytes;
       WAIT(kv_full, 0, 41);
       auto stage2 = [&](int i) {
         const int bb = i & 1, sq = i % QST;
         WAIT(&pds_full[bb], (i >> 1) & 1, 42);
         ptx::tc_fence_after();
-        const uint32_t aQ = ptx::smem_u32(sQ + sq * Cfg::kQBytes), adO = ptx::smem_u32(sdO + sq * Cfg::kQBytes);
-        const uint32_t aP = ptx::smem_u32(sPT + bb * Cfg::kPBytes), adS = ptx::smem_u32(sdST + bb * Cfg::kPBytes);
+        const uint32_t aQ = aQ0 + sq * Cfg::kQBytes, adO = adO0 + sq * Cfg::kQBytes;
+        const uint32_t aP = aP0 + bb * Cfg::kPBytes, adS = adS0 + bb * Cfg::kPBytes;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {  // K = 64 query rows
           const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
@@ -731,7 +739,7 @@ __global__ void __launch_bounds__(512, 1)
         WAIT(&qdo_full[sq], (j / QST) & 1, 43);
         if (j >= 2) WAIT(&dq_free[bb], ((j >> 1) - 1) & 1, 44);  // dQ^T_{j-2} read out of tS[bb]
         ptx::tc_fence_after();
-        const uint32_t aQ = ptx::smem_u32(sQ + sq * Cfg::kQBytes), adO = ptx::smem_u32(sdO + sq * Cfg::kQBytes);
+        const uint32_t aQ = aQ0 + sq * Cfg::kQBytes, adO = adO0 + sq * Cfg::kQBytes;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t ak = (kk / 4) * TB + (kk % 4) * 32, aq = (kk / 4) * 8192 + (kk % 4) * 32;

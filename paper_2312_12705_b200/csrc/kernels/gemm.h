@@ -31,6 +31,10 @@ struct GemmParams {
   const __nv_bfloat16* aux = nullptr;   // EPI_DGELU pre-activation
   int ldaux = 0;
   int accumulate = 0;
+  // K slices per output tile (EPI_F32 with accumulate only): slices are reduced into C with fp32
+  // vector atomics, which squares up the wave count of the few-tile, long-K weight-gradient GEMMs.
+  // 0 = automatic, 1 = off.
+  int split_k = 0;
 };
 
 // Requires M % 128 == 0, K % 64 == 0, N % 64 == 0, 16-byte aligned rows.

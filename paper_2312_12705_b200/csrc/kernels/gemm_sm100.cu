@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  const int warp = threadIdx.x / 32;
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0);  // provably warp-uniform
   const int lane = threadIdx.x % 32;
   const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0;
   const bool leader = rank == 0;
@@ -121,19 +121,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   else
     __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
 
   const int num_m = p.M / kTileM;
   const int num_n = p.N / BN;
   const int num_tiles = num_m * num_n;
-  const int kblocks = p.K / kBK;
+  const int S = p.split_k > 1 ? p.split_k : 1;  // K slices per tile (work unit = tile x slice)
+  const int kblocks_total = p.K / kBK;
+  const int num_units = num_tiles * S;
+  // k-block range of slice ks (slices may differ by one block)
+  auto slice_begin = [&](int ks) { return ks * kblocks_total / S; };
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+      for (int unit = cluster_id; unit < num_units; unit += num_clusters) {
+        const int tile = unit % num_tiles, kslice = unit / num_tiles;
+        const int kb0 = slice_begin(kslice), kblocks = slice_begin(kslice + 1) - kb0;
         int mb, nb;
         tile_coords(tile, num_m, num_n, mb, nb);
         const int m0 = mb * kTileM + rank * kBM, n0 = nb * BN + rank * kBN_cta;
@@ -142,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* sa = smem + stage * Cfg::kStageBytes;
           uint8_t* sb = sa + Cfg::kABytes;
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], CG * Cfg::kStageBytes);
-          const int k0 = kb * kBK;
+          const int k0 = (kb0 + kb) * kBK;
           auto load = [&](void* dst, const CUtensorMap* tm, int c0, int c1) {
             if constexpr (CG == 2)
               ptx::tma_load_2d_cg2(dst, tm, &full[stage], c0, c1);
@@ -175,7 +181,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
+      for (int unit = cluster_id; unit < num_units; unit += num_clusters, ++it) {
+        const int kslice = unit / num_tiles;
+        const int kblocks = slice_begin(kslice + 1) - slice_begin(kslice);
         const int acc = it & 1;
         ptx::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
@@ -221,7 +229,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int ehalf = (warp - 2) >> 2;  // which half of the tile's columns this warp converts
     int it = 0;
-    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
+    for (int unit = cluster_id; unit < num_units; unit += num_clusters, ++it) {
+      const int tile = unit % num_tiles;
       int mb, nb;
       tile_coords(tile, num_m, num_n, mb, nb);
       const int acc = it & 1;
@@ -241,6 +250,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (EPI == EPI_F32) {
           float* dst = reinterpret_cast<float*>(p.C) + static_cast<size_t>(row) * p.ldc + n;
           float4* d4 = reinterpret_cast<float4*>(dst);
+          if (S > 1) {  // K-sliced: the slices meet in C through fp32 reductions
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ptx::red_add_f32x4(dst + 4 * j, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          } else
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             float4 o = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
@@ -356,7 +369,7 @@ int launch(const GemmParams& p, cudaStream_t stream) {
   ok = ok && (B_MN ? make_tmap(&tb, p.B, p.N, p.K, p.ldb, 64)
                    : make_tmap(&tb, p.B, p.K, p.N, p.ldb, BN / CG));
   if (!ok) return kGemmErrTmap;
-  const int tiles = (p.M / (kBM * CG)) * (p.N / BN);
+  const int tiles = (p.M / (kBM * CG)) * (p.N / BN) * (p.split_k > 1 ? p.split_k : 1);
   const int max_clusters = num_sms() / CG;
   const int grid = CG * (tiles < max_clusters ? tiles : max_clusters);
   cudaLaunchConfig_t cfg = {};
@@ -396,6 +409,29 @@ int dispatch_epi(const GemmParams& p, cudaStream_t s) {
 
 int g_force_cg = 0;  // test hook: 1 or 2 forces the CTA-group choice (0 = automatic)
 
+// K-slice count for an accumulating fp32 GEMM: the S (slices >= 1024 deep) that best fills the
+// last wave of `slots` concurrent tiles, charging each extra slice for its fp32 reduction traffic
+// (measured: ~3% of the GEMM per extra slice at K = 16384, i.e. ~500/K).
+int choose_split(const GemmParams& p, int tiles, int slots) {
+  if (p.split_k > 0) return p.split_k;
+  if (p.epi != EPI_F32 || !p.accumulate) return 1;
+  const int kblocks = p.K / kBK;
+  int best = 1;
+  double best_score = -1.0;
+  for (int S = 1; S <= 8; ++S) {
+    if (S > 1 && kblocks / S < 16) continue;
+    const int units = tiles * S;
+    const int waves = (units + slots - 1) / slots;
+    const double score =
+        static_cast<double>(units) / (static_cast<double>(waves) * slots) - (S - 1) * 500.0 / p.K;
+    if (score > best_score + 1e-9) {
+      best_score = score;
+      best = S;
+    }
+  }
+  return best;
+}
+
 }  // namespace
 
 void gemm_force_cta_group(int cg) { g_force_cg = cg; }
@@ -405,16 +441,22 @@ int gemm_bf16(const GemmParams& p, cudaStream_t stream) {
   if (p.M % kBM != 0 || p.K % kBK != 0 || p.N % 64 != 0) return kGemmErrShape;
   if (p.epi == EPI_BIAS_GELU && p.C2 == nullptr) return kGemmErrShape;
   if (p.epi == EPI_DGELU && p.aux == nullptr) return kGemmErrShape;
+  if (p.split_k > 1 && (p.epi != EPI_F32 || !p.accumulate || p.K / kBK < p.split_k)) return kGemmErrShape;
   // CTA pairs (256 x 256 tiles) when the problem yields at least one full wave of pairs;
   // otherwise single-CTA 128 x BN tiles with the widest BN that still fills the machine.
   const bool pair_ok = p.M % 256 == 0 && p.N % 256 == 0;
   // >= ~85% of the pairs busy in a single wave beats 1.7 waves of single-CTA tiles
   const bool pair_wave = pair_ok && (p.M / 256) * (p.N / 256) * 8 >= (num_sms() / 2) * 7 - 8;
-  if (g_force_cg == 2 ? pair_ok : (g_force_cg == 0 && pair_wave)) return dispatch_epi<256, 2>(p, stream);
-  const bool n256 = (p.N % 256 == 0) && (p.M / kBM) * (p.N / 256) >= num_sms();
-  if (n256) return dispatch_epi<256, 1>(p, stream);
-  if (p.N % 128 == 0) return dispatch_epi<128, 1>(p, stream);
-  return dispatch_epi<64, 1>(p, stream);
+  GemmParams q = p;
+  if (g_force_cg == 2 ? pair_ok : (g_force_cg == 0 && pair_wave)) {
+    q.split_k = choose_split(p, (p.M / 256) * (p.N / 256), num_sms() / 2);
+    return dispatch_epi<256, 2>(q, stream);
+  }
+  const int bn = (p.N % 256 == 0) && (p.M / kBM) * (p.N / 256) >= num_sms() ? 256 : (p.N % 128 == 0 ? 128 : 64);
+  q.split_k = choose_split(p, (p.M / kBM) * (p.N / bn), num_sms());
+  if (bn == 256) return dispatch_epi<256, 1>(q, stream);
+  if (bn == 128) return dispatch_epi<128, 1>(q, stream);
+  return dispatch_epi<64, 1>(q, stream);
 }
 
 }  // namespace gptb200

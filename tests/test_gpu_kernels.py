@@ -61,6 +61,20 @@ def test_gemm_fp32_accumulate_epilogue(cg):
     assert _rel(C, C0 + A.float().t() @ B.float()) < 1e-5  # fp32 out: only summation order differs
 
 
+@pytest.mark.parametrize("M,N,K", [(2048, 2048, 16384), (6144, 2048, 16384), (512, 512, 4096)])
+def test_gemm_wgrad_split_k(M, N, K):
+    """Weight-gradient shape (few tiles, long K): the automatic K-slicing reduces the slices into
+    the fp32 accumulator with atomics; the result must equal C + A^T B up to summation order."""
+    A = torch.randn(K, M, device=DEV).bfloat16()
+    B = torch.randn(K, N, device=DEV).bfloat16()
+    C = torch.randn(M, N, device=DEV)
+    C0 = C.clone()
+    T.gemm_bf16(M, N, K, A.data_ptr(), M, 1, B.data_ptr(), N, 1, C.data_ptr(), N, epi=2, accumulate=1, stream=_stream())
+    torch.cuda.synchronize()
+    # fp32 accumulation over K terms in a different order than torch's: ~1e-7 * sqrt(K)
+    assert _rel(C, C0 + A.float().t() @ B.float()) < 5e-5
+
+
 def _attn_ref(qkv, b, s, h, hd):
     d = h * hd
     q, k, v = qkv.float().view(b, s, 3, h, hd).unbind(2)
