@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(320, 1)
   using Cfg = TcFwdCfg<HD>;
   constexpr int NC = Cfg::NC, ST = Cfg::kStages, PB = Cfg::kPBufs;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = ptx::smem_align1024(smem_raw);
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + Cfg::kQBytes;             // [ST][NC][128][64]
   uint8_t* sV = sK + ST * Cfg::kKVBytes;       // [ST][NC][128][64]
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(320, 1)
   using Cfg = TcBwdCfg<HD>;
   constexpr int NC = Cfg::NC, TB = Cfg::kTileBytes;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = ptx::smem_align1024(smem_raw);
   uint8_t* sK = smem;
   uint8_t* sV = sK + Cfg::kOpBytes;
   uint8_t* sQ = sV + Cfg::kOpBytes;
@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(512, 1)
   using Cfg = TcBwd2Cfg<HD>;
   constexpr int NC = Cfg::NC, TB = Cfg::kTileBytes;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = ptx::smem_align1024(smem_raw);
   uint8_t* sK = smem;
   uint8_t* sV = sK + Cfg::kKVBytes;
   constexpr int QST = Cfg::QST;

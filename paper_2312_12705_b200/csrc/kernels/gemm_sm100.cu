@@ -81,8 +81,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kTileM = kBM * CG;   // rows of C per tile (per CTA pair)
   constexpr int kBN_cta = BN / CG;   // rows of B staged by each CTA
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = ptx::smem_align1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;

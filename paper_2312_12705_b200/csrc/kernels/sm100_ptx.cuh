@@ -58,10 +58,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   do {
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
         "selp.b32 %0, 1, 0, P1;\n\t}"
         : "=r"(done)
-        : "r"(addr), "r"(parity)
+        : "r"(addr), "r"(parity), "r"(0x989680u)  // suspend-time hint (ns): sleep, don't spin
         : "memory");
   } while (!done);
 }
@@ -307,6 +307,13 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N, bool a_mn, b
          | ((a_mn ? 1u : 0u) << 15)     // A major
          | ((b_mn ? 1u : 0u) << 16)     // B major
          | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// 1024-byte aligned view of the dynamic smem array that keeps the shared address space (so
+// plain loads from it compile to LDS, not generic LD), offset computed from the window address.
+__device__ __forceinline__ uint8_t* smem_align1024(uint8_t* raw) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(raw));
+  return raw + (((a + 1023u) & ~1023u) - a);
 }
 
 // fp32 vector reduction into global memory (no return value).
