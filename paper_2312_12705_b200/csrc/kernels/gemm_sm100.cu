@@ -39,7 +39,8 @@ struct GemmCfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (kStageBytes <= 32768) ? 6 : 4;
   static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+  static constexpr int kStageOutBytes = 8 * 4096;  // per epilogue warp: one [32 rows][128 B] swizzled box
+  static constexpr int kSmemBytes = kStages * kStageBytes + kStageOutBytes + 1024 + 256;
 };
 
 __device__ __forceinline__ float tanh_fast(float x) {
@@ -72,17 +73,25 @@ __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int&
   nb = in_group / gsize;
 }
 
+// Output path: bf16 tiles of >= 128 columns and every fp32 tile leave through TMA (swizzled smem
+// box per epilogue warp -> full-line bulk tensor store, or bulk reduce-add for fp32 accumulation
+// and K slices); the 64-column bf16 configuration keeps direct vector stores.
+template <int BN, int EPI>
+constexpr bool kTmaOut = EPI == EPI_F32 || BN >= 128;
+
 template <int BN, int CG, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
-                      const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
+    gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
+                      const GemmParams p) {
   using Cfg = GemmCfg<BN, CG>;
   constexpr int kStages = Cfg::kStages;
   constexpr int kTileM = kBM * CG;   // rows of C per tile (per CTA pair)
   constexpr int kBN_cta = BN / CG;   // rows of B staged by each CTA
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = ptx::smem_align1024(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes);
+  uint8_t* stage_out = smem + kStages * Cfg::kStageBytes;  // 1024-aligned (stage sizes are 1 KB multiples)
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + Cfg::kStageOutBytes);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
@@ -235,8 +244,113 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int acc = it & 1;
       ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
       ptx::tc_fence_after();
-      const int row = mb * kTileM + rank * kBM + 32 * q + lane;
+      const int row_base = mb * kTileM + rank * kBM + 32 * q;
+      const int row = row_base + lane;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * BN;
+      if constexpr (kTmaOut<BN, EPI>) {
+        // this warp's [32 rows][128 B] box; 16-byte unit u of row `lane` at the 128B-swizzled slot
+        uint8_t* box = stage_out + (warp - 2) * 4096;
+        uint8_t* box_row = box + lane * 128;
+        auto put = [&](int u, uint4 val) { *reinterpret_cast<uint4*>(box_row + ((u ^ (lane & 7)) << 4)) = val; };
+        auto box_free = [&]() {  // the previous bulk op of this warp has finished reading the box
+          if (lane == 0) ptx::bulk_wait_read0();
+          __syncwarp();
+        };
+        auto flush = [&](const CUtensorMap* tm, int col, bool reduce) {
+          ptx::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            if (reduce)
+              ptx::tma_reduce_add_2d(tm, box, col, row_base);
+            else
+              ptx::tma_store_2d(tm, box, col, row_base);
+            ptx::bulk_commit();
+          }
+        };
+        if constexpr (EPI == EPI_F32) {
+          const bool reduce = p.accumulate || S > 1;
+#pragma unroll 1
+          for (int c = ehalf * (BN / 64); c < (ehalf + 1) * (BN / 64); ++c) {
+            uint32_t r[32];
+            ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
+            ptx::tmem_ld_wait();
+            box_free();
+#pragma unroll
+            for (int u = 0; u < 8; ++u) put(u, make_uint4(r[4 * u], r[4 * u + 1], r[4 * u + 2], r[4 * u + 3]));
+            flush(&tmC, nb * BN + c * 32, reduce);
+          }
+        } else {
+#pragma unroll 1
+          for (int c2 = ehalf * (BN / 128); c2 < (ehalf + 1) * (BN / 128); ++c2) {  // 64-column units
+            uint32_t g[2][16];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const int c = 2 * c2 + hh;
+              uint32_t r[32];
+              ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
+              ptx::tmem_ld_wait();
+              const int n = nb * BN + c * 32;
+              float v[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+              if constexpr (EPI == EPI_BF16 || EPI == EPI_BIAS_GELU) {
+                if (p.bias != nullptr) {
+                  const uint4* b4 = reinterpret_cast<const uint4*>(p.bias + n);
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    uint4 bb = b4[j];
+                    uint32_t w[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                      float2 f = ptx::unpack_bf16(w[e]);
+                      v[8 * j + 2 * e] += f.x;
+                      v[8 * j + 2 * e + 1] += f.y;
+                    }
+                  }
+                }
+              }
+              if constexpr (EPI == EPI_DGELU) {
+                const uint4* h4 = reinterpret_cast<const uint4*>(p.aux + static_cast<size_t>(row) * p.ldaux + n);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  uint4 hv = h4[j];
+                  uint32_t w[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    float2 f = ptx::unpack_bf16(w[e]);
+                    v[8 * j + 2 * e] *= gelu_tanh_grad(f.x);
+                    v[8 * j + 2 * e + 1] *= gelu_tanh_grad(f.y);
+                  }
+                }
+              }
+              uint32_t packed[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) packed[j] = ptx::pack_bf16(v[2 * j], v[2 * j + 1]);
+              if constexpr (EPI == EPI_BIAS_GELU) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                  float2 f = ptx::unpack_bf16(packed[j]);
+                  g[hh][j] = ptx::pack_bf16(gelu_tanh(f.x), gelu_tanh(f.y));
+                }
+              }
+              if (hh == 0) box_free();
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                put(4 * hh + j, make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]));
+            }
+            flush(&tmC, nb * BN + c2 * 64, false);
+            if constexpr (EPI == EPI_BIAS_GELU) {
+              box_free();
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  put(4 * hh + j, make_uint4(g[hh][4 * j], g[hh][4 * j + 1], g[hh][4 * j + 2], g[hh][4 * j + 3]));
+              flush(&tmC2, nb * BN + c2 * 64, false);
+            }
+          }
+        }
+      } else {
 #pragma unroll 1
       for (int c = ehalf * (BN / 64); c < (ehalf + 1) * (BN / 64); ++c) {
         uint32_t r[32];
@@ -320,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      }
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -331,6 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  if (warp >= 2 && lane == 0) ptx::bulk_wait0();  // output bulk stores / reductions complete
   if constexpr (CG == 2)
     ptx::cluster_sync();
   else
@@ -367,6 +483,14 @@ int launch(const GemmParams& p, cudaStream_t stream) {
                  : make_tmap(&ta, p.A, p.K, p.M, p.lda, kBM);
   ok = ok && (B_MN ? make_tmap(&tb, p.B, p.N, p.K, p.ldb, 64)
                    : make_tmap(&tb, p.B, p.K, p.N, p.ldb, BN / CG));
+  CUtensorMap tc, tc2;
+  if constexpr (EPI == EPI_F32) {
+    ok = ok && make_tmap_f32(&tc, p.C, p.N, p.M, p.ldc, 32, 32, true);
+    tc2 = tc;
+  } else {
+    ok = ok && make_tmap_bf16(&tc, p.C, p.N, p.M, p.ldc, 64, 32);
+    ok = ok && (EPI == EPI_BIAS_GELU ? make_tmap_bf16(&tc2, p.C2, p.N, p.M, p.ldc, 64, 32) : (tc2 = tc, true));
+  }
   if (!ok) return kGemmErrTmap;
   const int tiles = (p.M / (kBM * CG)) * (p.N / BN) * (p.split_k > 1 ? p.split_k : 1);
   const int max_clusters = num_sms() / CG;
@@ -383,7 +507,7 @@ int launch(const GemmParams& p, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, kern, ta, tb, p) != cudaSuccess) return kGemmErrCuda;
+  if (cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tc2, p) != cudaSuccess) return kGemmErrCuda;
   return cudaGetLastError() == cudaSuccess ? kGemmOk : kGemmErrCuda;
 }
 

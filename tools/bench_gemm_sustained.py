@@ -55,8 +55,13 @@ def run(name, fn, flops, secs=3.0):
 def main():
     lib = T.load()
     st = torch.cuda.current_stream().cuda_stream
-    for (M, N, K, a_mn, b_mn, epi) in [(8192, 8192, 8192, 0, 0, 0), (16384, 8192, 2048, 0, 0, 0),
-                                       (16384, 8192, 2048, 0, 0, 1), (8192, 2048, 16384, 1, 1, 2)]:
+    import os
+    shapes = [(8192, 8192, 8192, 0, 0, 0), (16384, 8192, 2048, 0, 0, 0), (16384, 8192, 2048, 0, 0, 1),
+              (8192, 2048, 16384, 1, 1, 2)]
+    if os.environ.get("SHAPES") == "square":
+        shapes = shapes[:2]
+    ldaux = int(os.environ.get("LDAUX", "0"))  # experiment hook (no effect in the product build)
+    for (M, N, K, a_mn, b_mn, epi) in shapes:
         A = torch.randn((K, M) if a_mn else (M, K), device="cuda").bfloat16()
         B = torch.randn((K, N) if b_mn else (N, K), device="cuda").bfloat16()
         C = torch.empty(M, N, device="cuda", dtype=torch.float32 if epi == 2 else torch.bfloat16)
@@ -65,7 +70,8 @@ def main():
         fl = 2.0 * M * N * K
         ours = lambda: T.gemm_bf16(M, N, K, A.data_ptr(), M if a_mn else K, a_mn, B.data_ptr(), N if b_mn else K, b_mn,
                                    C.data_ptr(), N, epi=epi, bias=bias.data_ptr() if epi == 1 else None,
-                                   C2=C2.data_ptr() if epi == 1 else None, accumulate=1 if epi == 2 else 0, stream=st)
+                                   C2=C2.data_ptr() if epi == 1 else None, ldaux=ldaux,
+                                   accumulate=1 if epi == 2 else 0, stream=st)
         At = A.t() if a_mn else A
         Bt = B if b_mn else B.t()
         out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
