@@ -172,6 +172,9 @@ int tp_session_read_flat(tp_session* s, int which, int64_t offset, int64_t n, fl
  * in its master/m/v shard at master_offset. Writes up to cap triples; *n = bucket count. */
 int tp_session_buckets(tp_session* s, int64_t* out, int cap, int* n);
 /* out = {flat_params, shard_params, device_bytes, microbatches, launches_last_step, rank, world, 0} */
+/* out = {flat params, ZeRO shard params, device bytes, microbatches, kernel launches per step,
+ * rank, world, TP mode (0 none, 1 ncclAllReduce, 2 NVLS allreduce kernel, 3 sequence parallel
+ * with the LayerNorms fused with the NVLS reduce-scatter / allgather)}. */
 int tp_session_info(tp_session* s, int64_t out[8]);
 
 /* Live timing. Kernel classes: 0 GEMM, 1 attention fwd, 2 attention bwd, 3 LayerNorm/residual,

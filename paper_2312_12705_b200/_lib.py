@@ -329,8 +329,9 @@ class Session:
     def info(self) -> dict:
         out = (_i64 * 8)()
         check(self._lib.tp_session_info(self.h, out))
-        keys = ["flat_params", "shard_params", "device_bytes", "microbatches", "launches", "rank", "world"]
-        return dict(zip(keys, list(out)[:7]))
+        keys = ["flat_params", "shard_params", "device_bytes", "microbatches", "launches", "rank", "world",
+                "tp_mode"]
+        return dict(zip(keys, list(out)))
 
 
 def global_index_map(info: dict):

@@ -68,6 +68,9 @@ struct LnBwdArgs {
 };
 size_t ln_bwd_workspace_floats(int rows, int d);
 int ln_bwd(const LnBwdArgs& a, cudaStream_t st);
+// Phase B alone: dgamma/dbeta += column sums of (dy*xhat, dy) over a.rows (when a.dy), dbias +=
+// column sums of dbias_src (when both set). Used by the sequence-parallel backward on its rows.
+int ln_bwd_cols(const LnBwdArgs& a, const bf16* dbias_src, cudaStream_t st);
 
 // out[n] += sum_rows X[rows, n] (bf16 in, fp32 accumulate). workspace >= colsum_workspace_floats.
 size_t colsum_workspace_floats(int rows, int n);

@@ -71,6 +71,13 @@ void Comms::tp_allreduce_bf16(void* buf, size_t n, cudaStream_t st, int mode) co
   nccl_check(ncclAllReduce(buf, buf, n, ncclBfloat16, ncclSum, tp_comm, st), "tp allreduce");
 }
 
+void Comms::tp_allreduce_f32_group(const std::vector<std::pair<float*, size_t>>& parts, cudaStream_t st) const {
+  if (tp == 1 || parts.empty()) return;
+  nccl_check(ncclGroupStart(), "group start");
+  for (const auto& p : parts) nccl_check(ncclAllReduce(p.first, p.first, p.second, ncclFloat, ncclSum, tp_comm, st), "tp allreduce f32");
+  nccl_check(ncclGroupEnd(), "group end");
+}
+
 void Comms::tp_allgather_f32(const float* send, float* recv, size_t n, cudaStream_t st) const {
   if (tp == 1) {
     if (send != recv) cudaMemcpyAsync(recv, send, n * sizeof(float), cudaMemcpyDeviceToDevice, st);

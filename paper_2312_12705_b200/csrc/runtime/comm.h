@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "kernels/tp_nvls.h"
@@ -52,6 +53,8 @@ class Comms {
   // Collectives on `st` (no-ops for singleton groups). Throw CommError on failure.
   // mode: 0 = automatic (NVLS kernel when buf is in the window), 1 = force ncclAllReduce.
   void tp_allreduce_bf16(void* buf, size_t n, cudaStream_t st, int mode = 0) const;
+  // Sum each (buffer, count) over TP in one ncclGroup.
+  void tp_allreduce_f32_group(const std::vector<std::pair<float*, size_t>>& parts, cudaStream_t st) const;
   void tp_allgather_f32(const float* send, float* recv, size_t n_per_rank, cudaStream_t st) const;
   void dp_reduce_scatter_f32(float* buf, size_t n_per_rank, cudaStream_t st) const;  // in place
   void dp_allgather_bf16(void* buf, size_t n_per_rank, cudaStream_t st) const;       // in place

@@ -172,7 +172,7 @@ int tp_session_info(tp_session* s, int64_t out[8]) {
     out[4] = s->stage->kernel_launches_per_step();
     out[5] = s->rank;
     out[6] = s->world;
-    out[7] = 0;
+    out[7] = s->stage->tp_mode();
   });
 }
 

@@ -211,24 +211,50 @@ void Stage::allocate() {
   adam_m_ = static_cast<float*>(alloc(shard_ * sizeof(float)));
   adam_v_ = static_cast<float*>(alloc(shard_ * sizeof(float)));
   tokens_ = static_cast<int32_t*>(alloc(static_cast<size_t>(cfg_.gbs) * (s_ + 1) * sizeof(int32_t)));
+
+  // TP > 1: full-width buffers that a collective reads or writes on every rank live in one NCCL
+  // symmetric window (NVSwitch multicast). With sequence parallelism (SP) that is the row-parallel
+  // partial sums (tmp_md_, dm_), the allgathered LayerNorm outputs (a, m2, hf_) and the allgathered
+  // input gradient dy_; the residual stream and per-row state shrink to this rank's M/tp rows.
+  const size_t Md = M * d;
+  const bool sp_wanted = cfg_.tp > 1 && M_ % cfg_.tp == 0 && !(std::getenv("GPTB200_TP_SP") &&
+                                                                  std::getenv("GPTB200_TP_SP")[0] == '0');
+  size_t sym_elems = 2 * Md;  // tmp_md_, dm_
+  if (sp_wanted) sym_elems += Md + (last_ ? Md : 0) + (ckpt_ ? 2 : 2 * static_cast<size_t>(nslots_) * Lc_) * Md;
+  char* sym = static_cast<char*>(comms_.init_tp_symmetric(sym_elems * 2));
+  sp_ = sp_wanted && sym != nullptr;
+  Ms_ = sp_ ? M_ / cfg_.tp : M_;
+  row0_ = sp_ ? comms_.me.t * Ms_ : 0;
+  size_t sym_used = 0;
+  auto full = [&](size_t elems) -> bf16* {  // [M, d]-class buffer: window when SP/NVLS, else HBM
+    if (sym) {
+      bf16* p = reinterpret_cast<bf16*>(sym + sym_used);
+      sym_used += (elems * 2 + 255) / 256 * 256;
+      return p;
+    }
+    return static_cast<bf16*>(alloc(elems * 2));
+  };
+  const size_t Ms = Ms_;
   auto layer_acts = [&](LayerActs& A) {
-    A.a = static_cast<bf16*>(alloc(M * d * 2));
+    A.a = sp_ ? full(Md) : static_cast<bf16*>(alloc(Md * 2));
     A.qkv = static_cast<bf16*>(alloc(M * 3 * dt * 2));
     A.o = static_cast<bf16*>(alloc(M * dt * 2));
-    A.hmid = static_cast<bf16*>(alloc(M * d * 2));
-    A.m2 = static_cast<bf16*>(alloc(M * d * 2));
+    A.hmid = static_cast<bf16*>(alloc(Ms * d * 2));
+    A.m2 = sp_ ? full(Md) : static_cast<bf16*>(alloc(Md * 2));
     A.u = static_cast<bf16*>(alloc(M * 4 * dt * 2));
     A.g = static_cast<bf16*>(alloc(M * 4 * dt * 2));
-    A.mu1 = static_cast<float*>(alloc(M * 4));
-    A.rs1 = static_cast<float*>(alloc(M * 4));
-    A.mu2 = static_cast<float*>(alloc(M * 4));
-    A.rs2 = static_cast<float*>(alloc(M * 4));
+    A.mu1 = static_cast<float*>(alloc(Ms * 4));
+    A.rs1 = static_cast<float*>(alloc(Ms * 4));
+    A.mu2 = static_cast<float*>(alloc(Ms * 4));
+    A.rs2 = static_cast<float*>(alloc(Ms * 4));
     A.lse = static_cast<float*>(alloc(static_cast<size_t>(mbs_) * ht_ * s_ * 4));
   };
+  tmp_md_ = full(Md);
+  dm_ = full(Md);
   slots_act_.resize(nslots_);
   for (auto& S : slots_act_) {
     S.h.resize(Lc_ + 1);
-    for (auto& h : S.h) h = static_cast<bf16*>(alloc(M * d * 2));
+    for (auto& h : S.h) h = static_cast<bf16*>(alloc(Ms * d * 2));
     if (!ckpt_) {
       S.acts.resize(Lc_);
       for (auto& A : S.acts) layer_acts(A);
@@ -237,17 +263,9 @@ void Stage::allocate() {
     S.labels = static_cast<int32_t*>(alloc(M * 4));
   }
   if (ckpt_) layer_acts(scratch_);
-  // The two TP-allreduced buffers live in the NVLS symmetric window when the TP group has one.
-  if (void* sym = comms_.init_tp_symmetric(2 * M * d * 2)) {
-    tmp_md_ = static_cast<bf16*>(sym);
-    dm_ = tmp_md_ + M * d;
-  } else {
-    tmp_md_ = static_cast<bf16*>(alloc(M * d * 2));
-    }
-  for (auto& b : dh_) b = static_cast<bf16*>(alloc(M * d * 2));
-  dy_ = static_cast<bf16*>(alloc(M * d * 2));
+  for (auto& b : dh_) b = static_cast<bf16*>(alloc(Ms * d * 2));
+  dy_ = sp_ ? full(Md) : static_cast<bf16*>(alloc(Md * 2));
   du_ = static_cast<bf16*>(alloc(M * 4 * dt * 2));
-  dm_ = static_cast<bf16*>(alloc(M * d * 2));
   do_ = static_cast<bf16*>(alloc(M * dt * 2));
   dqkv_ = static_cast<bf16*>(alloc(M * 3 * dt * 2));
   attn_D_ = static_cast<float*>(alloc(static_cast<size_t>(mbs_) * ht_ * s_ * 4));
@@ -256,9 +274,9 @@ void Stage::allocate() {
                         ln_bwd_workspace_floats(M_, d_)});
   ws_ = static_cast<float*>(alloc(ws * 4));
   if (last_) {
-    hf_ = static_cast<bf16*>(alloc(M * d * 2));
-    muf_ = static_cast<float*>(alloc(M * 4));
-    rsf_ = static_cast<float*>(alloc(M * 4));
+    hf_ = sp_ ? full(Md) : static_cast<bf16*>(alloc(Md * 2));
+    muf_ = static_cast<float*>(alloc(Ms * 4));
+    rsf_ = static_cast<float*>(alloc(Ms * 4));
     logits_ = static_cast<bf16*>(alloc(M * static_cast<size_t>(Vt_) * 2));
     xstats_ = static_cast<float*>(alloc(M * 3 * 4));
     xall_ = static_cast<float*>(alloc(M * 3 * 4 * cfg_.tp));
@@ -406,6 +424,33 @@ void Stage::layer_fwd(int l, LayerActs& A, const bf16* hin, bf16* hout, int slot
     ck(flash_attn_fwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, A.lse, st_), "flash fwd");
   }
   gemm_fwd(A.o, W.wo, nullptr, tmp_md_, M_, d_, dt_);
+  if (sp_) {
+    SpLnFwdArgs f;
+    f.nrows = Ms_, f.row0 = row0_, f.d = d_, f.seq = s_;
+    f.y_off = woff(tmp_md_), f.bias = W.bo, f.resid = hin;
+    f.drop = drop_key(opts_, step_no_, lg, 0, sample0, s_, d_);
+    f.h_out = A.hmid, f.gamma = W.ln2g, f.beta = W.ln2b, f.ln_off = woff(A.m2), f.mean = A.mu2, f.rstd = A.rs2;
+    sp_fwd(f);
+    gemm_fwd(A.m2, W.w1, W.b1, A.u, M_, 4 * dt_, d_, EPI_BIAS_GELU, A.g);
+    gemm_fwd(A.g, W.w2, nullptr, tmp_md_, M_, d_, 4 * dt_);
+    SpLnFwdArgs f2;
+    f2.nrows = Ms_, f2.row0 = row0_, f2.d = d_, f2.seq = s_;
+    f2.y_off = woff(tmp_md_), f2.bias = W.b2, f2.resid = A.hmid;
+    f2.drop = drop_key(opts_, step_no_, lg, 1, sample0, s_, d_);
+    f2.h_out = hout;
+    const bool next_in_chunk_sp = (l + 1) % Lc_ != 0;
+    if (next_in_chunk_sp) {
+      LayerActs& N = acts_for(slot, l + 1);
+      const LayerW Wn = w(l + 1);
+      f2.gamma = Wn.ln1g, f2.beta = Wn.ln1b, f2.ln_off = woff(N.a), f2.mean = N.mu1, f2.rstd = N.rs1;
+    } else if (last_vs(l / Lc_)) {
+      f2.gamma = params_ + slot_offset(2 + kPerLayer * L_);
+      f2.beta = params_ + slot_offset(2 + kPerLayer * L_ + 1);
+      f2.ln_off = woff(hf_), f2.mean = muf_, f2.rstd = rsf_;
+    }
+    sp_fwd(f2);
+    return;
+  }
   tp_allreduce(tmp_md_);
   ResidLnArgs r;
   r.rows = M_, r.d = d_, r.seq = s_;
@@ -446,6 +491,26 @@ void Stage::layer_recompute(int l, LayerActs& A, const bf16* hin) {
   const LayerW W = w(l);
   const int64_t sample0 = static_cast<int64_t>(comms_.me.d) * (cfg_.gbs / cfg_.dp) +
                           static_cast<int64_t>(cur_mb_) * mbs_;
+  if (sp_) {
+    SpLnFwdArgs f;
+    f.nrows = Ms_, f.row0 = row0_, f.d = d_, f.seq = s_;
+    f.resid = hin, f.gamma = W.ln1g, f.beta = W.ln1b, f.ln_off = woff(A.a), f.mean = A.mu1, f.rstd = A.rs1;
+    sp_fwd(f);
+    gemm_fwd(A.a, W.wqkv, W.bqkv, A.qkv, M_, 3 * dt_, d_);
+    {
+      KScope prof(this, K_ATTN_FWD, 2.0 * mbs_ * ht_ * static_cast<double>(s_) * s_ * hd_);
+      ck(flash_attn_fwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, A.lse, st_), "flash fwd");
+    }
+    gemm_fwd(A.o, W.wo, nullptr, tmp_md_, M_, d_, dt_);
+    SpLnFwdArgs f2;
+    f2.nrows = Ms_, f2.row0 = row0_, f2.d = d_, f2.seq = s_;
+    f2.y_off = woff(tmp_md_), f2.bias = W.bo, f2.resid = hin;
+    f2.drop = drop_key(opts_, step_no_, lg, 0, sample0, s_, d_);
+    f2.h_out = A.hmid, f2.gamma = W.ln2g, f2.beta = W.ln2b, f2.ln_off = woff(A.m2), f2.mean = A.mu2, f2.rstd = A.rs2;
+    sp_fwd(f2);
+    gemm_fwd(A.m2, W.w1, W.b1, A.u, M_, 4 * dt_, d_, EPI_BIAS_GELU, A.g);
+    return;
+  }
   ResidLnArgs r0;
   r0.rows = M_, r0.d = d_, r0.seq = s_;
   r0.resid = hin, r0.gamma = W.ln1g, r0.beta = W.ln1b, r0.ln_out = A.a, r0.mean = A.mu1, r0.rstd = A.rs1;
@@ -493,6 +558,24 @@ void Stage::forward_op(int mb, int c, int slot, bool head_now) {
   ResidLnArgs r;
   r.rows = M_, r.d = d_, r.seq = s_;
   r.gamma = W0.ln1g, r.beta = W0.ln1b, r.ln_out = A0.a, r.mean = A0.mu1, r.rstd = A0.rs1;
+  if (sp_) {  // embedding partials reduce-scattered / LN1 allgathered in one NVLS kernel
+    SpLnFwdArgs f;
+    f.nrows = Ms_, f.row0 = row0_, f.d = d_, f.seq = s_;
+    if (first_vs(c)) {
+      ck(embed_lookup(S.inputs, M_, params_ + slot_offset(0), comms_.me.t * Vt_, Vt_, d_, tmp_md_, st_), "embed");
+      const int64_t sample0 = static_cast<int64_t>(comms_.me.d) * (cfg_.gbs / cfg_.dp) + static_cast<int64_t>(mb) * mbs_;
+      f.y_off = woff(tmp_md_), f.resid = params_ + slot_offset(1), f.resid_pos_table = true;
+      f.drop = drop_key(opts_, step_no_, kEmbedLayer, 2, sample0, s_, d_);
+      f.h_out = S.h[0];
+    } else {
+      f.resid = S.h[0];
+    }
+    f.gamma = W0.ln1g, f.beta = W0.ln1b, f.ln_off = woff(A0.a), f.mean = A0.mu1, f.rstd = A0.rs1;
+    sp_fwd(f);
+    for (int l = 0; l < Lc_; ++l) layer_fwd(l0 + l, acts_for(slot, l0 + l), S.h[l], S.h[l + 1], slot);
+    if (last_vs(c) && head_now) head_and_loss(slot);
+    return;
+  }
   if (first_vs(c)) {
     ck(embed_lookup(S.inputs, M_, params_ + slot_offset(0), comms_.me.t * Vt_, Vt_, d_, tmp_md_, st_), "embed");
     tp_allreduce(tmp_md_);
@@ -512,6 +595,16 @@ void Stage::forward_op(int mb, int c, int slot, bool head_now) {
 }
 
 void Stage::final_ln(const bf16* h) {
+  if (sp_) {
+    SpLnFwdArgs f;
+    f.nrows = Ms_, f.row0 = row0_, f.d = d_, f.seq = s_;
+    f.resid = h;
+    f.gamma = params_ + slot_offset(2 + kPerLayer * L_);
+    f.beta = params_ + slot_offset(2 + kPerLayer * L_ + 1);
+    f.ln_off = woff(hf_), f.mean = muf_, f.rstd = rsf_;
+    sp_fwd(f);
+    return;
+  }
   ResidLnArgs r;
   r.rows = M_, r.d = d_, r.seq = s_;
   r.resid = h;
@@ -542,7 +635,7 @@ void Stage::head_and_loss(int slot) {
 void Stage::head_bwd(bf16* dh) {
   // logits_ holds scale*(softmax - onehot). Vocab-parallel: partial dX summed over TP.
   gemm_dgrad(logits_, params_ + slot_offset(0), tmp_md_, M_, Vt_, d_);
-  tp_allreduce(tmp_md_);
+  if (!sp_) tp_allreduce(tmp_md_);  // SP: reduced in the final-LN backward kernel
   gemm_wgrad(logits_, hf_, grads_ + slot_offset(0), M_, Vt_, d_);
 }
 
@@ -561,6 +654,41 @@ void Stage::layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2)
     ck(colsum_bf16(du_, M_, 4 * dt_, G.b1, ws_, st_), "db1");
   }
   gemm_dgrad(du_, W.w1, dm_, M_, 4 * dt_, d_);
+  if (sp_) {
+    gemm_wgrad(du_, A.m2, G.w1, M_, 4 * dt_, d_);
+    SpLnBwdArgs g;
+    g.nrows = Ms_, g.row0 = row0_, g.d = d_, g.workspace = ws_;
+    g.dy_off = woff(dm_), g.x = A.hmid, g.gamma = W.ln2g, g.mean = A.mu2, g.rstd = A.rs2;
+    g.resid_grad = dh, g.dx = dh;
+    g.drop = drop_key(opts_, step_no_, lg, 0, sample0, s_, d_);
+    g.dxd_off = woff(dy_), g.dgamma = G.ln2g, g.dbeta = G.ln2b, g.dbias = G.bo;
+    sp_bwd(g);
+    gemm_dgrad(dy_, W.wo, do_, M_, d_, dt_);
+    gemm_wgrad(dy_, A.o, G.wo, M_, d_, dt_);
+    {
+      KScope prof(this, K_ATTN_BWD, 5.0 * mbs_ * ht_ * static_cast<double>(s_) * s_ * hd_);
+      ck(flash_attn_bwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, do_, A.lse, attn_D_, dq_acc_, dqkv_, st_), "flash bwd");
+    }
+    {
+      KScope prof(this, K_ELEM);
+      ck(colsum_bf16(dqkv_, M_, 3 * dt_, G.bqkv, ws_, st_), "dbqkv");
+    }
+    gemm_dgrad(dqkv_, W.wqkv, dm_, M_, 3 * dt_, d_);
+    gemm_wgrad(dqkv_, A.a, G.wqkv, M_, 3 * dt_, d_);
+    SpLnBwdArgs g1;
+    g1.nrows = Ms_, g1.row0 = row0_, g1.d = d_, g1.workspace = ws_;
+    g1.dy_off = woff(dm_), g1.x = hin, g1.gamma = W.ln1g, g1.mean = A.mu1, g1.rstd = A.rs1;
+    g1.resid_grad = dh, g1.dx = dh, g1.dgamma = G.ln1g, g1.dbeta = G.ln1b;
+    if (l % Lc_ > 0) {  // preceding branch: MLP of layer l-1 in this chunk
+      g1.drop = drop_key(opts_, step_no_, lg - 1, 1, sample0, s_, d_);
+      g1.dxd_off = woff(dy_), g1.dbias = gr(l - 1).b2;
+    } else if (first_vs(l / Lc_)) {  // embedding dropout; dy_ feeds the embedding backward
+      g1.drop = drop_key(opts_, step_no_, kEmbedLayer, 2, sample0, s_, d_);
+      g1.dxd_off = woff(dy_);
+    }
+    sp_bwd(g1);
+    return;
+  }
   tp_allreduce(dm_);
   gemm_wgrad(du_, A.m2, G.w1, M_, 4 * dt_, d_);
   LnBwdArgs b;
@@ -614,6 +742,38 @@ void Stage::backward_op(int mb, int c, int slot, bf16* dh, bool head_late) {
   const bool drop_on = opts_.dropout > 0.f;
   const int l_last = (c + 1) * Lc_ - 1;
   const int64_t sample0 = static_cast<int64_t>(comms_.me.d) * (cfg_.gbs / cfg_.dp) + static_cast<int64_t>(mb) * mbs_;
+  if (sp_) {
+    // chunk output: final LN backward (last virtual stage) or the received gradient; either way
+    // the dropout' of the last layer's MLP branch is allgathered into dy_ for that MLP backward
+    SpLnBwdArgs g;
+    g.nrows = Ms_, g.row0 = row0_, g.d = d_, g.workspace = ws_;
+    g.drop = drop_key(opts_, step_no_, glayer(l_last), 1, sample0, s_, d_);
+    g.dxd_off = woff(dy_), g.dbias = gr(l_last).b2;
+    if (last_vs(c)) {
+      if (head_late) {
+        final_ln(S.h[Lc_]);
+        head_and_loss(slot);
+      }
+      head_bwd(dh);
+      const int f = 2 + kPerLayer * L_;
+      g.dy_off = woff(tmp_md_), g.x = S.h[Lc_], g.gamma = params_ + slot_offset(f), g.mean = muf_, g.rstd = rsf_;
+      g.dx = dh, g.dgamma = grads_ + slot_offset(f), g.dbeta = grads_ + slot_offset(f + 1);
+    } else {
+      g.resid_grad = dh;  // received gradient of the chunk output (shard); dh itself is unchanged
+    }
+    sp_bwd(g);
+    for (int l = Lc_ - 1; l >= 0; --l) {
+      const int li = c * Lc_ + l;
+      LayerActs& A = acts_for(slot, li);
+      if (ckpt_) layer_recompute(li, A, S.h[l]);
+      layer_bwd(li, A, S.h[l], dh, dy_);
+      if (in_last_bwd_) grads_ready(layer_bucket_[li]);
+    }
+    if (first_vs(c))
+      ck(embed_bwd(S.inputs, M_, dy_, comms_.me.t * Vt_, Vt_, d_, s_, grads_ + slot_offset(0), grads_ + slot_offset(1), st_),
+         "embed bwd");
+    return;
+  }
   LnBwdArgs b;
   b.rows = M_, b.d = d_, b.workspace = ws_;
   b.drop = drop_key(opts_, step_no_, glayer(l_last), 1, sample0, s_, d_);
@@ -651,6 +811,27 @@ void Stage::backward_op(int mb, int c, int slot, bf16* dh, bool head_late) {
   }
 }
 
+// ------------------------------------------------------------------------------ SP helpers
+int64_t Stage::woff(const void* p) const {
+  const int64_t o = nvls_offset(comms_.tp_nvls, p);
+  if (o < 0) throw StepError{TP_ERR_INVALID, "sequence-parallel buffer outside the symmetric window"};
+  return o;
+}
+
+void Stage::sp_fwd(const SpLnFwdArgs& a) {
+  ++launches_;
+  KScope prof(this, K_COMM_TP, 0, (a.y_off >= 0 ? 2.0 : 0.0) * M_ * d_ + 6.0 * Ms_ * d_);
+  const int r = sp_ln_fwd(comms_.tp_nvls, a, st_);
+  if (r != 0) throw StepError{r == 1 ? TP_ERR_INVALID : TP_ERR_CUDA, "sequence-parallel LN forward failed"};
+}
+
+void Stage::sp_bwd(const SpLnBwdArgs& a) {
+  launches_ += 3;
+  KScope prof(this, K_COMM_TP, 0, (a.dy_off >= 0 ? 2.0 : 0.0) * M_ * d_ + 10.0 * Ms_ * d_);
+  const int r = sp_ln_bwd(comms_.tp_nvls, a, st_);
+  if (r != 0) throw StepError{r == 1 ? TP_ERR_INVALID : TP_ERR_CUDA, "sequence-parallel LN backward failed"};
+}
+
 // ------------------------------------------------------------------------------ step
 // Adam on this rank's slice of one bucket, on `st` (fp32 master/m/v, writes the bf16 copy).
 void Stage::adam_bucket(int bucket, cudaStream_t st) {
@@ -677,6 +858,19 @@ void Stage::grads_ready(int bucket) {
   cudaEventRecord(bucket_ev_[bucket], st_);
   cudaStreamWaitEvent(comm_st_, bucket_ev_[bucket], 0);
   try {
+    if (sp_) {  // LayerNorm / row-parallel bias grads were summed over this rank's rows only
+      std::vector<std::pair<float*, size_t>> parts;
+      for (int li = 0; li < Ll_; ++li) {
+        if (layer_bucket_[li] != bucket) continue;
+        const LayerG G = gr(li);
+        for (float* g : {G.ln1g, G.ln1b, G.bo, G.ln2g, G.ln2b, G.b2}) parts.push_back({g, static_cast<size_t>(d_)});
+        if (li == Ll_ - 1 && last_) {
+          parts.push_back({grads_ + slot_offset(2 + kPerLayer * L_), static_cast<size_t>(d_)});
+          parts.push_back({grads_ + slot_offset(2 + kPerLayer * L_ + 1), static_cast<size_t>(d_)});
+        }
+      }
+      comms_.tp_allreduce_f32_group(parts, comm_st_);
+    }
     if (bucket == 0 && cfg_.pp > 1 && (first_ || last_))
       comms_.emb_allreduce_f32(grads_ + slot_offset(0), static_cast<size_t>(Vt_) * d_, comm_st_);
     if (cfg_.dp > 1) comms_.dp_reduce_scatter_f32(grads_ + b.off, b.len / cfg_.dp, comm_st_);
@@ -692,14 +886,14 @@ void Stage::grads_ready(int bucket) {
 void Stage::pp_recv(void* buf, int dir) {
   ++launches_;
   KScope prof(this, K_COMM_PP);
-  comms_.pp_recv(buf, static_cast<size_t>(M_) * d_, dir, st_);
+  comms_.pp_recv(buf, static_cast<size_t>(Ms_) * d_, dir, st_);  // SP: this rank's rows only
 }
 
 void Stage::pp_send(const void* buf, int dir, cudaEvent_t done) {
   ++launches_;
   cudaEventRecord(op_ev_, st_);
   cudaStreamWaitEvent(send_st_[dir], op_ev_, 0);
-  comms_.pp_send(buf, static_cast<size_t>(M_) * d_, dir, send_st_[dir]);
+  comms_.pp_send(buf, static_cast<size_t>(Ms_) * d_, dir, send_st_[dir]);
   cudaEventRecord(done, send_st_[dir]);
 }
 

@@ -106,6 +106,8 @@ class Stage {
   void debug_tp_allreduce(const uint16_t* in, uint16_t* out, int mode);
   float bench_tp_allreduce(int iters, int mode, int ctas);
   bool tp_uses_nvls() const { return comms_.tp_nvls != nullptr; }
+  // 0: no TP; 1: ncclAllReduce; 2: NVLS allreduce kernel; 3: sequence parallel (fused NVLS norms)
+  int tp_mode() const { return cfg_.tp == 1 ? 0 : (sp_ ? 3 : (comms_.tp_nvls ? 2 : 1)); }
 
  private:
   struct LayerW {
@@ -165,6 +167,9 @@ class Stage {
   bool profile_ = false;
   KernelTimes prof_acc_;
   void tp_allreduce(bf16* buf);
+  int64_t woff(const void* p) const;  // window offset of an SP buffer (throws when outside)
+  void sp_fwd(const SpLnFwdArgs& a);
+  void sp_bwd(const SpLnBwdArgs& a);
   int64_t slot_offset(int tid) const { return slot(tid)->offset; }
 
   trainplan::ModelSpec model_;
@@ -183,6 +188,11 @@ class Stage {
   bool last_vs(int c) const { return last_ && c == v_ - 1; }
   int L_ = 0, Ll_ = 0, Lc_ = 0, v_ = 1, d_ = 0, dt_ = 0, ht_ = 0, hd_ = 0, V_ = 0, Vt_ = 0, s_ = 0;
   int mbs_ = 1, M_ = 0, m_ = 1, nslots_ = 1;
+  // Sequence parallelism (tp > 1 with an NVLS window): this rank owns rows [row0_, row0_ + Ms_)
+  // of every [M, d] residual-stream tensor; LayerNorms run on those rows fused with the TP
+  // reduce-scatter / allgather (kernels/tp_nvls.h). Without SP, Ms_ == M_ and row0_ == 0.
+  bool sp_ = false;
+  int Ms_ = 0, row0_ = 0;
   bool first_ = true, last_ = true, ckpt_ = false;
   int step_no_ = 0;
   int cur_mb_ = 0;

@@ -46,6 +46,8 @@ def main():
     cfg = T.ParallelConfig(tp=c["tp"], pp=c["pp"], dp=c["dp"], mbs=c["mbs"], gbs=c["gbs"], zero_stage=1,
                            checkpoint_activations=c.get("ckpt", 0), interleave_v=c.get("v", 1))
     opts = T.TrainOptions(seed=1234, dropout=c.get("dropout", 0.0), lr=1e-3, weight_decay=0.01)
+    if c.get("tp_env"):
+        os.environ.update(c["tp_env"])
     sess = T.Session(spec, cfg, opts, rank=a.rank, world=a.world, device=a.rank, nccl_id=nid)
     sess.init_params()
     info = sess.info()
@@ -62,7 +64,7 @@ def main():
         if ti is not None:
             layout[tid] = ti
     coords = T.rank_coords(a.rank, c["tp"], c["pp"], c["dp"])
-    np.savez(out / f"rank{a.rank}.npz", grads=grads, master0=master0, master1=master1, loss=np.array(loss),
+    np.savez(out / f"rank{a.rank}.npz", tp_mode=np.array(info["tp_mode"]), grads=grads, master0=master0, master1=master1, loss=np.array(loss),
              coords=np.array(coords), P=np.array(P), shard=np.array(shard), layout=json.dumps(layout),
              buckets=np.array(sess.buckets(), dtype=np.int64).reshape(-1, 3))
     sess.barrier()

@@ -44,12 +44,14 @@ def _slice(full, info):
     return full[np.ix_(grow, gcol)] if info["cols"] > 1 else full[grow]
 
 
-def run_layout(tp, pp, dp, L=2, d=256, a=4, V=1024, s=128, mbs=1, gbs=None, ckpt=0, dropout=0.0, v=1):
+def run_layout(tp, pp, dp, L=2, d=256, a=4, V=1024, s=128, mbs=1, gbs=None, ckpt=0, dropout=0.0, v=1, tp_env=None,
+               want_tp_mode=None):
     world = tp * pp * dp
     if _ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
     gbs = gbs or mbs * dp * 2
-    c = dict(L=L, d=d, a=a, V=V, s=s, tp=tp, pp=pp, dp=dp, mbs=mbs, gbs=gbs, ckpt=ckpt, dropout=dropout, v=v)
+    c = dict(L=L, d=d, a=a, V=V, s=s, tp=tp, pp=pp, dp=dp, mbs=mbs, gbs=gbs, ckpt=ckpt, dropout=dropout, v=v,
+             tp_env=tp_env or {})
     with tempfile.TemporaryDirectory() as td:
         procs = [subprocess.Popen([sys.executable, str(ROOT / "tests" / "mp_worker.py"), "--cfg", json.dumps(c),
                                    "--rank", str(r), "--world", str(world), "--out", td],
@@ -78,6 +80,8 @@ def run_layout(tp, pp, dp, L=2, d=256, a=4, V=1024, s=128, mbs=1, gbs=None, ckpt
                          loss_scale=1.0 / (gbs * s), grads=grads)
         oloss += l
     oloss /= gbs * s
+    if want_tp_mode is not None:
+        assert {int(r["tp_mode"]) for r in ranks} == {want_tp_mode}, [int(r["tp_mode"]) for r in ranks]
     losses = [float(r["loss"]) for r in ranks]
     assert max(losses) - min(losses) < 1e-6, losses
     assert abs(losses[0] - oloss) <= 1e-2 * max(1.0, oloss), (losses[0], oloss)
@@ -119,7 +123,16 @@ def run_layout(tp, pp, dp, L=2, d=256, a=4, V=1024, s=128, mbs=1, gbs=None, ckpt
 
 
 def test_tp2():
-    run_layout(tp=2, pp=1, dp=1)
+    # NVSwitch boxes run sequence parallelism (LayerNorms fused with the NVLS reduce-scatter/allgather)
+    run_layout(tp=2, pp=1, dp=1, dropout=0.1, want_tp_mode=3)
+
+
+def test_tp2_nvls_allreduce_without_sp():
+    run_layout(tp=2, pp=1, dp=1, dropout=0.1, tp_env={"GPTB200_TP_SP": "0"}, want_tp_mode=2)
+
+
+def test_tp2_nccl_allreduce():
+    run_layout(tp=2, pp=1, dp=1, tp_env={"GPTB200_TP_SP": "0", "GPTB200_TP_NVLS": "0"}, want_tp_mode=1)
 
 
 def test_pp2_1f1b_four_microbatches():
