@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "ops.h"
 #include "rowops.cuh"
@@ -326,6 +327,106 @@ __global__ void ln_bwd_rows_kernel(LnBwdArgs a, DropDev dr) {
   }
 }
 
+// Single-HBM-pass LayerNorm backward: a CTA owns kLnFuseRows rows. Pass 1 (warp per row): the
+// two row reductions. Pass 2 (thread per 8 columns, rows walked in order): dx, dropout'(dx) and
+// the dgamma/dbeta/dbias column partials in registers; x and dy come back from L2 (the CTA's
+// 32-row slab was just read). HBM: 10 B/element instead of 16 for the two-kernel form.
+constexpr int kLnFuseRows = 32;
+
+__global__ void __launch_bounds__(256) ln_bwd_fused_kernel(LnBwdArgs a, DropDev dr, float* __restrict__ ws) {
+  __shared__ float sm1[kLnFuseRows], sm2[kLnFuseRows], smu[kLnFuseRows], srs[kLnFuseRows];
+  const int d = a.d;
+  const int r0 = blockIdx.x * kLnFuseRows;
+  const int nr = min(kLnFuseRows, a.rows - r0);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (a.dy) {
+    for (int rr = warp; rr < nr; rr += 8) {
+      const int row = r0 + rr;
+      const size_t roff = static_cast<size_t>(row) * d;
+      const float mu = a.mean[row], rs = a.rstd[row];
+      float s1 = 0.f, s2 = 0.f;
+      for (int c0 = lane * 8; c0 < d; c0 += 256) {
+        float x[8], dy[8], g[8];
+        unpack8(*reinterpret_cast<const uint4*>(a.x + roff + c0), x);
+        unpack8(*reinterpret_cast<const uint4*>(a.dy + roff + c0), dy);
+        unpack8(*reinterpret_cast<const uint4*>(a.gamma + c0), g);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float gy = dy[i] * g[i];
+          s1 += gy;
+          s2 += gy * (x[i] - mu) * rs;
+        }
+      }
+      for (int off = 16; off; off >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffff, s1, off);
+        s2 += __shfl_xor_sync(0xffffffff, s2, off);
+      }
+      if (lane == 0) {
+        sm1[rr] = s1 / d;
+        sm2[rr] = s2 / d;
+        smu[rr] = mu;
+        srs[rr] = rs;
+      }
+    }
+  }
+  __syncthreads();
+  for (int c0 = threadIdx.x * 8; c0 < d; c0 += 256 * 8) {
+    float g[8], ag[8], ab[8], as[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ag[i] = ab[i] = as[i] = 0.f;
+    if (a.dy) unpack8(*reinterpret_cast<const uint4*>(a.gamma + c0), g);
+#pragma unroll 2
+    for (int rr = 0; rr < nr; ++rr) {
+      const size_t o = static_cast<size_t>(r0 + rr) * d + c0;
+      float dx[8];
+      if (a.dy) {
+        const float mu = smu[rr], rs = srs[rr], m1 = sm1[rr], m2 = sm2[rr];
+        float x[8], dy[8];
+        unpack8(*reinterpret_cast<const uint4*>(a.x + o), x);
+        unpack8(*reinterpret_cast<const uint4*>(a.dy + o), dy);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float xh = (x[i] - mu) * rs;
+          dx[i] = rs * (dy[i] * g[i] - m1 - xh * m2);
+          ag[i] += dy[i] * xh;
+          ab[i] += dy[i];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dx[i] = 0.f;
+      }
+      if (a.resid_grad) {
+        float r[8];
+        unpack8(*reinterpret_cast<const uint4*>(a.resid_grad + o), r);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dx[i] += r[i];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dx[i] = round_bf16(dx[i]);
+      if (a.dx) *reinterpret_cast<uint4*>(a.dx + o) = pack8(dx);
+      float od[8];
+      const uint32_t kb = dr.on ? keep8(dr, static_cast<int64_t>(o)) : 0xFFu;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) od[i] = dr.on ? ((kb >> i) & 1u ? dx[i] * dr.scale : 0.f) : dx[i];
+      if (a.dxd && (dr.on || a.dxd != a.dx)) *reinterpret_cast<uint4*>(a.dxd + o) = pack8(od);
+      if (a.dbias) {
+        const uint4 q = pack8(od);  // bias grad sums the bf16 values that were stored
+        float qv[8];
+        unpack8(q, qv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) as[i] += qv[i];
+      }
+    }
+    float* w = ws + static_cast<size_t>(blockIdx.x) * 3 * d;
+    *reinterpret_cast<float4*>(w + c0) = make_float4(ag[0], ag[1], ag[2], ag[3]);
+    *reinterpret_cast<float4*>(w + c0 + 4) = make_float4(ag[4], ag[5], ag[6], ag[7]);
+    *reinterpret_cast<float4*>(w + d + c0) = make_float4(ab[0], ab[1], ab[2], ab[3]);
+    *reinterpret_cast<float4*>(w + d + c0 + 4) = make_float4(ab[4], ab[5], ab[6], ab[7]);
+    *reinterpret_cast<float4*>(w + 2 * d + c0) = make_float4(as[0], as[1], as[2], as[3]);
+    *reinterpret_cast<float4*>(w + 2 * d + c0 + 4) = make_float4(as[4], as[5], as[6], as[7]);
+  }
+}
+
 constexpr int kLnColRows = 64;
 
 // Phase B: column sums over 64-row chunks of (dy*xhat, dy, dxd); one thread = 8 columns,
@@ -619,6 +720,16 @@ __global__ void accumulate_sum_kernel(const float* __restrict__ x, int n, float*
   if (threadIdx.x == 0) *acc += v[0];
 }
 
+int device_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
 int grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   if (g > 148 * 16) g = 148 * 16;
@@ -656,7 +767,7 @@ int resid_ln_fwd(const ResidLnArgs& a, cudaStream_t st) {
 }
 
 size_t ln_bwd_workspace_floats(int rows, int d) {
-  return static_cast<size_t>((rows + kLnColRows - 1) / kLnColRows) * 3 * d;
+  return static_cast<size_t>((rows + kLnFuseRows - 1) / kLnFuseRows) * 3 * d;
 }
 
 int ln_bwd(const LnBwdArgs& a, cudaStream_t st) {
@@ -666,6 +777,18 @@ int ln_bwd(const LnBwdArgs& a, cudaStream_t st) {
   if (a.drop.p > 0.f && a.drop.elem_base % 8 != 0) return 1;
   if (a.dy && (!a.gamma || !a.mean || !a.rstd || !a.x)) return 1;
   const DropDev dr = make_drop(a.drop);
+  // fused single HBM pass when the row count alone fills the GPU (>= 2 waves of 32-row slabs);
+  // wide-row / few-row shapes keep the row-parallel two-pass form
+  const int blocks = (a.rows + kLnFuseRows - 1) / kLnFuseRows;
+  if (blocks >= 2 * device_sms() && std::getenv("GPTB200_LN_BWD_TWO_PASS") == nullptr) {
+    ln_bwd_fused_kernel<<<blocks, 256, 0, st>>>(a, dr, a.workspace);
+    const bool any = (a.dy && (a.dgamma || a.dbeta)) || a.dbias;
+    if (any)
+      reduce_partials_kernel<<<(a.d + 31) / 32, 256, 0, st>>>(a.workspace, blocks, 3 * a.d, a.d,
+                                                                a.dy ? a.dgamma : nullptr, a.dy ? a.dbeta : nullptr,
+                                                                a.dbias);
+    return status();
+  }
   // phase A: dx (+ dropout'(dx)) per row
   if (a.dx || a.dxd) {
     if (a.d % 256 == 0 && a.d <= 4096) {
