@@ -288,6 +288,8 @@ def main():
         line["roofline"] = {"kernel": "tcgen05 GEMM (all GEMM launches of the step)", "bound": "tensor",
                             "achieved": gemm_tf, "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
                             "frac": gemm_tf / peaks["bf16_tflops_sustained"], "traffic": gemm_traffic(),
+                            "traffic_algorithmic": gemm_traffic("algorithmic_bytes"),
+                            "traffic_kernel": gemm_traffic("kernel"),
                             "peak_source": peak_src + ", sustained bf16 (kernel timed inside a long step)",
                             "gemm_share_of_step": g["ms"] / ms_prof if ms_prof else None,
                             "algorithmic_flops_per_launch": g["flops"] / max(g["launches"], 1)}
@@ -308,12 +310,13 @@ def main():
     return 0
 
 
-def gemm_traffic():
-    """Per-launch DRAM bytes of the GEMM from the committed ncu capture (profiles/), else None."""
+def gemm_traffic(key="bytes_per_launch"):
+    """Per-launch DRAM bytes (or the algorithmic bytes, key="algorithmic_bytes") of the representative
+    GEMM launch in the committed ncu capture (profiles/gemm_traffic.json), else None."""
     p = ROOT / "profiles" / "gemm_traffic.json"
     if p.exists():
         try:
-            return json.loads(p.read_text()).get("bytes_per_launch")
+            return json.loads(p.read_text()).get(key)
         except (ValueError, KeyError):
             return None
     return None
