@@ -440,7 +440,7 @@ int fwd_impl(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, f
 template <int HD>
 int bwd_impl(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* out,
              const __nv_bfloat16* dout, const float* lse, float* D, float* dq_acc,
-             __nv_bfloat16* dqkv, cudaStream_t st) {
+             __nv_bfloat16* dqkv, cudaStream_t st, bool d_ready) {
   using Cfg = BwdCfg<HD>;
   static bool init = false;
   if (!init) {
@@ -449,7 +449,10 @@ int bwd_impl(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* 
   }
   const int M = a.batch * a.seq;
   const int warps = M * a.heads;
-  flash_bwd_pre_kernel<HD><<<(warps + 7) / 8, 256, 0, st>>>(out, dout, D, dq_acc, a.seq, a.heads, M);
+  if (d_ready)
+    cudaMemsetAsync(dq_acc, 0, static_cast<size_t>(M) * a.heads * HD * sizeof(float), st);
+  else
+    flash_bwd_pre_kernel<HD><<<(warps + 7) / 8, 256, 0, st>>>(out, dout, D, dq_acc, a.seq, a.heads, M);
   const float scale = 1.f / sqrtf(static_cast<float>(HD));
   if (HD != 160) {
     // tcgen05 main kernel (attention_sm100.cu); TMEM cannot hold dK+dV+S+dP at hd=160
@@ -486,12 +489,12 @@ int flash_attn_fwd_mma(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat
 
 int flash_attn_bwd(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* out,
                    const __nv_bfloat16* dout, const float* lse, float* D, float* dq_acc,
-                   __nv_bfloat16* dqkv, cudaStream_t st) {
+                   __nv_bfloat16* dqkv, cudaStream_t st, bool d_ready) {
   if (a.seq % 128 != 0) return 1;
   switch (a.head_dim) {
-    case 64: return bwd_impl<64>(a, qkv, out, dout, lse, D, dq_acc, dqkv, st);
-    case 128: return bwd_impl<128>(a, qkv, out, dout, lse, D, dq_acc, dqkv, st);
-    case 160: return bwd_impl<160>(a, qkv, out, dout, lse, D, dq_acc, dqkv, st);
+    case 64: return bwd_impl<64>(a, qkv, out, dout, lse, D, dq_acc, dqkv, st, false);
+    case 128: return bwd_impl<128>(a, qkv, out, dout, lse, D, dq_acc, dqkv, st, d_ready);
+    case 160: return bwd_impl<160>(a, qkv, out, dout, lse, D, dq_acc, dqkv, st, false);
     default: return 1;
   }
 }

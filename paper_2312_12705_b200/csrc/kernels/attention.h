@@ -28,8 +28,10 @@ int flash_attn_bwd_tc_main(const AttnShape& a, const __nv_bfloat16* qkv, const _
                            cudaStream_t st);
 
 // Writes dqkv[M, 3*heads*hd]. Workspaces: D[batch*heads*seq] fp32, dq_acc[M*heads*hd] fp32.
+// d_ready: D = rowsum(dO * O) was already produced (fused into the dO GEMM epilogue); only the
+// dQ accumulator is cleared before the main kernel.
 int flash_attn_bwd(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* out,
                    const __nv_bfloat16* dout, const float* lse, float* D, float* dq_acc,
-                   __nv_bfloat16* dqkv, cudaStream_t st);
+                   __nv_bfloat16* dqkv, cudaStream_t st, bool d_ready = false);
 
 }  // namespace gptb200

@@ -35,6 +35,12 @@ struct GemmParams {
   // vector atomics, which squares up the wave count of the few-tile, long-K weight-gradient GEMMs.
   // 0 = automatic, 1 = off.
   int split_k = 0;
+  // Optional fused row-dot (EPI_BF16 only): rowdot_out[(m / seq * heads + n / hd) * seq + m % seq]
+  // += sum over a head's hd columns of bf16(C[m, n]) * rowdot_b[m * ldc + n] (hd = 128; rowdot_out
+  // zeroed by the caller). Used for the attention-backward D = rowsum(dO * O) on the dO GEMM.
+  float* rowdot_out = nullptr;
+  const __nv_bfloat16* rowdot_b = nullptr;
+  int rowdot_seq = 0, rowdot_heads = 0;
 };
 
 // Requires M % 128 == 0, K % 64 == 0, N % 64 == 0, 16-byte aligned rows.

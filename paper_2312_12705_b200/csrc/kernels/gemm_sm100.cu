@@ -283,6 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
           for (int c2 = ehalf * (BN / 128); c2 < (ehalf + 1) * (BN / 128); ++c2) {  // 64-column units
             uint32_t g[2][16];
+            float rowdot = 0.f;
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
               const int c = 2 * c2 + hh;
@@ -326,6 +327,21 @@ __global__ void __launch_bounds__(kThreads, 1)
               uint32_t packed[16];
 #pragma unroll
               for (int j = 0; j < 16; ++j) packed[j] = ptx::pack_bf16(v[2 * j], v[2 * j + 1]);
+              if constexpr (EPI == EPI_BF16) {
+                if (p.rowdot_out != nullptr) {  // D partial over these 32 columns (of the stored bf16)
+                  const uint4* o4 = reinterpret_cast<const uint4*>(p.rowdot_b + static_cast<size_t>(row) * p.ldc + n);
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    const uint4 ov = o4[j];
+                    const uint32_t ow[4] = {ov.x, ov.y, ov.z, ov.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                      const float2 a = ptx::unpack_bf16(packed[4 * j + e]), b = ptx::unpack_bf16(ow[e]);
+                      rowdot = fmaf(a.x, b.x, fmaf(a.y, b.y, rowdot));
+                    }
+                  }
+                }
+              }
               if constexpr (EPI == EPI_BIAS_GELU) {
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
@@ -339,6 +355,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 put(4 * hh + j, make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]));
             }
             flush(&tmC, nb * BN + c2 * 64, false);
+            if constexpr (EPI == EPI_BF16) {
+              if (p.rowdot_out != nullptr) {  // <= 2 partials per (row, head) onto zero: order-free
+                const int n0 = nb * BN + c2 * 64;
+                const int bq = row / p.rowdot_seq, q = row % p.rowdot_seq;
+                atomicAdd(p.rowdot_out + (static_cast<size_t>(bq) * p.rowdot_heads + n0 / 128) * p.rowdot_seq + q, rowdot);
+              }
+            }
             if constexpr (EPI == EPI_BIAS_GELU) {
               box_free();
 #pragma unroll
@@ -565,6 +588,8 @@ int gemm_bf16(const GemmParams& p, cudaStream_t stream) {
   if (p.epi == EPI_BIAS_GELU && p.C2 == nullptr) return kGemmErrShape;
   if (p.epi == EPI_DGELU && p.aux == nullptr) return kGemmErrShape;
   if (p.split_k > 1 && (p.epi != EPI_F32 || !p.accumulate || p.K / kBK < p.split_k)) return kGemmErrShape;
+  if (p.rowdot_out && (p.epi != EPI_BF16 || p.N % 128 != 0 || p.rowdot_seq <= 0 || p.M % p.rowdot_seq != 0))
+    return kGemmErrShape;
   // CTA pairs (256 x 256 tiles) when the problem yields at least one full wave of pairs;
   // otherwise single-CTA 128 x BN tiles with the widest BN that still fills the machine.
   const bool pair_ok = p.M % 256 == 0 && p.N % 256 == 0;

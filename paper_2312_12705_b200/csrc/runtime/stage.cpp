@@ -373,13 +373,18 @@ void Stage::gemm_fwd(const bf16* X, const bf16* W, const bf16* bias, bf16* Y, in
 }
 
 // dX[M,K] = dY[M,N] . W[N,K]
-void Stage::gemm_dgrad(const bf16* dY, const bf16* W, bf16* dX, int M, int N, int K, int epi, const bf16* aux) {
+void Stage::gemm_dgrad(const bf16* dY, const bf16* W, bf16* dX, int M, int N, int K, int epi, const bf16* aux,
+                       const bf16* rowdot_b) {
   KScope prof(this, K_GEMM, 2.0 * M * N * K);
   GemmParams p;
   p.M = M, p.N = K, p.K = N;
   p.A = dY, p.lda = N, p.a_mn = false;
   p.B = W, p.ldb = K, p.b_mn = true;
   p.C = dX, p.ldc = K, p.epi = epi, p.aux = aux, p.ldaux = K;
+  if (rowdot_b) {  // attention backward's D = rowsum(dO * O) from the dO epilogue
+    cudaMemsetAsync(attn_D_, 0, static_cast<size_t>(mbs_) * ht_ * s_ * sizeof(float), st_);
+    p.rowdot_out = attn_D_, p.rowdot_b = rowdot_b, p.rowdot_seq = s_, p.rowdot_heads = ht_;
+  }
   ck(gemm_bf16(p, st_), "gemm dgrad");
 }
 
@@ -644,6 +649,7 @@ void Stage::layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2)
   const LayerW W = w(l);
   const LayerG G = gr(l);
   const bool drop_on = opts_.dropout > 0.f;
+  const bool fuse_d = hd_ == 128 && dt_ % 128 == 0;  // D computed in the W_o dgrad epilogue
   const int64_t sample0 = static_cast<int64_t>(comms_.me.d) * (cfg_.gbs / cfg_.dp) +
                           static_cast<int64_t>(cur_mb_) * mbs_;
   // MLP branch
@@ -663,11 +669,11 @@ void Stage::layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2)
     g.drop = drop_key(opts_, step_no_, lg, 0, sample0, s_, d_);
     g.dxd_off = woff(dy_), g.dgamma = G.ln2g, g.dbeta = G.ln2b, g.dbias = G.bo;
     sp_bwd(g);
-    gemm_dgrad(dy_, W.wo, do_, M_, d_, dt_);
+    gemm_dgrad(dy_, W.wo, do_, M_, d_, dt_, EPI_BF16, nullptr, fuse_d ? A.o : nullptr);
     gemm_wgrad(dy_, A.o, G.wo, M_, d_, dt_);
     {
       KScope prof(this, K_ATTN_BWD, 5.0 * mbs_ * ht_ * static_cast<double>(s_) * s_ * hd_);
-      ck(flash_attn_bwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, do_, A.lse, attn_D_, dq_acc_, dqkv_, st_), "flash bwd");
+      ck(flash_attn_bwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, do_, A.lse, attn_D_, dq_acc_, dqkv_, st_, fuse_d), "flash bwd");
     }
     {
       KScope prof(this, K_ELEM);
@@ -704,11 +710,11 @@ void Stage::layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2)
   }
   const bf16* dya = drop_on ? dy_ : dh;
   // attention branch
-  gemm_dgrad(dya, W.wo, do_, M_, d_, dt_);
+  gemm_dgrad(dya, W.wo, do_, M_, d_, dt_, EPI_BF16, nullptr, fuse_d ? A.o : nullptr);
   gemm_wgrad(dya, A.o, G.wo, M_, d_, dt_);
   {
     KScope prof(this, K_ATTN_BWD, 5.0 * mbs_ * ht_ * static_cast<double>(s_) * s_ * hd_);
-    ck(flash_attn_bwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, do_, A.lse, attn_D_, dq_acc_, dqkv_, st_), "flash bwd");
+    ck(flash_attn_bwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, do_, A.lse, attn_D_, dq_acc_, dqkv_, st_, fuse_d), "flash bwd");
   }
   {
     KScope prof(this, K_ELEM);

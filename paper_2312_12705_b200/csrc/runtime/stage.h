@@ -150,7 +150,7 @@ class Stage {
   void gemm_fwd(const bf16* X, const bf16* W, const bf16* bias, bf16* Y, int M, int N, int K, int epi = 0,
                 bf16* C2 = nullptr);
   void gemm_dgrad(const bf16* dY, const bf16* W, bf16* dX, int M, int N, int K, int epi = 0,
-                  const bf16* aux = nullptr);
+                  const bf16* aux = nullptr, const bf16* rowdot_b = nullptr);
   void gemm_wgrad(const bf16* dY, const bf16* X, float* dW, int M, int N, int K);
   void ck(int status, const char* what);
   friend struct KScope;

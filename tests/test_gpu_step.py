@@ -117,6 +117,11 @@ def test_step_parity_head_dim_128_activation_checkpointing():
     run_parity(L=2, d=512, heads=4, V=2048, s=256, mbs=2, gbs=2, ckpt=True)
 
 
+def test_step_parity_head_dim_128_dropout():
+    # hd 128: tcgen05 backward with D = rowsum(dO*O) fused into the W_o dgrad GEMM epilogue
+    run_parity(L=2, d=512, heads=4, V=2048, s=256, mbs=2, gbs=4, dropout=0.1)
+
+
 def test_step_parity_full_vocab():
     run_parity(L=1, d=256, heads=4, V=51200, s=128, mbs=1, gbs=2)
 
