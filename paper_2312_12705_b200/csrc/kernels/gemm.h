@@ -38,6 +38,10 @@ struct GemmParams {
   // Optional fused row-dot (EPI_BF16 only): rowdot_out[(m / seq * heads + n / hd) * seq + m % seq]
   // += sum over a head's hd columns of bf16(C[m, n]) * rowdot_b[m * ldc + n] (hd = 128; rowdot_out
   // zeroed by the caller). Used for the attention-backward D = rowsum(dO * O) on the dO GEMM.
+  // Optional column partial sums of the stored bf16 C (EPI_DGELU / EPI_BF16, N % 128 == 0):
+  // colsum_part[(m / 32) * N + n] = sum of C[m', n] over the 32-row block of m (deterministic;
+  // reduce over the M/32 blocks afterwards). Used for the fc1 bias gradient from dGeLU(dgrad).
+  float* colsum_part = nullptr;
   float* rowdot_out = nullptr;
   const __nv_bfloat16* rowdot_b = nullptr;
   int rowdot_seq = 0, rowdot_heads = 0;

@@ -355,6 +355,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 put(4 * hh + j, make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]));
             }
             flush(&tmC, nb * BN + c2 * 64, false);
+            if constexpr (EPI == EPI_BF16 || EPI == EPI_DGELU) {
+              if (p.colsum_part != nullptr) {  // this warp's 32 rows x 64 columns, from the staged box
+                float s0 = 0.f, s1 = 0.f;
+#pragma unroll 8
+                for (int r = 0; r < 32; ++r) {
+                  const uint8_t* brow = box + r * 128;
+                  s0 += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
+                      brow + (((lane >> 3) ^ (r & 7)) << 4) + (lane & 7) * 2));
+                  s1 += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
+                      brow + ((((lane >> 3) + 4) ^ (r & 7)) << 4) + (lane & 7) * 2));
+                }
+                float* dst = p.colsum_part + static_cast<size_t>(row_base / 32) * p.N + nb * BN + c2 * 64;
+                dst[lane] = s0;
+                dst[lane + 32] = s1;
+              }
+            }
             if constexpr (EPI == EPI_BF16) {
               if (p.rowdot_out != nullptr) {  // <= 2 partials per (row, head) onto zero: order-free
                 const int n0 = nb * BN + c2 * 64;
@@ -588,6 +604,7 @@ int gemm_bf16(const GemmParams& p, cudaStream_t stream) {
   if (p.epi == EPI_BIAS_GELU && p.C2 == nullptr) return kGemmErrShape;
   if (p.epi == EPI_DGELU && p.aux == nullptr) return kGemmErrShape;
   if (p.split_k > 1 && (p.epi != EPI_F32 || !p.accumulate || p.K / kBK < p.split_k)) return kGemmErrShape;
+  if (p.colsum_part && ((p.epi != EPI_BF16 && p.epi != EPI_DGELU) || p.N % 128 != 0)) return kGemmErrShape;
   if (p.rowdot_out && (p.epi != EPI_BF16 || p.N % 128 != 0 || p.rowdot_seq <= 0 || p.M % p.rowdot_seq != 0))
     return kGemmErrShape;
   // CTA pairs (256 x 256 tiles) when the problem yields at least one full wave of pairs;

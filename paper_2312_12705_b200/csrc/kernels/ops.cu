@@ -833,6 +833,12 @@ int ln_bwd_cols(const LnBwdArgs& a, const bf16* dbias_src, cudaStream_t st) {
   return status();
 }
 
+int reduce_col_partials(const float* partial, int nblocks, int n, float* out, cudaStream_t st) {
+  if (nblocks <= 0 || n <= 0) return 1;
+  reduce_partials_kernel<<<(n + 31) / 32, 256, 0, st>>>(partial, nblocks, n, n, out, nullptr, nullptr);
+  return status();
+}
+
 size_t colsum_workspace_floats(int rows, int n) {
   return static_cast<size_t>((rows + kColsumRows - 1) / kColsumRows) * n;
 }

@@ -76,6 +76,10 @@ int ln_bwd_cols(const LnBwdArgs& a, const bf16* dbias_src, cudaStream_t st);
 size_t colsum_workspace_floats(int rows, int n);
 int colsum_bf16(const bf16* X, int rows, int n, float* out, float* workspace, cudaStream_t st);
 
+// out[c] += sum_b partial[b * n + c] over nblocks (deterministic order); for GEMM-epilogue column
+// partials (GemmParams::colsum_part).
+int reduce_col_partials(const float* partial, int nblocks, int n, float* out, cudaStream_t st);
+
 // Vocab-parallel embedding lookup: out[r, :] = wte_shard[tok[r] - vstart] if the token is in
 // [vstart, vstart + vrows) else 0.
 int embed_lookup(const int32_t* tokens, int rows, const bf16* wte_shard, int vstart, int vrows,

@@ -273,6 +273,7 @@ void Stage::allocate() {
   size_t ws = std::max({colsum_workspace_floats(M_, 4 * dt_), colsum_workspace_floats(M_, 3 * dt_),
                         ln_bwd_workspace_floats(M_, d_)});
   ws_ = static_cast<float*>(alloc(ws * 4));
+  colpart_ = static_cast<float*>(alloc(static_cast<size_t>(M_ / 32) * 4 * dt * 4));
   if (last_) {
     hf_ = sp_ ? full(Md) : static_cast<bf16*>(alloc(Md * 2));
     muf_ = static_cast<float*>(alloc(Ms * 4));
@@ -374,13 +375,14 @@ void Stage::gemm_fwd(const bf16* X, const bf16* W, const bf16* bias, bf16* Y, in
 
 // dX[M,K] = dY[M,N] . W[N,K]
 void Stage::gemm_dgrad(const bf16* dY, const bf16* W, bf16* dX, int M, int N, int K, int epi, const bf16* aux,
-                       const bf16* rowdot_b) {
+                       const bf16* rowdot_b, float* colsum_part) {
   KScope prof(this, K_GEMM, 2.0 * M * N * K);
   GemmParams p;
   p.M = M, p.N = K, p.K = N;
   p.A = dY, p.lda = N, p.a_mn = false;
   p.B = W, p.ldb = K, p.b_mn = true;
   p.C = dX, p.ldc = K, p.epi = epi, p.aux = aux, p.ldaux = K;
+  p.colsum_part = colsum_part;
   if (rowdot_b) {  // attention backward's D = rowsum(dO * O) from the dO epilogue
     cudaMemsetAsync(attn_D_, 0, static_cast<size_t>(mbs_) * ht_ * s_ * sizeof(float), st_);
     p.rowdot_out = attn_D_, p.rowdot_b = rowdot_b, p.rowdot_seq = s_, p.rowdot_heads = ht_;
@@ -653,11 +655,11 @@ void Stage::layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2)
   const int64_t sample0 = static_cast<int64_t>(comms_.me.d) * (cfg_.gbs / cfg_.dp) +
                           static_cast<int64_t>(cur_mb_) * mbs_;
   // MLP branch
-  gemm_dgrad(dy2, W.w2, du_, M_, d_, 4 * dt_, EPI_DGELU, A.u);
+  gemm_dgrad(dy2, W.w2, du_, M_, d_, 4 * dt_, EPI_DGELU, A.u, nullptr, colpart_);  // + db1 partials
   gemm_wgrad(dy2, A.g, G.w2, M_, d_, 4 * dt_);
   {
     KScope prof(this, K_ELEM);
-    ck(colsum_bf16(du_, M_, 4 * dt_, G.b1, ws_, st_), "db1");
+    ck(reduce_col_partials(colpart_, M_ / 32, 4 * dt_, G.b1, st_), "db1");
   }
   gemm_dgrad(du_, W.w1, dm_, M_, 4 * dt_, d_);
   if (sp_) {

@@ -150,7 +150,7 @@ class Stage {
   void gemm_fwd(const bf16* X, const bf16* W, const bf16* bias, bf16* Y, int M, int N, int K, int epi = 0,
                 bf16* C2 = nullptr);
   void gemm_dgrad(const bf16* dY, const bf16* W, bf16* dX, int M, int N, int K, int epi = 0,
-                  const bf16* aux = nullptr, const bf16* rowdot_b = nullptr);
+                  const bf16* aux = nullptr, const bf16* rowdot_b = nullptr, float* colsum_part = nullptr);
   void gemm_wgrad(const bf16* dY, const bf16* X, float* dW, int M, int N, int K);
   void ck(int status, const char* what);
   friend struct KScope;
@@ -225,6 +225,7 @@ class Stage {
   bf16 *tmp_md_ = nullptr, *dy_ = nullptr, *du_ = nullptr, *dm_ = nullptr,
        *do_ = nullptr, *dqkv_ = nullptr;
   float *attn_D_ = nullptr, *dq_acc_ = nullptr, *ws_ = nullptr;
+  float* colpart_ = nullptr;  // [M/32][4d/t] column partials of the dGeLU dgrad (fc1 bias grad)
   bf16* hf_ = nullptr;
   float *muf_ = nullptr, *rsf_ = nullptr;
   bf16* logits_ = nullptr;
