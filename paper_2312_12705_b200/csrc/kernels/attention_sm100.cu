@@ -18,6 +18,7 @@
 #include "tma_host.h"
 
 #include <cstdio>
+#include <cstdlib>
 
 namespace gptb200 {
 
@@ -56,11 +57,13 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-template <int HD>
+// PT: P stays in TMEM (bf16 over the S columns it replaces) and PV reads its A operand from TMEM;
+// without PT, P is staged through 128B-swizzled smem.
+template <int HD, bool PT>
 struct TcFwdCfg {
   static constexpr int NC = (HD + 63) / 64;             // 64-wide swizzle chunks of the head dim
-  static constexpr int kStages = NC <= 2 ? 2 : 1;       // K ring and V ring depth
-  static constexpr int kPBufs = NC <= 2 ? 2 : 1;        // P double buffer when smem allows
+  static constexpr int kStages = PT ? (NC <= 2 ? 3 : 1) : (NC <= 2 ? 2 : 1);  // K ring and V ring depth
+  static constexpr int kPBufs = PT ? 0 : (NC <= 2 ? 2 : 1);                   // smem P buffers
   static constexpr int kTileBytes = 128 * 128;          // one [128 rows][64] bf16 chunk
   static constexpr int kQBytes = NC * kTileBytes;
   static constexpr int kKVBytes = NC * kTileBytes;
@@ -69,19 +72,19 @@ struct TcFwdCfg {
   static constexpr int kTmemCols = 512;                 // S0 | S1 | O
 };
 
-template <int HD>
+template <int HD, bool PT>
 __global__ void __launch_bounds__(320, 1)
     fa_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, __nv_bfloat16* __restrict__ out,
                      float* __restrict__ lse, int s, int ht, float scale_log2) {
-  using Cfg = TcFwdCfg<HD>;
-  constexpr int NC = Cfg::NC, ST = Cfg::kStages, PB = Cfg::kPBufs;
+  using Cfg = TcFwdCfg<HD, PT>;
+  constexpr int NC = Cfg::NC, ST = Cfg::kStages, PB = PT ? 2 : Cfg::kPBufs;  // PB: P / PV barrier slots
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = ptx::smem_align1024(smem_raw);
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + Cfg::kQBytes;             // [ST][NC][128][64]
   uint8_t* sV = sK + ST * Cfg::kKVBytes;       // [ST][NC][128][64]
-  uint8_t* sP = sV + ST * Cfg::kKVBytes;       // [PB][2][128][64]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + PB * Cfg::kPBytes);
+  uint8_t* sP = sV + ST * Cfg::kKVBytes;       // [kPBufs][2][128][64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + Cfg::kPBufs * Cfg::kPBytes);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;        // [ST]
   uint64_t* k_empty = k_full + ST;    // [ST]  released when S_j completes
@@ -112,7 +115,7 @@ __global__ void __launch_bounds__(320, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&s_free[i], 8);
+      ptx::mbar_init(&s_free[i], PT ? 1 : 8);  // PT: freed by the PV commit that consumed P
     }
     for (int i = 0; i < PB; ++i) {
       ptx::mbar_init(&p_full[i], 8);
@@ -161,12 +164,17 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t pa = p_addr + pb * Cfg::kPBytes;
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk) {
-          const uint64_t a = ptx::smem_desc_sw128(pa + (kk / 4) * Cfg::kTileBytes + (kk % 4) * 32, 16, 1024);
           const uint64_t bd = ptx::smem_desc_sw128(v_addr + kk * 2048, Cfg::kTileBytes, 1024);
-          ptx::mma_bf16_ss_w(tO, a, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          if constexpr (PT) {  // P: 8 packed bf16x2 TMEM columns per K = 16 step
+            ptx::mma_bf16_ts_w(tO, tmem + (j & 1) * kBN + kk * 8, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          } else {
+            const uint64_t a = ptx::smem_desc_sw128(pa + (kk / 4) * Cfg::kTileBytes + (kk % 4) * 32, 16, 1024);
+            ptx::mma_bf16_ss_w(tO, a, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          }
         }
         ptx::mma_commit_w(&pv_done[pb]);
         ptx::mma_commit_w(&v_empty[st]);
+        if constexpr (PT) ptx::mma_commit_w(&s_free[j & 1]);  // P (in S_j's columns) consumed
       };
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j % ST, buf = j & 1;
@@ -215,9 +223,11 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) x[c * 32 + i] = __uint_as_float(v[i]);
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&s_free[buf]);
+      if constexpr (!PT) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&s_free[buf]);
+      }
       if (j == qb) {  // diagonal tile: causal mask (the only tile that needs one)
 #pragma unroll
         for (int i = 0; i < 64; ++i)
@@ -233,9 +243,9 @@ __global__ void __launch_bounds__(320, 1)
       float mt = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
       mt *= scale_log2;
       xmax[half * 128 + r] = mt;
-      named_sync(1, 256);
+      named_sync(1 + quarter, 64);
       mt = fmaxf(mt, xmax[(half ^ 1) * 128 + r]);
-      named_sync(1, 256);  // exchange slots are reused next tile
+      named_sync(1 + quarter, 64);  // exchange slots are reused next tile
       // Lazy rescale (only when a row's max grows by > 2^8). tcgen05.ld/st are warp-collective,
       // so the decision is warp-uniform (and identical in both halves of a row).
       if (__any_sync(0xffffffffu, mt > m_used + 8.f)) {
@@ -259,36 +269,55 @@ __global__ void __launch_bounds__(320, 1)
         }
         m_used = m_new;
       }
-      // the P buffer of tile j must be free of PV_{j-PB}
-      if (j >= PB) WAIT(&pv_done[j % PB], ((j / PB) - 1) & 1, 10);
-      uint8_t* p_row = p_row0 + (j % PB) * Cfg::kPBytes;
-      // P = exp2(x - m_used) -> bf16 into this half's 64-column swizzle chunk, 16B unit u
       const float neg_m = -m_used;
       float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // independent partial row sums
+      if constexpr (PT) {
+        // P = exp2(x - m_used) as bf16 pairs into this half's 32 columns of S_j (already read by both
+        // halves: the max exchange above is a barrier), the A operand of PV_j
+        uint32_t pk[32];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        float p[8];
+        for (int u = 0; u < 8; ++u) {
+          float p[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          p[e] = ex2(fmaf(x[u * 8 + e], scale_log2, neg_m));
-          ls[e] += p[e];
+          for (int e = 0; e < 8; ++e) {
+            p[e] = ex2(fmaf(x[u * 8 + e], scale_log2, neg_m));
+            ls[e] += p[e];
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) pk[u * 4 + e] = ptx::pack_bf16(p[2 * e], p[2 * e + 1]);
         }
-        uint4 pk;
-        pk.x = ptx::pack_bf16(p[0], p[1]);
-        pk.y = ptx::pack_bf16(p[2], p[3]);
-        pk.z = ptx::pack_bf16(p[4], p[5]);
-        pk.w = ptx::pack_bf16(p[6], p[7]);
-        *reinterpret_cast<uint4*>(p_row + ((u ^ (r & 7)) * 16)) = pk;
+        ptx::tmem_st_32x32b_x32(tmem + lane_base + buf * kBN + half * 32, pk);
+        ptx::tmem_st_wait();
+      } else {
+        // the P buffer of tile j must be free of PV_{j-PB}
+        if (j >= PB) WAIT(&pv_done[j % PB], ((j / PB) - 1) & 1, 10);
+        uint8_t* p_row = p_row0 + (j % PB) * Cfg::kPBytes;
+        // P = exp2(x - m_used) -> bf16 into this half's 64-column swizzle chunk, 16B unit u
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          float p[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            p[e] = ex2(fmaf(x[u * 8 + e], scale_log2, neg_m));
+            ls[e] += p[e];
+          }
+          uint4 pk;
+          pk.x = ptx::pack_bf16(p[0], p[1]);
+          pk.y = ptx::pack_bf16(p[2], p[3]);
+          pk.z = ptx::pack_bf16(p[4], p[5]);
+          pk.w = ptx::pack_bf16(p[6], p[7]);
+          *reinterpret_cast<uint4*>(p_row + ((u ^ (r & 7)) * 16)) = pk;
+        }
+        ptx::fence_proxy_async();
       }
       l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
-      ptx::fence_proxy_async();
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&p_full[j % PB]);
     }
     // combine the two halves' row sums
     xmax[half * 128 + r] = l;
-    named_sync(1, 256);
+    named_sync(1 + quarter, 64);
     const float l_tot = l + xmax[(half ^ 1) * 128 + r];
     WAIT(&pv_done[(n_tiles - 1) % PB], ((n_tiles - 1) / PB) & 1, 11);
     ptx::tc_fence_after();
@@ -919,12 +948,12 @@ int bwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* do
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
-template <int HD>
+template <int HD, bool PT>
 int fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, cudaStream_t st) {
-  using Cfg = TcFwdCfg<HD>;
+  using Cfg = TcFwdCfg<HD, PT>;
   static bool init = false;
   if (!init) {
-    if (cudaFuncSetAttribute(fa_fwd_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
+    if (cudaFuncSetAttribute(fa_fwd_tc_kernel<HD, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
         cudaSuccess)
       return 3;
     init = true;
@@ -934,7 +963,7 @@ int fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, flo
   if (!make_tmap_bf16(&tm, qkv, 3 * static_cast<uint64_t>(dt), static_cast<uint64_t>(a.batch) * a.seq, 3 * dt, 64, 128))
     return 3;
   dim3 grid(a.seq / kBM, a.batch * a.heads);
-  fa_fwd_tc_kernel<HD><<<grid, 320, Cfg::kSmem, st>>>(tm, out, lse, a.seq, a.heads,
+  fa_fwd_tc_kernel<HD, PT><<<grid, 320, Cfg::kSmem, st>>>(tm, out, lse, a.seq, a.heads,
                                                        kLog2e / sqrtf(static_cast<float>(HD)));
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
@@ -953,10 +982,11 @@ int flash_attn_bwd_tc_main(const AttnShape& a, const __nv_bfloat16* qkv, const _
 
 int flash_attn_fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, cudaStream_t st) {
   if (a.seq % kBM != 0) return 1;
+  static const bool p_smem = std::getenv("GPTB200_ATTN_P_SMEM") != nullptr;  // A/B hook
   switch (a.head_dim) {
-    case 64: return fwd_tc<64>(a, qkv, out, lse, st);
-    case 128: return fwd_tc<128>(a, qkv, out, lse, st);
-    case 160: return fwd_tc<160>(a, qkv, out, lse, st);
+    case 64: return p_smem ? fwd_tc<64, false>(a, qkv, out, lse, st) : fwd_tc<64, true>(a, qkv, out, lse, st);
+    case 128: return p_smem ? fwd_tc<128, false>(a, qkv, out, lse, st) : fwd_tc<128, true>(a, qkv, out, lse, st);
+    case 160: return p_smem ? fwd_tc<160, false>(a, qkv, out, lse, st) : fwd_tc<160, true>(a, qkv, out, lse, st);
     default: return 1;
   }
 }
