@@ -104,6 +104,12 @@ Stage::~Stage() {
       cudaStreamDestroy(send_st_[i]);
       cudaEventDestroy(send_done_ev_[i]);
     }
+  if (sp_st_) {
+    cudaStreamSynchronize(sp_st_);
+    cudaStreamDestroy(sp_st_);
+    cudaEventDestroy(sp_fork_);
+    cudaEventDestroy(sp_join_);
+  }
   for (auto& e : slot_send_ev_) cudaEventDestroy(e);
   for (auto& e : dh_send_ev_)
     if (e) cudaEventDestroy(e);
@@ -284,6 +290,11 @@ void Stage::allocate() {
     row_loss_ = static_cast<float*>(alloc(M * 4));
   }
   loss_acc_ = static_cast<float*>(alloc(4));
+  if (sp_) {
+    cudaStreamCreateWithFlags(&sp_st_, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&sp_fork_, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&sp_join_, cudaEventDisableTiming);
+  }
   if (cfg_.pp > 1) {
     for (int i = 0; i < 2; ++i) {
       cudaStreamCreateWithFlags(&send_st_[i], cudaStreamNonBlocking);
@@ -663,14 +674,15 @@ void Stage::layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2)
   }
   gemm_dgrad(du_, W.w1, dm_, M_, 4 * dt_, d_);
   if (sp_) {
-    gemm_wgrad(du_, A.m2, G.w1, M_, 4 * dt_, d_);
+    // the fused reduce-scatter + LN2 backward needs only the dgrad partials: it runs on the SP
+    // stream while the independent fc1 weight-gradient GEMM runs here (NVLink under tensor work)
     SpLnBwdArgs g;
     g.nrows = Ms_, g.row0 = row0_, g.d = d_, g.workspace = ws_;
     g.dy_off = woff(dm_), g.x = A.hmid, g.gamma = W.ln2g, g.mean = A.mu2, g.rstd = A.rs2;
     g.resid_grad = dh, g.dx = dh;
     g.drop = drop_key(opts_, step_no_, lg, 0, sample0, s_, d_);
     g.dxd_off = woff(dy_), g.dgamma = G.ln2g, g.dbeta = G.ln2b, g.dbias = G.bo;
-    sp_bwd(g);
+    sp_bwd_overlapped(g, [&] { gemm_wgrad(du_, A.m2, G.w1, M_, 4 * dt_, d_); });
     gemm_dgrad(dy_, W.wo, do_, M_, d_, dt_, EPI_BF16, nullptr, fuse_d ? A.o : nullptr);
     gemm_wgrad(dy_, A.o, G.wo, M_, d_, dt_);
     {
@@ -682,7 +694,6 @@ void Stage::layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2)
       ck(colsum_bf16(dqkv_, M_, 3 * dt_, G.bqkv, ws_, st_), "dbqkv");
     }
     gemm_dgrad(dqkv_, W.wqkv, dm_, M_, 3 * dt_, d_);
-    gemm_wgrad(dqkv_, A.a, G.wqkv, M_, 3 * dt_, d_);
     SpLnBwdArgs g1;
     g1.nrows = Ms_, g1.row0 = row0_, g1.d = d_, g1.workspace = ws_;
     g1.dy_off = woff(dm_), g1.x = hin, g1.gamma = W.ln1g, g1.mean = A.mu1, g1.rstd = A.rs1;
@@ -694,7 +705,7 @@ void Stage::layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2)
       g1.drop = drop_key(opts_, step_no_, kEmbedLayer, 2, sample0, s_, d_);
       g1.dxd_off = woff(dy_);
     }
-    sp_bwd(g1);
+    sp_bwd_overlapped(g1, [&] { gemm_wgrad(dqkv_, A.a, G.wqkv, M_, 3 * dt_, d_); });
     return;
   }
   tp_allreduce(dm_);
@@ -831,6 +842,25 @@ void Stage::sp_fwd(const SpLnFwdArgs& a) {
   KScope prof(this, K_COMM_TP, 0, (a.y_off >= 0 ? 2.0 : 0.0) * M_ * d_ + 6.0 * Ms_ * d_);
   const int r = sp_ln_fwd(comms_.tp_nvls, a, st_);
   if (r != 0) throw StepError{r == 1 ? TP_ERR_INVALID : TP_ERR_CUDA, "sequence-parallel LN forward failed"};
+}
+
+// SP backward on sp_st_ concurrently with `independent` (a weight-gradient GEMM) on st_; the step
+// stream joins before the next consumer of dh / dy_. SP kernels stay totally ordered on every rank.
+template <typename F>
+void Stage::sp_bwd_overlapped(const SpLnBwdArgs& a, F&& independent) {
+  if (profile_ || !sp_st_) {  // profiled pass: keep every launch on the timed stream
+    independent();
+    sp_bwd(a);
+    return;
+  }
+  cudaEventRecord(sp_fork_, st_);
+  cudaStreamWaitEvent(sp_st_, sp_fork_, 0);
+  launches_ += 3;
+  const int r = sp_ln_bwd(comms_.tp_nvls, a, sp_st_);
+  if (r != 0) throw StepError{r == 1 ? TP_ERR_INVALID : TP_ERR_CUDA, "sequence-parallel LN backward failed"};
+  independent();
+  cudaEventRecord(sp_join_, sp_st_);
+  cudaStreamWaitEvent(st_, sp_join_, 0);
 }
 
 void Stage::sp_bwd(const SpLnBwdArgs& a) {

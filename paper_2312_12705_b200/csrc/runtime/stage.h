@@ -170,6 +170,10 @@ class Stage {
   int64_t woff(const void* p) const;  // window offset of an SP buffer (throws when outside)
   void sp_fwd(const SpLnFwdArgs& a);
   void sp_bwd(const SpLnBwdArgs& a);
+  template <typename F>
+  void sp_bwd_overlapped(const SpLnBwdArgs& a, F&& independent);
+  cudaStream_t sp_st_ = nullptr;
+  cudaEvent_t sp_fork_ = nullptr, sp_join_ = nullptr;
   int64_t slot_offset(int tid) const { return slot(tid)->offset; }
 
   trainplan::ModelSpec model_;
