@@ -57,44 +57,48 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// PT: P stays in TMEM (bf16 over the S columns it replaces) and PV reads its A operand from TMEM;
-// without PT, P is staged through 128B-swizzled smem.
-template <int HD, bool PT>
+// P stays in TMEM (bf16 over the S columns it replaces) and PV reads its A operand from TMEM.
+// CS softmax warps per TMEM lane quarter, each owning 128/CS score columns of its 32 query rows.
+template <int HD>
 struct TcFwdCfg {
   static constexpr int NC = (HD + 63) / 64;             // 64-wide swizzle chunks of the head dim
-  static constexpr int kStages = PT ? (NC <= 2 ? 3 : 1) : (NC <= 2 ? 2 : 1);  // K ring and V ring depth
-  static constexpr int kPBufs = PT ? 0 : (NC <= 2 ? 2 : 1);                   // smem P buffers
+  static constexpr int kStages = NC <= 2 ? 3 : 1;       // K ring and V ring depth
+  static constexpr int CS = 4;                          // column splits (softmax warps per quarter)
+  static constexpr int kThreads = 64 + 128 * CS;
   static constexpr int kTileBytes = 128 * 128;          // one [128 rows][64] bf16 chunk
   static constexpr int kQBytes = NC * kTileBytes;
   static constexpr int kKVBytes = NC * kTileBytes;
-  static constexpr int kPBytes = 2 * kTileBytes;        // P [128][128] = 2 chunks
-  static constexpr int kSmem = kQBytes + 2 * kStages * kKVBytes + kPBufs * kPBytes + 1024 + 256 + 1024;
+  // dynamic smem is declared __align__(1024) (checked at run time), so no alignment slack
+  static constexpr int kSmem = kQBytes + 2 * kStages * kKVBytes + CS * 128 * 4 + 256;
+  static_assert(kSmem <= 232448, "fa_fwd smem over the 227 KB opt-in limit");
   static constexpr int kTmemCols = 512;                 // S0 | S1 | O
 };
 
-template <int HD, bool PT>
-__global__ void __launch_bounds__(320, 1)
+template <int HD>
+__global__ void __launch_bounds__(TcFwdCfg<HD>::kThreads, 1)
     fa_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, __nv_bfloat16* __restrict__ out,
                      float* __restrict__ lse, int s, int ht, float scale_log2) {
-  using Cfg = TcFwdCfg<HD, PT>;
-  constexpr int NC = Cfg::NC, ST = Cfg::kStages, PB = PT ? 2 : Cfg::kPBufs;  // PB: P / PV barrier slots
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = ptx::smem_align1024(smem_raw);
+  using Cfg = TcFwdCfg<HD>;
+  constexpr int NC = Cfg::NC, ST = Cfg::kStages, CS = Cfg::CS;
+  constexpr int CW = kBN / CS;  // score columns per softmax warp
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if ((ptx::smem_u32(smem_raw) & 1023u) != 0) __trap();  // 128B-swizzle atoms need 1 KB alignment
+  uint8_t* smem = smem_raw;
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + Cfg::kQBytes;             // [ST][NC][128][64]
   uint8_t* sV = sK + ST * Cfg::kKVBytes;       // [ST][NC][128][64]
-  uint8_t* sP = sV + ST * Cfg::kKVBytes;       // [kPBufs][2][128][64]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + Cfg::kPBufs * Cfg::kPBytes);
+  float* xch = reinterpret_cast<float*>(sV + ST * Cfg::kKVBytes);  // [CS][128] row max / sum exchange
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xch + CS * 128);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;        // [ST]
   uint64_t* k_empty = k_full + ST;    // [ST]  released when S_j completes
   uint64_t* v_full = k_empty + ST;    // [ST]
   uint64_t* v_empty = v_full + ST;    // [ST]  released when PV_j completes
   uint64_t* s_full = v_empty + ST;    // [2]
-  uint64_t* s_free = s_full + 2;      // [2]
-  uint64_t* p_full = s_free + 2;      // [PB]
-  uint64_t* pv_done = p_full + PB;    // [PB]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + PB);
+  uint64_t* s_free = s_full + 2;      // [2]   released by the PV commit that consumed P_j
+  uint64_t* p_full = s_free + 2;      // [2]
+  uint64_t* pv_done = p_full + 2;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
 
   // warp index via shfl: provably warp-uniform, so role branches are not treated as divergent
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
@@ -115,10 +119,8 @@ __global__ void __launch_bounds__(320, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&s_free[i], PT ? 1 : 8);  // PT: freed by the PV commit that consumed P
-    }
-    for (int i = 0; i < PB; ++i) {
-      ptx::mbar_init(&p_full[i], 8);
+      ptx::mbar_init(&s_free[i], 1);
+      ptx::mbar_init(&p_full[i], 4 * CS);
       ptx::mbar_init(&pv_done[i], 1);
     }
     ptx::fence_mbar_init();
@@ -153,28 +155,22 @@ __global__ void __launch_bounds__(320, 1)
     {  // all 32 lanes: uniform descriptors, one elected lane issues
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBM, kBN, false, false);
       constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(kBM, HD, false, true);
-      const uint32_t q_addr = ptx::smem_u32(sQ), p_addr = ptx::smem_u32(sP);
+      const uint32_t q_addr = ptx::smem_u32(sQ);
       WAIT(q_full, 0, 3);
       auto issue_pv = [&](int j) {
-        const int st = j % ST, pb = j % PB;
-        WAIT(&p_full[pb], (j / PB) & 1, 4);
+        const int st = j % ST, pb = j & 1;
+        WAIT(&p_full[pb], (j >> 1) & 1, 4);
         WAIT(&v_full[st], (j / ST) & 1, 5);
         ptx::tc_fence_after();
         const uint32_t v_addr = ptx::smem_u32(sV + st * Cfg::kKVBytes);
-        const uint32_t pa = p_addr + pb * Cfg::kPBytes;
 #pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk) {
+        for (int kk = 0; kk < kBN / 16; ++kk) {  // P: 8 packed bf16x2 TMEM columns per K = 16 step
           const uint64_t bd = ptx::smem_desc_sw128(v_addr + kk * 2048, Cfg::kTileBytes, 1024);
-          if constexpr (PT) {  // P: 8 packed bf16x2 TMEM columns per K = 16 step
-            ptx::mma_bf16_ts_w(tO, tmem + (j & 1) * kBN + kk * 8, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-          } else {
-            const uint64_t a = ptx::smem_desc_sw128(pa + (kk / 4) * Cfg::kTileBytes + (kk % 4) * 32, 16, 1024);
-            ptx::mma_bf16_ss_w(tO, a, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-          }
+          ptx::mma_bf16_ts_w(tO, tmem + pb * kBN + kk * 8, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
         ptx::mma_commit_w(&pv_done[pb]);
         ptx::mma_commit_w(&v_empty[st]);
-        if constexpr (PT) ptx::mma_commit_w(&s_free[j & 1]);  // P (in S_j's columns) consumed
+        ptx::mma_commit_w(&s_free[pb]);  // P (in S_j's columns) consumed
       };
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j % ST, buf = j & 1;
@@ -186,7 +182,7 @@ __global__ void __launch_bounds__(320, 1)
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk / 4) * Cfg::kTileBytes + (kk % 4) * 32;
           ptx::mma_bf16_ss_w(tmem + buf * kBN, ptx::smem_desc_sw128(q_addr + off, 16, 1024),
-                           ptx::smem_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+                             ptx::smem_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
         }
         ptx::mma_commit_w(&s_full[buf]);
         ptx::mma_commit_w(&k_empty[st]);
@@ -196,63 +192,59 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
-    // 8 warps: warp w owns TMEM lane quarter (w & 3) = query rows 32q..32q+31 and one half of the
-    // 128 score columns (the other half belongs to the warp with the same quarter); the two
-    // halves exchange their row max through smem once per tile and their row sums at the end.
+    // CS warps per TMEM lane quarter: warp owns query rows 32q..32q+31 (its lanes) and CW score
+    // columns; the CS column parts of a row exchange their max through smem once per tile (one
+    // named barrier per quarter) and their row sums at the end.
     const int quarter = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int part = (warp - 2) >> 2;   // 0..CS-1
     const int r = quarter * 32 + lane;  // query row within the block == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
     const int q_row = qb * kBM + r;
-    constexpr int NCH = HD / 32;           // 32-column chunks of O
-    const int oc0 = half ? (NCH + 1) / 2 : 0, oc1 = half ? NCH : (NCH + 1) / 2;
-    float* xmax = reinterpret_cast<float*>(tmem_slot + 4);  // [2 halves][128]
+    constexpr int NCH = HD / 32;  // 32-column chunks of O, split over the CS parts
+    const int oc0 = part * NCH / CS, oc1 = (part + 1) * NCH / CS;
     float m_used = -INFINITY, l = 0.f;
-    uint8_t* p_row0 = sP + half * Cfg::kTileBytes + r * 128;
     for (int j = 0; j < n_tiles; ++j) {
       const int buf = j & 1;
       WAIT(&s_full[buf], (j >> 1) & 1, 8);
       ptx::tc_fence_after();
       // raw scores (scale_log2 > 0 is applied inside the exponent: max commutes with it)
-      float x[64];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(tmem + lane_base + buf * kBN + half * 64 + c * 32, v);
+      float x[CW];
+      {
+        uint32_t v[CW];
+        if constexpr (CW == 32)
+          ptx::tmem_ld_32x32b_x32(tmem + lane_base + buf * kBN + part * CW, v);
+        else
+          static_assert(CW == 32, "column split must give 32-column parts");
         ptx::tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) x[c * 32 + i] = __uint_as_float(v[i]);
-      }
-      if constexpr (!PT) {
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&s_free[buf]);
+        for (int i = 0; i < CW; ++i) x[i] = __uint_as_float(v[i]);
       }
       if (j == qb) {  // diagonal tile: causal mask (the only tile that needs one)
 #pragma unroll
-        for (int i = 0; i < 64; ++i)
-          if (half * 64 + i > r) x[i] = -INFINITY;
+        for (int i = 0; i < CW; ++i)
+          if (part * CW + i > r) x[i] = -INFINITY;
       }
       float pm[8];  // 8 independent partial maxima (short dependency chains)
 #pragma unroll
       for (int k = 0; k < 8; ++k) pm[k] = fmaxf(x[k], x[k + 8]);
 #pragma unroll
-      for (int i = 16; i < 64; i += 8)
+      for (int i = 16; i < CW; i += 8)
 #pragma unroll
         for (int k = 0; k < 8; ++k) pm[k] = fmaxf(pm[k], x[i + k]);
       float mt = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
       mt *= scale_log2;
-      xmax[half * 128 + r] = mt;
-      named_sync(1 + quarter, 64);
-      mt = fmaxf(mt, xmax[(half ^ 1) * 128 + r]);
-      named_sync(1 + quarter, 64);  // exchange slots are reused next tile
+      xch[part * 128 + r] = mt;
+      named_sync(1 + quarter, 32 * CS);
+#pragma unroll
+      for (int o = 1; o < CS; ++o) mt = fmaxf(mt, xch[((part + o) % CS) * 128 + r]);
+      named_sync(1 + quarter, 32 * CS);  // exchange slots are reused next tile
       // Lazy rescale (only when a row's max grows by > 2^8). tcgen05.ld/st are warp-collective,
-      // so the decision is warp-uniform (and identical in both halves of a row).
+      // so the decision is warp-uniform (and identical in every part of a row).
       if (__any_sync(0xffffffffu, mt > m_used + 8.f)) {
         const float m_new = fmaxf(m_used, mt);
         if (j > 0) {
           // O must hold all of PV_0..PV_{j-1} before it is rescaled
-          WAIT(&pv_done[(j - 1) % PB], ((j - 1) / PB) & 1, 9);
+          WAIT(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1, 9);
           const float f = exp2f(m_used - m_new);
           l *= f;
           ptx::tc_fence_after();
@@ -269,57 +261,36 @@ __global__ void __launch_bounds__(320, 1)
         }
         m_used = m_new;
       }
+      // P = exp2(x - m_used) as bf16 pairs into this part's CW/2 columns of S_j (every part has read
+      // its scores: the max exchange above is a barrier), the A operand of PV_j
       const float neg_m = -m_used;
       float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // independent partial row sums
-      if constexpr (PT) {
-        // P = exp2(x - m_used) as bf16 pairs into this half's 32 columns of S_j (already read by both
-        // halves: the max exchange above is a barrier), the A operand of PV_j
-        uint32_t pk[32];
+      uint32_t pk[CW / 2];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          float p[8];
+      for (int u = 0; u < CW / 8; ++u) {
+        float pv[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            p[e] = ex2(fmaf(x[u * 8 + e], scale_log2, neg_m));
-            ls[e] += p[e];
-          }
-#pragma unroll
-          for (int e = 0; e < 4; ++e) pk[u * 4 + e] = ptx::pack_bf16(p[2 * e], p[2 * e + 1]);
+        for (int e = 0; e < 8; ++e) {
+          pv[e] = ex2(fmaf(x[u * 8 + e], scale_log2, neg_m));
+          ls[e] += pv[e];
         }
-        ptx::tmem_st_32x32b_x32(tmem + lane_base + buf * kBN + half * 32, pk);
-        ptx::tmem_st_wait();
-      } else {
-        // the P buffer of tile j must be free of PV_{j-PB}
-        if (j >= PB) WAIT(&pv_done[j % PB], ((j / PB) - 1) & 1, 10);
-        uint8_t* p_row = p_row0 + (j % PB) * Cfg::kPBytes;
-        // P = exp2(x - m_used) -> bf16 into this half's 64-column swizzle chunk, 16B unit u
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          float p[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            p[e] = ex2(fmaf(x[u * 8 + e], scale_log2, neg_m));
-            ls[e] += p[e];
-          }
-          uint4 pk;
-          pk.x = ptx::pack_bf16(p[0], p[1]);
-          pk.y = ptx::pack_bf16(p[2], p[3]);
-          pk.z = ptx::pack_bf16(p[4], p[5]);
-          pk.w = ptx::pack_bf16(p[6], p[7]);
-          *reinterpret_cast<uint4*>(p_row + ((u ^ (r & 7)) * 16)) = pk;
-        }
-        ptx::fence_proxy_async();
+        for (int e = 0; e < 4; ++e) pk[u * 4 + e] = ptx::pack_bf16(pv[2 * e], pv[2 * e + 1]);
       }
+      ptx::tmem_st_32x32b_x16(tmem + lane_base + buf * kBN + part * (CW / 2), pk);
+      ptx::tmem_st_wait();
       l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&p_full[j % PB]);
+      if (lane == 0) ptx::mbar_arrive(&p_full[buf]);
     }
-    // combine the two halves' row sums
-    xmax[half * 128 + r] = l;
-    named_sync(1 + quarter, 64);
-    const float l_tot = l + xmax[(half ^ 1) * 128 + r];
-    WAIT(&pv_done[(n_tiles - 1) % PB], ((n_tiles - 1) / PB) & 1, 11);
+    // combine the parts' row sums
+    xch[part * 128 + r] = l;
+    named_sync(1 + quarter, 32 * CS);
+    float l_tot = l;
+#pragma unroll
+    for (int o = 1; o < CS; ++o) l_tot += xch[((part + o) % CS) * 128 + r];
+    WAIT(&pv_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1, 11);
     ptx::tc_fence_after();
     const float inv = 1.f / l_tot;
     __nv_bfloat16* orow = out + static_cast<size_t>(row0 + q_row) * dt + h * HD;
@@ -331,15 +302,15 @@ __global__ void __launch_bounds__(320, 1)
       uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        uint4 pk;
-        pk.x = ptx::pack_bf16(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
-        pk.y = ptx::pack_bf16(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
-        pk.z = ptx::pack_bf16(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
-        pk.w = ptx::pack_bf16(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
-        dst[q] = pk;
+        uint4 pkk;
+        pkk.x = ptx::pack_bf16(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
+        pkk.y = ptx::pack_bf16(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
+        pkk.z = ptx::pack_bf16(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
+        pkk.w = ptx::pack_bf16(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
+        dst[q] = pkk;
       }
     }
-    if (half == 0) lse[(static_cast<size_t>(b) * ht + h) * s + q_row] = m_used + log2f(l_tot);
+    if (part == 0) lse[(static_cast<size_t>(b) * ht + h) * s + q_row] = m_used + log2f(l_tot);
   }
   __syncthreads();
   if (warp == 1) {
@@ -948,12 +919,12 @@ int bwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* do
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
-template <int HD, bool PT>
+template <int HD>
 int fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, cudaStream_t st) {
-  using Cfg = TcFwdCfg<HD, PT>;
+  using Cfg = TcFwdCfg<HD>;
   static bool init = false;
   if (!init) {
-    if (cudaFuncSetAttribute(fa_fwd_tc_kernel<HD, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
+    if (cudaFuncSetAttribute(fa_fwd_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
         cudaSuccess)
       return 3;
     init = true;
@@ -963,7 +934,7 @@ int fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, flo
   if (!make_tmap_bf16(&tm, qkv, 3 * static_cast<uint64_t>(dt), static_cast<uint64_t>(a.batch) * a.seq, 3 * dt, 64, 128))
     return 3;
   dim3 grid(a.seq / kBM, a.batch * a.heads);
-  fa_fwd_tc_kernel<HD, PT><<<grid, 320, Cfg::kSmem, st>>>(tm, out, lse, a.seq, a.heads,
+  fa_fwd_tc_kernel<HD><<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(tm, out, lse, a.seq, a.heads,
                                                        kLog2e / sqrtf(static_cast<float>(HD)));
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
@@ -982,11 +953,10 @@ int flash_attn_bwd_tc_main(const AttnShape& a, const __nv_bfloat16* qkv, const _
 
 int flash_attn_fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, cudaStream_t st) {
   if (a.seq % kBM != 0) return 1;
-  static const bool p_smem = std::getenv("GPTB200_ATTN_P_SMEM") != nullptr;  // A/B hook
   switch (a.head_dim) {
-    case 64: return p_smem ? fwd_tc<64, false>(a, qkv, out, lse, st) : fwd_tc<64, true>(a, qkv, out, lse, st);
-    case 128: return p_smem ? fwd_tc<128, false>(a, qkv, out, lse, st) : fwd_tc<128, true>(a, qkv, out, lse, st);
-    case 160: return p_smem ? fwd_tc<160, false>(a, qkv, out, lse, st) : fwd_tc<160, true>(a, qkv, out, lse, st);
+    case 64: return fwd_tc<64>(a, qkv, out, lse, st);
+    case 128: return fwd_tc<128>(a, qkv, out, lse, st);
+    case 160: return fwd_tc<160>(a, qkv, out, lse, st);
     default: return 1;
   }
 }
