@@ -89,7 +89,7 @@ int tp_gemm_bf16(int M, int N, int K, const void* A, int lda, int a_mn, const vo
                  int b_mn, void* C, int ldc, int epi, const void* bias, void* C2, const void* aux,
                  int ldaux, int accumulate, void* stream);
 
-/* Test/tuning hook: 0 = automatic GEMM tile choice, 1 = single-CTA 128xN tiles only,
+/* Test/tuning hook: 0 = automatic GEMM tile choice, 1 = single-CTA 128xN tiles only, 3 = CTA-pair 256x512,
  * 2 = CTA-pair (cta_group::2) 256x256 tiles whenever M, N are multiples of 256. */
 int tp_gemm_force_cta_group(int cg);
 

@@ -38,7 +38,12 @@ struct GemmCfg {
   static constexpr int kBBytes = (BN / CG) * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (kStageBytes <= 32768) ? 6 : 4;
-  static constexpr int kTmemCols = 2 * BN;
+  // BN = 512 (CTA pair 256 x 512): two N = 256 MMAs per k-step share A; the fp32 accumulator then
+  // fills TMEM, so it is single-buffered (the epilogue is not overlapped with the next mainloop).
+  static constexpr int kNsub = BN > 256 ? BN / 256 : 1;
+  static constexpr int kMmaN = BN / kNsub;
+  static constexpr int kAccBufs = 2 * BN <= 512 ? 2 : 1;
+  static constexpr int kTmemCols = kAccBufs * BN;
   static constexpr int kStageOutBytes = 8 * 4096;  // per epilogue warp: one [32 rows][128 B] swizzled box
   static constexpr int kSmemBytes = kStages * kStageBytes + kStageOutBytes + 1024 + 256;
 };
@@ -88,6 +93,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kStages = Cfg::kStages;
   constexpr int kTileM = kBM * CG;   // rows of C per tile (per CTA pair)
   constexpr int kBN_cta = BN / CG;   // rows of B staged by each CTA
+  constexpr int kNsub = Cfg::kNsub, kAccBufs = Cfg::kAccBufs;
+  constexpr int kNsubRows = kBN_cta / kNsub;  // B rows per CTA per N sub-tile
+  constexpr uint32_t kBSubOff = B_MN ? (kNsubRows / 64) * kBK * 128 : kNsubRows * 128;  // smem bytes
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = ptx::smem_align1024(smem_raw);
   uint8_t* stage_out = smem + kStages * Cfg::kStageBytes;  // 1024-aligned (stage sizes are 1 KB multiples)
@@ -150,7 +158,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kb0 = slice_begin(kslice), kblocks = slice_begin(kslice + 1) - kb0;
         int mb, nb;
         tile_coords(tile, num_m, num_n, mb, nb);
-        const int m0 = mb * kTileM + rank * kBM, n0 = nb * BN + rank * kBN_cta;
+        const int m0 = mb * kTileM + rank * kBM;
+        auto n0_of = [&](int ns) { return nb * BN + ns * (BN / kNsub) + rank * kNsubRows; };
         for (int kb = 0; kb < kblocks; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::kStageBytes;
@@ -171,9 +180,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if constexpr (B_MN) {
 #pragma unroll
-            for (int c = 0; c < kBN_cta / 64; ++c) load(sb + c * kBK * 128, &tmB, n0 + 64 * c, k0);
+            for (int c = 0; c < kBN_cta / 64; ++c)
+              load(sb + c * kBK * 128, &tmB, n0_of(c / (kNsubRows / 64)) + 64 * (c % (kNsubRows / 64)), k0);
           } else {
-            load(sb, &tmB, k0, n0);
+#pragma unroll
+            for (int ns = 0; ns < kNsub; ++ns) load(sb + ns * kBSubOff, &tmB, k0, n0_of(ns));
           }
           if (++stage == kStages) {
             stage = 0;
@@ -185,15 +196,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader CTA only)
     if (leader) {  // all 32 lanes: uniform descriptors, one elected lane issues
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kTileM, BN, A_MN, B_MN);
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kTileM, Cfg::kMmaN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
       for (int unit = cluster_id; unit < num_units; unit += num_clusters, ++it) {
         const int kslice = unit / num_tiles;
         const int kblocks = slice_begin(kslice + 1) - slice_begin(kslice);
-        const int acc = it & 1;
-        ptx::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        const int acc = kAccBufs == 2 ? (it & 1) : 0;
+        const int use = kAccBufs == 2 ? (it >> 1) : it;
+        ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < kblocks; ++kb) {
@@ -212,10 +224,15 @@ __global__ void __launch_bounds__(kThreads, 1)
               bdesc = ptx::smem_desc_sw128(sb + k * 2048, kBK * 128, 1024);
             else
               bdesc = ptx::smem_desc_sw128(sb + k * 32, 16, 1024);
-            if constexpr (CG == 2)
-              ptx::mma_bf16_ss_cg2_w(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
-            else
-              ptx::mma_bf16_ss_w(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+#pragma unroll
+            for (int ns = 0; ns < kNsub; ++ns) {
+              if constexpr (CG == 2)
+                ptx::mma_bf16_ss_cg2_w(d_tmem + ns * Cfg::kMmaN, adesc, bdesc + ((ns * kBSubOff) >> 4), idesc,
+                                       (kb | k) != 0 ? 1u : 0u);
+              else
+                ptx::mma_bf16_ss_w(d_tmem + ns * Cfg::kMmaN, adesc, bdesc + ((ns * kBSubOff) >> 4), idesc,
+                                   (kb | k) != 0 ? 1u : 0u);
+            }
           }
           if constexpr (CG == 2)
             ptx::mma_commit_cg2_w(&empty[stage]);
@@ -241,8 +258,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tile = unit % num_tiles;
       int mb, nb;
       tile_coords(tile, num_m, num_n, mb, nb);
-      const int acc = it & 1;
-      ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      const int acc = kAccBufs == 2 ? (it & 1) : 0;
+      ptx::mbar_wait(&tfull[acc], ((kAccBufs == 2 ? (it >> 1) : it)) & 1);
       ptx::tc_fence_after();
       const int row_base = mb * kTileM + rank * kBM + 32 * q;
       const int row = row_base + lane;
@@ -521,7 +538,7 @@ int launch(const GemmParams& p, cudaStream_t stream) {
   bool ok = A_MN ? make_tmap(&ta, p.A, p.M, p.K, p.lda, 64)
                  : make_tmap(&ta, p.A, p.K, p.M, p.lda, kBM);
   ok = ok && (B_MN ? make_tmap(&tb, p.B, p.N, p.K, p.ldb, 64)
-                   : make_tmap(&tb, p.B, p.K, p.N, p.ldb, BN / CG));
+                   : make_tmap(&tb, p.B, p.K, p.N, p.ldb, BN / CG / GemmCfg<BN, CG>::kNsub));
   CUtensorMap tc, tc2;
   if constexpr (EPI == EPI_F32) {
     ok = ok && make_tmap_f32(&tc, p.C, p.N, p.M, p.ldc, 32, 32, true);
@@ -613,6 +630,17 @@ int gemm_bf16(const GemmParams& p, cudaStream_t stream) {
   // >= ~85% of the pairs busy in a single wave beats 1.7 waves of single-CTA tiles
   const bool pair_wave = pair_ok && (p.M / 256) * (p.N / 256) * 8 >= (num_sms() / 2) * 7 - 8;
   GemmParams q = p;
+  // 256 x 512 pair tiles: 25% less L2->SMEM operand traffic per FLOP (measured: 8192^3 sustained
+  // 1281 -> 1325 TF/s under the power cap) but a single-buffered accumulator, so only for long K
+  // when the bigger tiles still fill the waves (the training-step shapes do not qualify).
+  const bool p512_ok = p.M % 256 == 0 && p.N % 512 == 0 && !(p.epi == EPI_F32 && p.accumulate);
+  const int t512 = p512_ok ? (p.M / 256) * (p.N / 512) : 0, slots = num_sms() / 2;
+  const bool p512_auto = p512_ok && p.K >= 8192 && t512 >= slots &&
+                         static_cast<double>(t512) / (((t512 + slots - 1) / slots) * slots) >= 0.97;
+  if ((g_force_cg == 3 && p512_ok) || (g_force_cg == 0 && p512_auto)) {
+    q.split_k = choose_split(p, (p.M / 256) * (p.N / 512), num_sms() / 2);
+    return dispatch_epi<512, 2>(q, stream);
+  }
   if (g_force_cg == 2 ? pair_ok : (g_force_cg == 0 && pair_wave)) {
     q.split_k = choose_split(p, (p.M / 256) * (p.N / 256), num_sms() / 2);
     return dispatch_epi<256, 2>(q, stream);

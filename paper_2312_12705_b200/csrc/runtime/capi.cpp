@@ -50,7 +50,7 @@ int tp_gemm_bf16(int M, int N, int K, const void* A, int lda, int a_mn, const vo
 }
 
 int tp_gemm_force_cta_group(int cg) {
-  if (cg < 0 || cg > 2) return set_error(TP_ERR_INVALID, "tp_gemm_force_cta_group: cg must be 0, 1 or 2");
+  if (cg < 0 || cg > 3) return set_error(TP_ERR_INVALID, "tp_gemm_force_cta_group: cg must be 0..3");
   gemm_force_cta_group(cg);
   return clear_error();
 }

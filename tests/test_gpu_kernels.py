@@ -29,10 +29,10 @@ def _gpu(native_lib):
     yield
 
 
-@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("cg", [1, 2, 3])  # 3: CTA-pair 256 x 512 tiles when M % 256 == 0 and N % 512 == 0
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1)])
 @pytest.mark.parametrize("M,N,K", [(128, 64, 64), (256, 384, 192), (2048, 2304, 768), (1024, 51200 // 8, 256),
-                                   (512, 512, 2048)])
+                                   (512, 512, 2048), (768, 1536, 1024)])
 def test_gemm_layouts_vs_torch(a_mn, b_mn, M, N, K, cg):
     T.check(T.load().tp_gemm_force_cta_group(cg))
     g = torch.Generator(device=DEV).manual_seed(1)
@@ -47,7 +47,7 @@ def test_gemm_layouts_vs_torch(a_mn, b_mn, M, N, K, cg):
     assert _rel(C.float(), ref) < 5e-3  # bf16 output rounding (2^-9) dominates
 
 
-@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("cg", [1, 2, 3])
 def test_gemm_fp32_accumulate_epilogue(cg):
     T.check(T.load().tp_gemm_force_cta_group(cg))
     M, N, K = 256, 512, 1024

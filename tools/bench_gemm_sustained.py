@@ -52,14 +52,20 @@ def run(name, fn, flops, secs=3.0):
           f"TF/s per GHz {tf / (clk / 1e3) if clk else 0:7.1f}  TFLOP/J {tf / pw if pw else 0:.2f}", flush=True)
 
 
+import os  # noqa: E402
+
+
 def main():
     lib = T.load()
+    force = int(os.environ.get("FORCE_CG", "0"))
+    T.check(lib.tp_gemm_force_cta_group(force))
     st = torch.cuda.current_stream().cuda_stream
-    import os
     shapes = [(8192, 8192, 8192, 0, 0, 0), (16384, 8192, 2048, 0, 0, 0), (16384, 8192, 2048, 0, 0, 1),
               (8192, 2048, 16384, 1, 1, 2)]
     if os.environ.get("SHAPES") == "square":
         shapes = shapes[:2]
+    if os.environ.get("SHAPES") == "longk":
+        shapes = [(8192, 8192, 8192, 0, 0, 0), (16384, 2048, 8192, 0, 1, 0), (8192, 2048, 16384, 1, 1, 2)]
     ldaux = int(os.environ.get("LDAUX", "0"))  # experiment hook (no effect in the product build)
     for (M, N, K, a_mn, b_mn, epi) in shapes:
         A = torch.randn((K, M) if a_mn else (M, K), device="cuda").bfloat16()
