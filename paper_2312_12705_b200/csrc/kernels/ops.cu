@@ -780,7 +780,8 @@ int ln_bwd(const LnBwdArgs& a, cudaStream_t st) {
   // fused single HBM pass when the row count alone fills the GPU (>= 2 waves of 32-row slabs);
   // wide-row / few-row shapes keep the row-parallel two-pass form
   const int blocks = (a.rows + kLnFuseRows - 1) / kLnFuseRows;
-  if (blocks >= 2 * device_sms() && std::getenv("GPTB200_LN_BWD_TWO_PASS") == nullptr) {
+  static const bool two_pass_only = std::getenv("GPTB200_LN_BWD_TWO_PASS") != nullptr;  // A/B switch
+  if (blocks >= 2 * device_sms() && !two_pass_only) {
     ln_bwd_fused_kernel<<<blocks, 256, 0, st>>>(a, dr, a.workspace);
     const bool any = (a.dy && (a.dgamma || a.dbeta)) || a.dbias;
     if (any)
