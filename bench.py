@@ -39,8 +39,13 @@ FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_g
 
 WORKLOADS = {
     # name: (L, d, heads, V, s, mbs, tp, pp, ckpt, dropout, microbatches per DP replica)
-    # BASELINE config 2 (headline): 1.4B on 1 GPU, DP = N with ZeRO-1 beyond.
-    "gpt-1.4b": (24, 2048, 16, 51200, 2048, 8, 1, 1, False, 0.1, 1),
+    # BASELINE config 2 (headline): 1.4B on 1 GPU, DP = N with ZeRO-1 beyond. Micro-batch 16 is the
+    # B200 choice from the sweep below (4: 927, 8: 1020, 16: 1062-1075, 32: 1085 TFLOPS/GPU at 138 GB;
+    # 16 keeps half the HBM free) — the reference's own search tunes mbs the same way.
+    "gpt-1.4b": (24, 2048, 16, 51200, 2048, 16, 1, 1, False, 0.1, 1),
+    "gpt-1.4b-mbs4": (24, 2048, 16, 51200, 2048, 4, 1, 1, False, 0.1, 1),
+    "gpt-1.4b-mbs8": (24, 2048, 16, 51200, 2048, 8, 1, 1, False, 0.1, 1),
+    "gpt-1.4b-mbs32": (24, 2048, 16, 51200, 2048, 32, 1, 1, False, 0.1, 1),
     # BASELINE config 1 shape (tiny GPT) — smoke-sized.
     "gpt-tiny": (2, 256, 4, 51200, 128, 1, 1, 1, False, 0.0, 1),
     # BASELINE config 3: 22B shape with TP = 2/4/8 and activation checkpointing, MBS 1, m = 8.
@@ -55,6 +60,8 @@ WORKLOADS = {
     # BASELINE config 5: 1T-shape layer slice (4 layers, 160 heads, hd 160) TP8 / TP4 x PP2.
     "gpt-1t-slice-tp8": (4, 25600, 160, 51200, 2048, 1, 8, 1, True, 0.1, 8),
     "gpt-1t-slice-tp4pp2": (4, 25600, 160, 51200, 2048, 1, 4, 2, True, 0.1, 8),
+    # the same 4-layer 1T slice on 4 GPUs (TP4; ~140 GB/GPU) for single-box measurements
+    "gpt-1t-slice-tp4": (4, 25600, 160, 51200, 2048, 1, 4, 1, True, 0.1, 8),
 }
 
 
