@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(kSpThreads) sp_ln_fwd_kernel(ncclDevComm dev, 
                                                                DropDev dr) {
   __shared__ float red[64];
   ncclCoopCta coop;
-  ncclLsaBarrierSession<ncclCoopCta> bar(coop, dev, ncclTeamTagLsa(), blockIdx.x, /*multimem=*/true);
+  ncclLsaBarrierSession<ncclCoopCta> bar(coop, dev, ncclTeamTagLsa(), a.bar_base + blockIdx.x,
+                                         /*multimem=*/true);
   bar.sync(coop, cuda::memory_order_acq_rel);  // partials complete; every reader of the ln buffer done
   const bf16* ymc = a.y_off >= 0 ? static_cast<const bf16*>(ncclGetLsaMultimemPointer(win, a.y_off, dev)) : nullptr;
   bf16* lnmc = a.ln_off >= 0 ? static_cast<bf16*>(ncclGetLsaMultimemPointer(win, a.ln_off, dev)) : nullptr;
@@ -163,7 +164,8 @@ __global__ void __launch_bounds__(kSpThreads) sp_ln_bwd_kernel(ncclDevComm dev, 
                                                                DropDev dr) {
   __shared__ float red[64];
   ncclCoopCta coop;
-  ncclLsaBarrierSession<ncclCoopCta> bar(coop, dev, ncclTeamTagLsa(), blockIdx.x, /*multimem=*/true);
+  ncclLsaBarrierSession<ncclCoopCta> bar(coop, dev, ncclTeamTagLsa(), a.bar_base + blockIdx.x,
+                                         /*multimem=*/true);
   bar.sync(coop, cuda::memory_order_acq_rel);
   const bf16* dymc = a.dy_off >= 0 ? static_cast<const bf16*>(ncclGetLsaMultimemPointer(win, a.dy_off, dev)) : nullptr;
   bf16* dyloc = a.dy_off >= 0 ? static_cast<bf16*>(ncclGetLocalPointer(win, a.dy_off)) : nullptr;
@@ -259,7 +261,7 @@ NvlsContext* nvls_create(ncclComm_t comm, size_t bytes, int max_ctas) {
   }
   ncclDevCommRequirements reqs{};
   reqs.lsaMultimem = true;
-  reqs.lsaBarrierCount = max_ctas;
+  reqs.lsaBarrierCount = kNvlsBarrierSets * max_ctas;
   if (ncclDevCommCreate(comm, &reqs, &c->dev) != ncclSuccess) {
     ncclCommWindowDeregister(comm, c->win);
     ncclMemFree(c->base);
@@ -291,8 +293,11 @@ namespace {
 int sp_grid(const NvlsContext* c, int nrows) { return nrows < c->max_ctas ? nrows : c->max_ctas; }
 }  // namespace
 
-int sp_ln_fwd(NvlsContext* c, const SpLnFwdArgs& a, cudaStream_t st) {
-  if (!c || a.nrows <= 0 || a.d % 8 != 0 || a.d > 16 * kSpThreads * 8) return 1;
+int sp_ln_fwd(NvlsContext* c, const SpLnFwdArgs& a_in, cudaStream_t st) {
+  if (!c || a_in.nrows <= 0 || a_in.d % 8 != 0 || a_in.d > 16 * kSpThreads * 8) return 1;
+  if (a_in.lane_set < 0 || a_in.lane_set >= kNvlsBarrierSets) return 1;
+  SpLnFwdArgs a = a_in;
+  a.bar_base = a.lane_set * c->max_ctas;
   if (a.drop.p > 0.f && a.drop.elem_base % 8 != 0) return 1;
   if (a.gamma && (a.ln_off < 0 || !a.beta || !a.mean || !a.rstd)) return 1;
   const int vpt = (a.d / 8 + kSpThreads - 1) / kSpThreads;
@@ -308,8 +313,11 @@ int sp_ln_fwd(NvlsContext* c, const SpLnFwdArgs& a, cudaStream_t st) {
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }
 
-int sp_ln_bwd(NvlsContext* c, const SpLnBwdArgs& a, cudaStream_t st) {
-  if (!c || a.nrows <= 0 || a.d % 8 != 0 || a.d > 16 * kSpThreads * 8 || !a.workspace) return 1;
+int sp_ln_bwd(NvlsContext* c, const SpLnBwdArgs& a_in, cudaStream_t st) {
+  if (!c || a_in.nrows <= 0 || a_in.d % 8 != 0 || a_in.d > 16 * kSpThreads * 8 || !a_in.workspace) return 1;
+  if (a_in.lane_set < 0 || a_in.lane_set >= kNvlsBarrierSets) return 1;
+  SpLnBwdArgs a = a_in;
+  a.bar_base = a.lane_set * c->max_ctas;
   if (a.drop.p > 0.f && a.drop.elem_base % 8 != 0) return 1;
   if (a.dy_off >= 0 && (!a.x || !a.gamma || !a.mean || !a.rstd)) return 1;
   const int vpt = (a.d / 8 + kSpThreads - 1) / kSpThreads;

@@ -21,6 +21,9 @@ struct NvlsContext;
 
 // Collective over the TP communicator. Returns nullptr (and leaves NCCL state clean) when the
 // TP group is not one NVLink/multicast domain; the caller then uses ncclAllReduce.
+// The device barriers come in kNvlsBarrierSets sets of max_ctas: kernels that may run concurrently
+// on different streams must use different sets (set 0: allreduce / step stream).
+constexpr int kNvlsBarrierSets = 2;
 NvlsContext* nvls_create(ncclComm_t tp_comm, size_t bytes, int max_ctas);
 void nvls_destroy(NvlsContext* ctx, ncclComm_t tp_comm);
 void* nvls_base(const NvlsContext* ctx);
@@ -44,6 +47,8 @@ int64_t nvls_offset(const NvlsContext* ctx, const void* p);
 // y_off < 0: h = resid (pure LayerNorm of the shard, allgathered).
 struct SpLnFwdArgs {
   int nrows = 0, row0 = 0, d = 0, seq = 1;
+  int lane_set = 0;  // barrier-index set: kernels on different streams use different sets
+  int bar_base = 0;  // (set by sp_ln_fwd: lane_set * max CTAs)
   int64_t y_off = -1;
   const bf16* bias = nullptr;
   const bf16* resid = nullptr;  // shard [nrows, d] or position table
@@ -67,6 +72,8 @@ int sp_ln_fwd(NvlsContext* ctx, const SpLnFwdArgs& a, cudaStream_t st);
 // them over TP once per step).
 struct SpLnBwdArgs {
   int nrows = 0, row0 = 0, d = 0;
+  int lane_set = 0;
+  int bar_base = 0;  // (set by sp_ln_bwd)
   int64_t dy_off = -1;
   const bf16* x = nullptr;  // shard
   const bf16* gamma = nullptr;

@@ -104,6 +104,12 @@ Stage::~Stage() {
       cudaStreamDestroy(send_st_[i]);
       cudaEventDestroy(send_done_ev_[i]);
     }
+  if (rc_st_) {
+    cudaStreamSynchronize(rc_st_);
+    cudaStreamDestroy(rc_st_);
+    cudaEventDestroy(rc_fork_);
+    for (auto& e : rc_done_) cudaEventDestroy(e);
+  }
   if (sp_st_) {
     cudaStreamSynchronize(sp_st_);
     cudaStreamDestroy(sp_st_);
@@ -226,7 +232,12 @@ void Stage::allocate() {
   const bool sp_wanted = cfg_.tp > 1 && M_ % cfg_.tp == 0 && !(std::getenv("GPTB200_TP_SP") &&
                                                                   std::getenv("GPTB200_TP_SP")[0] == '0');
   size_t sym_elems = 2 * Md;  // tmp_md_, dm_
-  if (sp_wanted) sym_elems += Md + (last_ ? Md : 0) + (ckpt_ ? 2 : 2 * static_cast<size_t>(nslots_) * Lc_) * Md;
+  // SP + checkpointing with >= 2 layers per chunk: recompute of layer l-1 runs on its own stream
+  // during layer l's backward, so the scratch activations are double-buffered by layer parity and the
+  // recompute has its own partial-sum buffer (window: a, m2 per scratch set + rc_tmp_).
+  const bool rc_overlap = cfg_.tp > 1 && ckpt_ && Lc_ >= 2;
+  if (sp_wanted)
+    sym_elems += Md + (last_ ? Md : 0) + (ckpt_ ? (rc_overlap ? 5 : 2) : 2 * static_cast<size_t>(nslots_) * Lc_) * Md;
   char* sym = static_cast<char*>(comms_.init_tp_symmetric(sym_elems * 2));
   sp_ = sp_wanted && sym != nullptr;
   Ms_ = sp_ ? M_ / cfg_.tp : M_;
@@ -269,6 +280,14 @@ void Stage::allocate() {
     S.labels = static_cast<int32_t*>(alloc(M * 4));
   }
   if (ckpt_) layer_acts(scratch_);
+  rc_overlap_ = sp_ && rc_overlap;
+  if (rc_overlap_) {
+    layer_acts(scratch2_);
+    rc_tmp_ = full(Md);
+    cudaStreamCreateWithFlags(&rc_st_, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&rc_fork_, cudaEventDisableTiming);
+    for (auto& e : rc_done_) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  }
   for (auto& b : dh_) b = static_cast<bf16*>(alloc(Ms * d * 2));
   dy_ = sp_ ? full(Md) : static_cast<bf16*>(alloc(Md * 2));
   du_ = static_cast<bf16*>(alloc(M * 4 * dt * 2));
@@ -331,7 +350,10 @@ Stage::LayerG Stage::gr(int l) const {
   return {p(LN1G), p(LN1B), p(WQKV), p(BQKV), p(WO), p(BO), p(LN2G), p(LN2B), p(W1), p(B1), p(W2), p(B2)};
 }
 
-LayerActs& Stage::acts_for(int slot, int l) { return ckpt_ ? scratch_ : slots_act_[slot].acts[l % Lc_]; }
+LayerActs& Stage::acts_for(int slot, int l) {
+  if (ckpt_) return (rc_overlap_ && (l & 1)) ? scratch2_ : scratch_;  // parity sets when recompute overlaps
+  return slots_act_[slot].acts[l % Lc_];
+}
 
 void Stage::init_params() {
   cudaMemsetAsync(grads_, 0, P_ * sizeof(float), st_);
@@ -781,10 +803,23 @@ void Stage::backward_op(int mb, int c, int slot, bf16* dh, bool head_late) {
       g.resid_grad = dh;  // received gradient of the chunk output (shard); dh itself is unchanged
     }
     sp_bwd(g);
+    const bool prefetch = ckpt_ && rc_overlap_ && !profile_;
     for (int l = Lc_ - 1; l >= 0; --l) {
       const int li = c * Lc_ + l;
       LayerActs& A = acts_for(slot, li);
-      if (ckpt_) layer_recompute(li, A, S.h[l]);
+      if (ckpt_) {
+        if (prefetch && l < Lc_ - 1)
+          cudaStreamWaitEvent(st_, rc_done_[li & 1], 0);  // recompute(li) ran on rc_st_ meanwhile
+        else
+          layer_recompute(li, A, S.h[l]);
+      }
+      if (prefetch && l >= 1) {  // recompute(li - 1) on rc_st_ while layer li's backward runs here
+        cudaEventRecord(rc_fork_, st_);  // its scratch set was last read by layer li + 1 (issued above)
+        cudaStreamWaitEvent(rc_st_, rc_fork_, 0);
+        RecomputeOnSide side(this);
+        layer_recompute(li - 1, acts_for(slot, li - 1), S.h[l - 1]);
+        cudaEventRecord(rc_done_[(li - 1) & 1], rc_st_);
+      }
       layer_bwd(li, A, S.h[l], dh, dy_);
       if (in_last_bwd_) grads_ready(layer_bucket_[li]);
     }
@@ -837,9 +872,25 @@ int64_t Stage::woff(const void* p) const {
   return o;
 }
 
-void Stage::sp_fwd(const SpLnFwdArgs& a) {
+// Issue the enclosed recompute on rc_st_: launches go to that stream, its row-parallel partials to
+// rc_tmp_, and its SP kernels use NVLS barrier set 1 (they may run concurrently with set-0 kernels).
+Stage::RecomputeOnSide::RecomputeOnSide(Stage* st) : s(st), st(st->st_), tmp(st->tmp_md_) {
+  s->st_ = s->rc_st_;
+  s->tmp_md_ = s->rc_tmp_;
+  s->sp_lane_set_ = 1;
+}
+
+Stage::RecomputeOnSide::~RecomputeOnSide() {
+  s->st_ = st;
+  s->tmp_md_ = tmp;
+  s->sp_lane_set_ = 0;
+}
+
+void Stage::sp_fwd(const SpLnFwdArgs& a_in) {
   ++launches_;
-  KScope prof(this, K_COMM_TP, 0, (a.y_off >= 0 ? 2.0 : 0.0) * M_ * d_ + 6.0 * Ms_ * d_);
+  KScope prof(this, K_COMM_TP, 0, (a_in.y_off >= 0 ? 2.0 : 0.0) * M_ * d_ + 6.0 * Ms_ * d_);
+  SpLnFwdArgs a = a_in;
+  a.lane_set = sp_lane_set_;
   const int r = sp_ln_fwd(comms_.tp_nvls, a, st_);
   if (r != 0) throw StepError{r == 1 ? TP_ERR_INVALID : TP_ERR_CUDA, "sequence-parallel LN forward failed"};
 }

@@ -174,6 +174,21 @@ class Stage {
   void sp_bwd_overlapped(const SpLnBwdArgs& a, F&& independent);
   cudaStream_t sp_st_ = nullptr;
   cudaEvent_t sp_fork_ = nullptr, sp_join_ = nullptr;
+  // recompute prefetch (SP + checkpointing): see backward_op / RecomputeOnSide
+  bool rc_overlap_ = false;
+  LayerActs scratch2_;
+  bf16* rc_tmp_ = nullptr;
+  cudaStream_t rc_st_ = nullptr;
+  cudaEvent_t rc_fork_ = nullptr, rc_done_[2] = {nullptr, nullptr};
+  int sp_lane_set_ = 0;
+  struct RecomputeOnSide {
+    Stage* s;
+    cudaStream_t st;
+    bf16* tmp;
+    explicit RecomputeOnSide(Stage* st);
+    ~RecomputeOnSide();
+  };
+  friend struct RecomputeOnSide;
   int64_t slot_offset(int tid) const { return slot(tid)->offset; }
 
   trainplan::ModelSpec model_;

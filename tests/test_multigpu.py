@@ -151,6 +151,11 @@ def test_tp2_pp2():
     run_layout(tp=2, pp=2, dp=1, gbs=4)
 
 
+def test_tp2_ckpt_four_layers_dropout():
+    # sequence parallel + checkpointing: recompute of layer l-1 overlaps the backward of layer l
+    run_layout(tp=2, pp=1, dp=1, L=4, gbs=2, ckpt=1, dropout=0.1, want_tp_mode=3)
+
+
 def test_tp2_dp2_ckpt():
     run_layout(tp=2, pp=1, dp=2, ckpt=1)
 

@@ -64,6 +64,9 @@ def main():
               (8192, 2048, 16384, 1, 1, 2)]
     if os.environ.get("SHAPES") == "square":
         shapes = shapes[:2]
+    if os.environ.get("SHAPES") == "mbs16":  # 1.4B step shapes at M = 32768 tokens
+        shapes = [(32768, 6144, 2048, 0, 0, 0), (32768, 8192, 2048, 0, 0, 1), (32768, 2048, 2048, 0, 1, 0),
+                  (32768, 2048, 8192, 0, 1, 0), (32768, 8192, 2048, 0, 1, 3)]
     if os.environ.get("SHAPES") == "longk":
         shapes = [(8192, 8192, 8192, 0, 0, 0), (16384, 2048, 8192, 0, 1, 0), (8192, 2048, 16384, 1, 1, 2)]
     ldaux = int(os.environ.get("LDAUX", "0"))  # experiment hook (no effect in the product build)
