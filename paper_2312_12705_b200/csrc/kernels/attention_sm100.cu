@@ -634,9 +634,10 @@ __global__ void __launch_bounds__(512, 1)
   uint64_t* s_full = qdo_empty + QST;       // [2]
   uint64_t* pds_full = s_full + 2;          // [2]
   uint64_t* pds_free = pds_full + 2;        // [2]
-  uint64_t* dq_full = pds_free + 2;         // [2]
-  uint64_t* dq_free = dq_full + 2;          // [2]
-  uint64_t* kdv_full = dq_free + 2;
+  uint64_t* st_free = pds_free + 2;         // [2]  S^T_j / dP^T_j read out by the compute warps
+  uint64_t* dq_full = st_free + 2;          // dQ^T in its own TMEM columns
+  uint64_t* dq_free = dq_full + 1;
+  uint64_t* kdv_full = dq_free + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kdv_full + 1);
 
   // warp index via shfl: provably warp-uniform, so role branches are not treated as divergent
@@ -662,9 +663,10 @@ __global__ void __launch_bounds__(512, 1)
       ptx::mbar_init(&s_full[i], 1);
       ptx::mbar_init(&pds_full[i], 8);
       ptx::mbar_init(&pds_free[i], 1);
-      ptx::mbar_init(&dq_full[i], 1);
-      ptx::mbar_init(&dq_free[i], 4);
+      ptx::mbar_init(&st_free[i], 8);
     }
+    ptx::mbar_init(dq_full, 1);
+    ptx::mbar_init(dq_free, 4);
     ptx::mbar_init(kdv_full, 1);
     ptx::fence_mbar_init();
   }
@@ -673,7 +675,8 @@ __global__ void __launch_bounds__(512, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
-  const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 256 + HD;  // tS/tdP: [2][64]
+  // TMEM: S^T [2][64] | dP^T [64] (released as soon as it is loaded) | dQ^T [64] | dV | dK
+  const uint32_t tS = tmem, tdP = tmem + 128, tDQ = tmem + 192, tdV = tmem + 256, tdK = tmem + 256 + HD;
   const int wg = warp / 4;
   if (wg == 0) ptx::setmaxnreg_dec<64>();
 
@@ -726,18 +729,22 @@ __global__ void __launch_bounds__(512, 1)
           ptx::mma_bf16_ss_w(tdK, ptx::smem_desc_sw128(adS + kk * 32, 16, 1024),
                            ptx::smem_desc_sw128(aQ + kk * 2048, 8192, 1024), id_acc, acc);
         }
+        if (i > 0) WAIT(dq_free, (i - 1) & 1, 44);  // dQ^T_{i-1} read out of its TMEM columns
+        ptx::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // K = 128 kv rows
-          ptx::mma_bf16_ss_w(tS + bb * 64, ptx::smem_desc_sw128(aK + kk * 2048, TB, 1024),
-                           ptx::smem_desc_sw128(adS + kk * 2048, TB, 1024), id_dq, kk > 0 ? 1u : 0u);
-        ptx::mma_commit_w(&dq_full[bb]);
+          ptx::mma_bf16_ss_w(tDQ, ptx::smem_desc_sw128(aK + kk * 2048, TB, 1024),
+                             ptx::smem_desc_sw128(adS + kk * 2048, TB, 1024), id_dq, kk > 0 ? 1u : 0u);
+        ptx::mma_commit_w(dq_full);
         ptx::mma_commit_w(&qdo_empty[sq]);
         ptx::mma_commit_w(&pds_free[bb]);
       };
       for (int j = 0; j < n_it; ++j) {
         const int bb = j & 1, sq = j % QST;
         WAIT(&qdo_full[sq], (j / QST) & 1, 43);
-        if (j >= 2) WAIT(&dq_free[bb], ((j >> 1) - 1) & 1, 44);  // dQ^T_{j-2} read out of tS[bb]
+        // S^T_{j-1} and dP^T_{j-1} loaded by the compute warps: dP^T is free, and so is S^T[bb]
+        // (its previous tile j-2 was loaded before j-1)
+        if (j >= 1) WAIT(&st_free[(j - 1) & 1], ((j - 1) >> 1) & 1, 50);
         ptx::tc_fence_after();
         const uint32_t aQ = aQ0 + sq * Cfg::kQBytes, adO = adO0 + sq * Cfg::kQBytes;
 #pragma unroll
@@ -745,7 +752,7 @@ __global__ void __launch_bounds__(512, 1)
           const uint32_t ak = (kk / 4) * TB + (kk % 4) * 32, aq = (kk / 4) * 8192 + (kk % 4) * 32;
           ptx::mma_bf16_ss_w(tS + bb * 64, ptx::smem_desc_sw128(aK + ak, 16, 1024),
                            ptx::smem_desc_sw128(aQ + aq, 16, 1024), id_s, kk > 0 ? 1u : 0u);
-          ptx::mma_bf16_ss_w(tdP + bb * 64, ptx::smem_desc_sw128(aV + ak, 16, 1024),
+          ptx::mma_bf16_ss_w(tdP, ptx::smem_desc_sw128(aV + ak, 16, 1024),
                            ptx::smem_desc_sw128(adO + aq, 16, 1024), id_s, kk > 0 ? 1u : 0u);
         }
         ptx::mma_commit_w(&s_full[bb]);
@@ -764,17 +771,17 @@ __global__ void __launch_bounds__(512, 1)
       const int bb = i & 1;
       const int q0 = (qt_first + i) * 64;
       float* dst = dq_acc + static_cast<size_t>(row0 + q0) * dt + h * HD + quarter * 32 + lane;
-      WAIT(&dq_full[bb], (i >> 1) & 1, 45);
+      WAIT(dq_full, i & 1, 45);
       ptx::tc_fence_after();
 #pragma unroll
       for (int hq = 0; hq < 2; ++hq) {
         uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(tS + lb + bb * 64 + hq * 32, v);
+        ptx::tmem_ld_32x32b_x32(tDQ + lb + hq * 32, v);
         ptx::tmem_ld_wait();
         if (hq == 1) {
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&dq_free[bb]);
+          if (lane == 0) ptx::mbar_arrive(dq_free);
         }
 #pragma unroll
         for (int e = 0; e < 32; ++e) atomicAdd(dst + static_cast<size_t>(hq * 32 + e) * dt, __uint_as_float(v[e]));
@@ -795,8 +802,11 @@ __global__ void __launch_bounds__(512, 1)
       const int qc = half * 32;
       uint32_t sv[32], dv[32];
       ptx::tmem_ld_32x32b_x32(tS + lb + bb * 64 + qc, sv);
-      ptx::tmem_ld_32x32b_x32(tdP + lb + bb * 64 + qc, dv);
+      ptx::tmem_ld_32x32b_x32(tdP + lb + qc, dv);
       ptx::tmem_ld_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&st_free[bb]);  // S^T / dP^T of this tile consumed
       const float4* L4 = reinterpret_cast<const float4*>(sL + sq * 64 + qc);
       const float4* D4 = reinterpret_cast<const float4*>(sD + sq * 64 + qc);
       uint32_t pk[16], dk[16];
