@@ -470,16 +470,21 @@ __global__ void __launch_bounds__(256) ln_bwd_cols_kernel(LnBwdArgs a, const bf1
   *reinterpret_cast<float4*>(w + 2 * d + c0 + 4) = make_float4(sb[4], sb[5], sb[6], sb[7]);
 }
 
-// out_k[c] += sum_b ws[b*stride + k*n + c] for k = 0..2 (outputs may be null). Block (32, 8):
-// 32 consecutive columns x 8 partial-row lanes, fixed summation order (deterministic).
-__global__ void reduce_partials_kernel(const float* __restrict__ ws, int nblocks, int stride, int n,
-                                       float* out0, float* out1, float* out2) {
-  __shared__ float red[3][8][33];
+// out_k[c] += sum_b ws[b*stride + k*n + c] for k = 0..2 (outputs may be null). Block (32, 32):
+// 32 consecutive columns x 32 partial-row lanes (lane ty sums rows ty, ty+32, ...), then a fixed
+// tree over the 32 lanes: deterministic, and 1024 threads per 32 columns keep enough loads in
+// flight for the ~1000-row partial matrices of the big-M steps.
+constexpr int kRedLanes = 32;
+__global__ void __launch_bounds__(32 * kRedLanes) reduce_partials_kernel(const float* __restrict__ ws, int nblocks,
+                                                                          int stride, int n, float* out0, float* out1,
+                                                                          float* out2) {
+  __shared__ float red[3][kRedLanes][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + tx;
   float s0 = 0.f, s1 = 0.f, s2 = 0.f;
   if (c < n) {
-    for (int b = ty; b < nblocks; b += 8) {
+#pragma unroll 4
+    for (int b = ty; b < nblocks; b += kRedLanes) {
       const float* w = ws + static_cast<size_t>(b) * stride;
       s0 += w[c];
       if (out1) s1 += w[n + c];
@@ -490,17 +495,18 @@ __global__ void reduce_partials_kernel(const float* __restrict__ ws, int nblocks
   red[1][ty][tx] = s1;
   red[2][ty][tx] = s2;
   __syncthreads();
-  if (ty == 0 && c < n) {
-    float t0 = 0.f, t1 = 0.f, t2 = 0.f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      t0 += red[0][k][tx];
-      t1 += red[1][k][tx];
-      t2 += red[2][k][tx];
+  for (int off = kRedLanes / 2; off > 0; off >>= 1) {  // fixed pairwise tree over the lanes
+    if (ty < off) {
+      red[0][ty][tx] += red[0][ty + off][tx];
+      red[1][ty][tx] += red[1][ty + off][tx];
+      red[2][ty][tx] += red[2][ty + off][tx];
     }
-    if (out0) out0[c] += t0;
-    if (out1) out1[c] += t1;
-    if (out2) out2[c] += t2;
+    __syncthreads();
+  }
+  if (ty == 0 && c < n) {
+    if (out0) out0[c] += red[0][0][tx];
+    if (out1) out1[c] += red[1][0][tx];
+    if (out2) out2[c] += red[2][0][tx];
   }
 }
 
@@ -785,7 +791,7 @@ int ln_bwd(const LnBwdArgs& a, cudaStream_t st) {
     ln_bwd_fused_kernel<<<blocks, 256, 0, st>>>(a, dr, a.workspace);
     const bool any = (a.dy && (a.dgamma || a.dbeta)) || a.dbias;
     if (any)
-      reduce_partials_kernel<<<(a.d + 31) / 32, 256, 0, st>>>(a.workspace, blocks, 3 * a.d, a.d,
+      reduce_partials_kernel<<<(a.d + 31) / 32, 32 * kRedLanes, 0, st>>>(a.workspace, blocks, 3 * a.d, a.d,
                                                                 a.dy ? a.dgamma : nullptr, a.dy ? a.dbeta : nullptr,
                                                                 a.dbias);
     return status();
@@ -828,7 +834,7 @@ int ln_bwd_cols(const LnBwdArgs& a, const bf16* dbias_src, cudaStream_t st) {
   const int chunks = (a.rows + kLnColRows - 1) / kLnColRows;
   dim3 grid((a.d / 8 + 255) / 256, chunks);
   ln_bwd_cols_kernel<<<grid, 256, 0, st>>>(a, a.dbias ? dbias_src : nullptr, a.workspace);
-  reduce_partials_kernel<<<(a.d + 31) / 32, 256, 0, st>>>(a.workspace, chunks, 3 * a.d, a.d,
+  reduce_partials_kernel<<<(a.d + 31) / 32, 32 * kRedLanes, 0, st>>>(a.workspace, chunks, 3 * a.d, a.d,
                                                             a.dy ? a.dgamma : nullptr, a.dy ? a.dbeta : nullptr,
                                                             a.dbias ? a.dbias : nullptr);
   return status();
@@ -836,7 +842,7 @@ int ln_bwd_cols(const LnBwdArgs& a, const bf16* dbias_src, cudaStream_t st) {
 
 int reduce_col_partials(const float* partial, int nblocks, int n, float* out, cudaStream_t st) {
   if (nblocks <= 0 || n <= 0) return 1;
-  reduce_partials_kernel<<<(n + 31) / 32, 256, 0, st>>>(partial, nblocks, n, n, out, nullptr, nullptr);
+  reduce_partials_kernel<<<(n + 31) / 32, 32 * kRedLanes, 0, st>>>(partial, nblocks, n, n, out, nullptr, nullptr);
   return status();
 }
 
@@ -849,7 +855,7 @@ int colsum_bf16(const bf16* X, int rows, int n, float* out, float* ws, cudaStrea
   const int splits = (rows + kColsumRows - 1) / kColsumRows;
   dim3 grid((n / 2 + 255) / 256, splits);
   colsum_kernel<<<grid, 256, 0, st>>>(X, rows, n, ws);
-  reduce_partials_kernel<<<(n + 31) / 32, 256, 0, st>>>(ws, splits, n, n, out, nullptr, nullptr);
+  reduce_partials_kernel<<<(n + 31) / 32, 32 * kRedLanes, 0, st>>>(ws, splits, n, n, out, nullptr, nullptr);
   return status();
 }
 
