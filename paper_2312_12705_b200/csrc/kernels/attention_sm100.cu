@@ -319,6 +319,284 @@ __global__ void __launch_bounds__(TcFwdCfg<HD>::kThreads, 1)
   }
 }
 
+// Persistent variant (hd <= 128): one CTA per SM walks (q block, sequence-head) work items in
+// heaviest-first order; the barrier rings run on a per-CTA global tile counter across items, the
+// next item's Q loads as soon as the last S of the current one is issued, and the O accumulator
+// alternates between two TMEM buffers so one item's epilogue overlaps the next item's MMAs.
+// TMEM: S0 | S1 | O0 | O1.
+template <int HD>
+__global__ void __launch_bounds__(TcFwdCfg<HD>::kThreads, 1)
+    fa_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_qkv, __nv_bfloat16* __restrict__ out,
+                         float* __restrict__ lse, int s, int ht, int batch, float scale_log2) {
+  using Cfg = TcFwdCfg<HD>;
+  static_assert(2 * kBN + 2 * HD <= 512, "two O accumulators must fit in TMEM");
+  constexpr int NC = Cfg::NC, ST = Cfg::kStages, CS = Cfg::CS;
+  constexpr int CW = kBN / CS;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if ((ptx::smem_u32(smem_raw) & 1023u) != 0) __trap();
+  uint8_t* sQ = smem_raw;
+  uint8_t* sK = sQ + Cfg::kQBytes;
+  uint8_t* sV = sK + ST * Cfg::kKVBytes;
+  float* xch = reinterpret_cast<float*>(sV + ST * Cfg::kKVBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xch + CS * 128);
+  uint64_t* q_full = bars;
+  uint64_t* q_empty = bars + 1;       // all S MMAs of the item issued and complete
+  uint64_t* k_full = bars + 2;        // [ST]
+  uint64_t* k_empty = k_full + ST;    // [ST]
+  uint64_t* v_full = k_empty + ST;    // [ST]
+  uint64_t* v_empty = v_full + ST;    // [ST]
+  uint64_t* s_full = v_empty + ST;    // [2]
+  uint64_t* s_free = s_full + 2;      // [2]
+  uint64_t* p_full = s_free + 2;      // [2]
+  uint64_t* pv_done = p_full + 2;     // [2]
+  uint64_t* o_free = pv_done + 2;     // [2] O buffer drained by the epilogue
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
+
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
+  const int dt = ht * HD;
+  const int n_qb = s / kBM, BH = batch * ht;
+  const int n_items = n_qb * BH;
+  // items sorted heaviest first; round t hands them out forwards or backwards ("snake") so every
+  // CTA gets a balanced mix of long and short causal blocks
+  auto snake = [&](int t) {
+    const int G = gridDim.x, c = blockIdx.x;
+    return t * G + ((t & 1) ? G - 1 - c : c);
+  };
+  auto item = [&](int k, int& qb, int& b, int& h) {  // heaviest q blocks first
+    qb = n_qb - 1 - k / BH;
+    const int bh = k % BH;
+    b = bh / ht;
+    h = bh % ht;
+  };
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tm_qkv);
+    ptx::mbar_init(q_full, 1);
+    ptx::mbar_init(q_empty, 1);
+    for (int i = 0; i < ST; ++i) {
+      ptx::mbar_init(&k_full[i], 1);
+      ptx::mbar_init(&k_empty[i], 1);
+      ptx::mbar_init(&v_full[i], 1);
+      ptx::mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&s_full[i], 1);
+      ptx::mbar_init(&s_free[i], 1);
+      ptx::mbar_init(&p_full[i], 4 * CS);
+      ptx::mbar_init(&pv_done[i], 1);
+      ptx::mbar_init(&o_free[i], 4 * CS);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int gt = 0, t = 0;
+      for (int k = snake(0); k < n_items; k = snake(t + 1), ++t) {
+        int qb, b, h;
+        item(k, qb, b, h);
+        const int row0 = b * s;
+        WAIT(q_empty, (t & 1) ^ 1, 12);
+        ptx::mbar_arrive_expect_tx(q_full, Cfg::kQBytes);
+        for (int c = 0; c < NC; ++c)
+          ptx::tma_load_2d(sQ + c * Cfg::kTileBytes, &tm_qkv, q_full, h * HD + 64 * c, row0 + qb * kBM);
+        for (int j = 0; j <= qb; ++j, ++gt) {
+          const int st = gt % ST, use = gt / ST;
+          WAIT(&k_empty[st], (use & 1) ^ 1, 1);
+          ptx::mbar_arrive_expect_tx(&k_full[st], Cfg::kKVBytes);
+          for (int c = 0; c < NC; ++c)
+            ptx::tma_load_2d(sK + st * Cfg::kKVBytes + c * Cfg::kTileBytes, &tm_qkv, &k_full[st],
+                             dt + h * HD + 64 * c, row0 + j * kBN);
+          WAIT(&v_empty[st], (use & 1) ^ 1, 2);
+          ptx::mbar_arrive_expect_tx(&v_full[st], Cfg::kKVBytes);
+          for (int c = 0; c < NC; ++c)
+            ptx::tma_load_2d(sV + st * Cfg::kKVBytes + c * Cfg::kTileBytes, &tm_qkv, &v_full[st],
+                             2 * dt + h * HD + 64 * c, row0 + j * kBN);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBM, kBN, false, false);
+    constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(kBM, HD, false, true);
+    const uint32_t q_addr = ptx::smem_u32(sQ);
+    int gt = 0, t = 0;
+    for (int k = snake(0); k < n_items; k = snake(t + 1), ++t) {
+      int qb, b, h;
+      item(k, qb, b, h);
+      const int n_tiles = qb + 1;
+      const int ob = t & 1;
+      const uint32_t tO = tmem + 2 * kBN + ob * HD;
+      WAIT(q_full, t & 1, 3);
+      auto issue_pv = [&](int g, bool first) {
+        const int st = g % ST, pb = g & 1;
+        if (first && t >= 2) WAIT(&o_free[ob], ((t >> 1) - 1) & 1, 13);  // O_ob drained (item t-2)
+        WAIT(&p_full[pb], (g >> 1) & 1, 4);
+        WAIT(&v_full[st], (g / ST) & 1, 5);
+        ptx::tc_fence_after();
+        const uint32_t v_addr = ptx::smem_u32(sV + st * Cfg::kKVBytes);
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          const uint64_t bd = ptx::smem_desc_sw128(v_addr + kk * 2048, Cfg::kTileBytes, 1024);
+          ptx::mma_bf16_ts_w(tO, tmem + pb * kBN + kk * 8, bd, idesc_o, (!first || kk > 0) ? 1u : 0u);
+        }
+        ptx::mma_commit_w(&pv_done[pb]);
+        ptx::mma_commit_w(&v_empty[st]);
+        ptx::mma_commit_w(&s_free[pb]);
+      };
+      for (int j = 0; j < n_tiles; ++j) {
+        const int g = gt + j, st = g % ST, buf = g & 1;
+        WAIT(&k_full[st], (g / ST) & 1, 6);
+        WAIT(&s_free[buf], ((g >> 1) & 1) ^ 1, 7);
+        ptx::tc_fence_after();
+        const uint32_t k_addr = ptx::smem_u32(sK + st * Cfg::kKVBytes);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk / 4) * Cfg::kTileBytes + (kk % 4) * 32;
+          ptx::mma_bf16_ss_w(tmem + buf * kBN, ptx::smem_desc_sw128(q_addr + off, 16, 1024),
+                             ptx::smem_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+        }
+        ptx::mma_commit_w(&s_full[buf]);
+        ptx::mma_commit_w(&k_empty[st]);
+        if (j == n_tiles - 1) ptx::mma_commit_w(q_empty);  // Q free for the next item
+        if (j > 0) issue_pv(g - 1, j == 1);
+      }
+      issue_pv(gt + n_tiles - 1, n_tiles == 1);
+      gt += n_tiles;
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int part = (warp - 2) >> 2;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+    constexpr int NCH = HD / 32;
+    const int oc0 = part * NCH / CS, oc1 = (part + 1) * NCH / CS;
+    int gt = 0, t = 0;
+    for (int k = snake(0); k < n_items; k = snake(t + 1), ++t) {
+      int qb, b, h;
+      item(k, qb, b, h);
+      const int n_tiles = qb + 1;
+      const uint32_t tO = tmem + 2 * kBN + (t & 1) * HD;
+      const int q_row = qb * kBM + r;
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < n_tiles; ++j) {
+        const int g = gt + j, buf = g & 1;
+        WAIT(&s_full[buf], (g >> 1) & 1, 8);
+        ptx::tc_fence_after();
+        float x[CW];
+        {
+          uint32_t v[CW];
+          ptx::tmem_ld_32x32b_x32(tmem + lane_base + buf * kBN + part * CW, v);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < CW; ++i) x[i] = __uint_as_float(v[i]);
+        }
+        if (j == qb) {
+#pragma unroll
+          for (int i = 0; i < CW; ++i)
+            if (part * CW + i > r) x[i] = -INFINITY;
+        }
+        float pm[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) pm[q] = fmaxf(x[q], x[q + 8]);
+#pragma unroll
+        for (int i = 16; i < CW; i += 8)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) pm[q] = fmaxf(pm[q], x[i + q]);
+        float mt = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+        mt *= scale_log2;
+        xch[part * 128 + r] = mt;
+        named_sync(1 + quarter, 32 * CS);
+#pragma unroll
+        for (int o = 1; o < CS; ++o) mt = fmaxf(mt, xch[((part + o) % CS) * 128 + r]);
+        named_sync(1 + quarter, 32 * CS);
+        if (__any_sync(0xffffffffu, mt > m_used + 8.f)) {
+          const float m_new = fmaxf(m_used, mt);
+          if (j > 0) {
+            WAIT(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1, 9);
+            const float f = exp2f(m_used - m_new);
+            l *= f;
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int c = oc0; c < oc1; ++c) {
+              uint32_t v[32];
+              ptx::tmem_ld_32x32b_x32(tO + lane_base + c * 32, v);
+              ptx::tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * f);
+              ptx::tmem_st_32x32b_x32(tO + lane_base + c * 32, v);
+            }
+            ptx::tmem_st_wait();
+          }
+          m_used = m_new;
+        }
+        const float neg_m = -m_used;
+        float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[CW / 2];
+#pragma unroll
+        for (int u = 0; u < CW / 8; ++u) {
+          float pv[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            pv[e] = ex2(fmaf(x[u * 8 + e], scale_log2, neg_m));
+            ls[e] += pv[e];
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) pk[u * 4 + e] = ptx::pack_bf16(pv[2 * e], pv[2 * e + 1]);
+        }
+        ptx::tmem_st_32x32b_x16(tmem + lane_base + buf * kBN + part * (CW / 2), pk);
+        ptx::tmem_st_wait();
+        l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&p_full[buf]);
+      }
+      // epilogue of this item: combine row sums, O / l -> bf16, lse; then release O for item t+2
+      xch[part * 128 + r] = l;
+      named_sync(1 + quarter, 32 * CS);
+      float l_tot = l;
+#pragma unroll
+      for (int o = 1; o < CS; ++o) l_tot += xch[((part + o) % CS) * 128 + r];
+      named_sync(1 + quarter, 32 * CS);  // exchange slots are reused by the next item
+      const int g_last = gt + n_tiles - 1;
+      WAIT(&pv_done[g_last & 1], (g_last >> 1) & 1, 11);
+      ptx::tc_fence_after();
+      const float inv = 1.f / l_tot;
+      __nv_bfloat16* orow = out + static_cast<size_t>(b * s + q_row) * dt + h * HD;
+#pragma unroll 1
+      for (int c = oc0; c < oc1; ++c) {
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(tO + lane_base + c * 32, v);
+        ptx::tmem_ld_wait();
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 pkk;
+          pkk.x = ptx::pack_bf16(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
+          pkk.y = ptx::pack_bf16(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
+          pkk.z = ptx::pack_bf16(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
+          pkk.w = ptx::pack_bf16(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
+          dst[q] = pkk;
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&o_free[t & 1]);
+      if (part == 0) lse[(static_cast<size_t>(b) * ht + h) * s + q_row] = m_used + log2f(l_tot);
+      gt += n_tiles;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
 // ----------------------------------------------------------------------------- backward
 // K6 on tcgen05. CTA = one (sequence, head, 128-row KV block); loops over the 128-row query tiles
 // at and after the diagonal. Per tile:  S^T = K Q^T and dP^T = V dO^T (TMEM), one thread per KV
@@ -930,6 +1208,27 @@ int bwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* do
 }
 
 template <int HD>
+int fwd_tc_persistent(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, cudaStream_t st) {
+  using Cfg = TcFwdCfg<HD>;
+  static bool init = false;
+  if (!init) {
+    if (cudaFuncSetAttribute(fa_fwd_tc_persistent<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
+        cudaSuccess)
+      return 3;
+    init = true;
+  }
+  const int dt = a.heads * HD;
+  CUtensorMap tm;
+  if (!make_tmap_bf16(&tm, qkv, 3 * static_cast<uint64_t>(dt), static_cast<uint64_t>(a.batch) * a.seq, 3 * dt, 64, 128))
+    return 3;
+  const int items = (a.seq / kBM) * a.batch * a.heads;
+  const int grid = items < device_sm_count() ? items : device_sm_count();
+  fa_fwd_tc_persistent<HD><<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(tm, out, lse, a.seq, a.heads, a.batch,
+                                                                    kLog2e / sqrtf(static_cast<float>(HD)));
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+template <int HD>
 int fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, cudaStream_t st) {
   using Cfg = TcFwdCfg<HD>;
   static bool init = false;
@@ -963,9 +1262,10 @@ int flash_attn_bwd_tc_main(const AttnShape& a, const __nv_bfloat16* qkv, const _
 
 int flash_attn_fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, cudaStream_t st) {
   if (a.seq % kBM != 0) return 1;
+  static const bool per_block = std::getenv("GPTB200_ATTN_FWD_PER_BLOCK") != nullptr;  // A/B switch
   switch (a.head_dim) {
-    case 64: return fwd_tc<64>(a, qkv, out, lse, st);
-    case 128: return fwd_tc<128>(a, qkv, out, lse, st);
+    case 64: return per_block ? fwd_tc<64>(a, qkv, out, lse, st) : fwd_tc_persistent<64>(a, qkv, out, lse, st);
+    case 128: return per_block ? fwd_tc<128>(a, qkv, out, lse, st) : fwd_tc_persistent<128>(a, qkv, out, lse, st);
     case 160: return fwd_tc<160>(a, qkv, out, lse, st);
     default: return 1;
   }
