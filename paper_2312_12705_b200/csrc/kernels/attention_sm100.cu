@@ -1161,6 +1161,321 @@ __global__ void __launch_bounds__(512, 1)
 }
 
 template <int HD>
+__global__ void __launch_bounds__(512, 1)
+    fa_bwd_tc2_persistent(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
+                      const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse,
+                      const float* __restrict__ Dg, float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv,
+                      int s, int ht, int batch, float scale_log2, float scale) {
+  using Cfg = TcBwd2Cfg<HD>;
+  constexpr int NC = Cfg::NC, TB = Cfg::kTileBytes;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = ptx::smem_align1024(smem_raw);
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + Cfg::kKVBytes;
+  constexpr int QST = Cfg::QST;
+  uint8_t* sQ = sV + Cfg::kKVBytes;          // [QST][NC][64][64]
+  uint8_t* sdO = sQ + QST * Cfg::kQBytes;    // [QST][NC][64][64]
+  uint8_t* sPT = sdO + QST * Cfg::kQBytes;   // [2][128 kv][64 q]
+  uint8_t* sdST = sPT + 2 * Cfg::kPBytes;    // [2][128 kv][64 q]
+  float* sL = reinterpret_cast<float*>(sdST + 2 * Cfg::kPBytes);  // [QST][64]
+  float* sD = sL + QST * 64;                                      // [QST][64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + QST * 64);
+  uint64_t* kv_full = bars;
+  uint64_t* qdo_full = bars + 1;            // [QST]
+  uint64_t* qdo_empty = qdo_full + QST;     // [QST]
+  uint64_t* s_full = qdo_empty + QST;       // [2]
+  uint64_t* pds_full = s_full + 2;          // [2]
+  uint64_t* pds_free = pds_full + 2;        // [2]
+  uint64_t* st_free = pds_free + 2;         // [2]  S^T_j / dP^T_j read out by the compute warps
+  uint64_t* dq_full = st_free + 2;          // dQ^T in its own TMEM columns
+  uint64_t* dq_free = dq_full + 1;
+  uint64_t* kdv_full = dq_free + 1;
+  uint64_t* kv_empty = kdv_full + 1;  // every MMA reading this item's K / V complete
+  uint64_t* kdv_free = kv_empty + 1;  // dK / dV drained from TMEM by the epilogue
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kdv_free + 1);
+
+  // warp index via shfl: provably warp-uniform, so role branches are not treated as divergent
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
+  const int dt = ht * HD;
+  const int n_kvb = s / 128, BH = batch * ht;
+  const int n_items = n_kvb * BH;
+  // work items (kv block, sequence-head), heaviest (kv block 0) first, handed out in snake order
+  auto snake = [&](int t) {
+    const int G = gridDim.x, c = blockIdx.x;
+    return t * G + ((t & 1) ? G - 1 - c : c);
+  };
+  struct Item {
+    int b, h, row0, kv0, qt_first, n_it;
+  };
+  auto item = [&](int kidx) {
+    Item it;
+    const int kvb = kidx / BH, bh = kidx % BH;
+    it.b = bh / ht;
+    it.h = bh % ht;
+    it.row0 = it.b * s;
+    it.kv0 = kvb * 128;
+    it.qt_first = it.kv0 / 64;
+    it.n_it = s / 64 - it.qt_first;
+    return it;
+  };
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tm_kv);
+    ptx::tma_prefetch_desc(&tm_q);
+    ptx::tma_prefetch_desc(&tm_do);
+    ptx::mbar_init(kv_full, 1);
+    for (int i = 0; i < QST; ++i) {
+      ptx::mbar_init(&qdo_full[i], 1);
+      ptx::mbar_init(&qdo_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&s_full[i], 1);
+      ptx::mbar_init(&pds_full[i], 8);
+      ptx::mbar_init(&pds_free[i], 1);
+      ptx::mbar_init(&st_free[i], 8);
+    }
+    ptx::mbar_init(dq_full, 1);
+    ptx::mbar_init(dq_free, 4);
+    ptx::mbar_init(kdv_full, 1);
+    ptx::mbar_init(kv_empty, 1);
+    ptx::mbar_init(kdv_free, 8);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
+  // TMEM: S^T [2][64] | dP^T [64] (released as soon as it is loaded) | dQ^T [64] | dV | dK
+  const uint32_t tS = tmem, tdP = tmem + 128, tDQ = tmem + 192, tdV = tmem + 256, tdK = tmem + 256 + HD;
+  const int wg = warp / 4;
+  if (wg == 0) ptx::setmaxnreg_dec<64>();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int gt = 0, t = 0;
+      for (int kidx = snake(0); kidx < n_items; kidx = snake(t + 1), ++t) {
+        const Item it = item(kidx);
+        const float* gLq = lse + (static_cast<size_t>(it.b) * ht + it.h) * s;
+        const float* gDq = Dg + (static_cast<size_t>(it.b) * ht + it.h) * s;
+        WAIT(kv_empty, (t & 1) ^ 1, 39);  // previous item's MMAs are done with K / V
+        ptx::mbar_arrive_expect_tx(kv_full, 2 * Cfg::kKVBytes);
+        for (int c = 0; c < NC; ++c) {
+          ptx::tma_load_2d(sK + c * TB, &tm_kv, kv_full, dt + it.h * HD + 64 * c, it.row0 + it.kv0);
+          ptx::tma_load_2d(sV + c * TB, &tm_kv, kv_full, 2 * dt + it.h * HD + 64 * c, it.row0 + it.kv0);
+        }
+        for (int j = 0; j < it.n_it; ++j, ++gt) {
+          const int sq = gt % QST;
+          const int q0 = (it.qt_first + j) * 64;
+          WAIT(&qdo_empty[sq], ((gt / QST) & 1) ^ 1, 40);
+          ptx::mbar_arrive_expect_tx(&qdo_full[sq], 2 * Cfg::kQBytes + 2 * 64 * 4);
+          for (int c = 0; c < NC; ++c) {
+            ptx::tma_load_2d(sQ + sq * Cfg::kQBytes + c * 8192, &tm_q, &qdo_full[sq], it.h * HD + 64 * c, it.row0 + q0);
+            ptx::tma_load_2d(sdO + sq * Cfg::kQBytes + c * 8192, &tm_do, &qdo_full[sq], it.h * HD + 64 * c,
+                             it.row0 + q0);
+          }
+          ptx::bulk_load(sL + sq * 64, gLq + q0, 64 * 4, &qdo_full[sq]);
+          ptx::bulk_load(sD + sq * 64, gDq + q0, 64 * 4, &qdo_full[sq]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    {  // all 32 lanes: uniform descriptors, one elected lane issues
+      constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 64, false, false);   // S^T, dP^T
+      constexpr uint32_t id_acc = ptx::idesc_bf16_f32(128, HD, false, true);  // dV, dK
+      constexpr uint32_t id_dq = ptx::idesc_bf16_f32(HD, 64, true, true);     // dQ^T
+      // Shared-window addresses from the symbol (provably warp-uniform, so descriptors stay in
+      // uniform registers): same layout as the generic pointers above.
+      const uint32_t u0 = (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + 1023u) & ~1023u;
+      const uint32_t aK = u0, aV = u0 + Cfg::kKVBytes;
+      const uint32_t aQ0 = u0 + 2 * Cfg::kKVBytes, adO0 = aQ0 + QST * Cfg::kQBytes;
+      const uint32_t aP0 = adO0 + QST * Cfg::kQBytes, adS0 = aP0 + 2 * Cfg::kPBytes;
+      int gt = 0, t = 0;
+      for (int kidx = snake(0); kidx < n_items; kidx = snake(t + 1), ++t) {
+        const int n_it = item(kidx).n_it;
+        WAIT(kv_full, t & 1, 41);
+        auto stage2 = [&](int i, int g) {  // i: tile within the item, g: global tile
+          const int bb = g & 1, sq = g % QST;
+          if (i == 0 && t > 0) WAIT(kdv_free, (t - 1) & 1, 51);  // previous item's dK / dV drained
+          WAIT(&pds_full[bb], (g >> 1) & 1, 42);
+          ptx::tc_fence_after();
+          const uint32_t aQ = aQ0 + sq * Cfg::kQBytes, adO = adO0 + sq * Cfg::kQBytes;
+          const uint32_t aP = aP0 + bb * Cfg::kPBytes, adS = adS0 + bb * Cfg::kPBytes;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {  // K = 64 query rows
+            const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+            ptx::mma_bf16_ss_w(tdV, ptx::smem_desc_sw128(aP + kk * 32, 16, 1024),
+                               ptx::smem_desc_sw128(adO + kk * 2048, 8192, 1024), id_acc, acc);
+            ptx::mma_bf16_ss_w(tdK, ptx::smem_desc_sw128(adS + kk * 32, 16, 1024),
+                               ptx::smem_desc_sw128(aQ + kk * 2048, 8192, 1024), id_acc, acc);
+          }
+          if (g > 0) WAIT(dq_free, (g - 1) & 1, 44);  // dQ^T_{g-1} read out of its TMEM columns
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)  // K = 128 kv rows
+            ptx::mma_bf16_ss_w(tDQ, ptx::smem_desc_sw128(aK + kk * 2048, TB, 1024),
+                               ptx::smem_desc_sw128(adS + kk * 2048, TB, 1024), id_dq, kk > 0 ? 1u : 0u);
+          ptx::mma_commit_w(dq_full);
+          ptx::mma_commit_w(&qdo_empty[sq]);
+          ptx::mma_commit_w(&pds_free[bb]);
+        };
+        for (int j = 0; j < n_it; ++j) {
+          const int g = gt + j, bb = g & 1, sq = g % QST;
+          WAIT(&qdo_full[sq], (g / QST) & 1, 43);
+          if (g >= 1) WAIT(&st_free[(g - 1) & 1], ((g - 1) >> 1) & 1, 50);
+          ptx::tc_fence_after();
+          const uint32_t aQ = aQ0 + sq * Cfg::kQBytes, adO = adO0 + sq * Cfg::kQBytes;
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint32_t ak = (kk / 4) * TB + (kk % 4) * 32, aq = (kk / 4) * 8192 + (kk % 4) * 32;
+            ptx::mma_bf16_ss_w(tS + bb * 64, ptx::smem_desc_sw128(aK + ak, 16, 1024),
+                               ptx::smem_desc_sw128(aQ + aq, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+            ptx::mma_bf16_ss_w(tdP, ptx::smem_desc_sw128(aV + ak, 16, 1024),
+                               ptx::smem_desc_sw128(adO + aq, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+          }
+          ptx::mma_commit_w(&s_full[bb]);
+          if (j > 0) stage2(j - 1, g - 1);
+        }
+        stage2(n_it - 1, gt + n_it - 1);
+        ptx::mma_commit_w(kdv_full);
+        ptx::mma_commit_w(kv_empty);
+        gt += n_it;
+      }
+    }
+  } else if (wg == 3) {
+    ptx::setmaxnreg_dec<64>();
+    // dQ_i flush: TMEM (lane = head dim, column = query) -> fp32 reductions into dq_acc; per
+    // query one warp instruction covers 32 consecutive head dims (one 128-byte L2 request).
+    const int quarter = warp & 3;
+    const uint32_t lb = static_cast<uint32_t>(quarter * 32) << 16;
+    int gt = 0, t = 0;
+    for (int kidx = snake(0); kidx < n_items; kidx = snake(t + 1), ++t) {
+      const Item it = item(kidx);
+      for (int i = 0; i < it.n_it; ++i, ++gt) {
+        const int q0 = (it.qt_first + i) * 64;
+        float* dst = dq_acc + static_cast<size_t>(it.row0 + q0) * dt + it.h * HD + quarter * 32 + lane;
+        WAIT(dq_full, gt & 1, 45);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int hq = 0; hq < 2; ++hq) {
+          uint32_t v[32];
+          ptx::tmem_ld_32x32b_x32(tDQ + lb + hq * 32, v);
+          ptx::tmem_ld_wait();
+          if (hq == 1) {
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(dq_free);
+          }
+#pragma unroll
+          for (int e = 0; e < 32; ++e) atomicAdd(dst + static_cast<size_t>(hq * 32 + e) * dt, __uint_as_float(v[e]));
+        }
+      }
+    }
+  } else if (wg == 1 || wg == 2) {
+    ptx::setmaxnreg_inc<192>();
+    const int quarter = warp & 3;
+    const int half = wg - 1;            // which 32 query columns of the 64-row tile
+    const int r = quarter * 32 + lane;  // TMEM lane: kv row (S^T, dP^T, dK, dV)
+    const uint32_t lb = static_cast<uint32_t>(quarter * 32) << 16;
+    int gt = 0, t = 0;
+    for (int kidx = snake(0); kidx < n_items; kidx = snake(t + 1), ++t) {
+    const Item it = item(kidx);
+    const int kv0 = it.kv0, row0 = it.row0, h = it.h;
+    for (int j = 0; j < it.n_it; ++j) {
+      const int g = gt + j, bb = g & 1, sq = g % QST;
+      const int q0 = (it.qt_first + j) * 64;
+      WAIT(&s_full[bb], (g >> 1) & 1, 46);
+      WAIT(&qdo_full[sq], (g / QST) & 1, 49);  // LSE / D rows of this tile (already complete)
+      ptx::tc_fence_after();
+      const int qc = half * 32;
+      uint32_t sv[32], dv[32];
+      ptx::tmem_ld_32x32b_x32(tS + lb + bb * 64 + qc, sv);
+      ptx::tmem_ld_32x32b_x32(tdP + lb + qc, dv);
+      ptx::tmem_ld_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&st_free[bb]);  // S^T / dP^T of this tile consumed
+      const float4* L4 = reinterpret_cast<const float4*>(sL + sq * 64 + qc);
+      const float4* D4 = reinterpret_cast<const float4*>(sD + sq * 64 + qc);
+      uint32_t pk[16], dk[16];
+#pragma unroll
+      for (int e4 = 0; e4 < 8; ++e4) {
+        const float4 l4 = L4[e4], d4 = D4[e4];
+        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dvv[4] = {d4.x, d4.y, d4.z, d4.w};
+        float pp[4], ds[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          pp[k] = ex2(fmaf(__uint_as_float(sv[4 * e4 + k]), scale_log2, -lv[k]));
+          ds[k] = pp[k] * (__uint_as_float(dv[4 * e4 + k]) - dvv[k]);
+        }
+        pk[2 * e4] = ptx::pack_bf16(pp[0], pp[1]);
+        pk[2 * e4 + 1] = ptx::pack_bf16(pp[2], pp[3]);
+        dk[2 * e4] = ptx::pack_bf16(ds[0], ds[1]);
+        dk[2 * e4 + 1] = ptx::pack_bf16(ds[2], ds[3]);
+      }
+      if (q0 + qc < kv0 + r) {  // near the diagonal: queries before this kv row see nothing
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (q0 + qc + e < kv0 + r) {
+            pk[e / 2] &= (e & 1) ? 0x0000FFFFu : 0xFFFF0000u;
+            dk[e / 2] &= (e & 1) ? 0x0000FFFFu : 0xFFFF0000u;
+          }
+      }
+      WAIT(&pds_free[bb], ((g >> 1) & 1) ^ 1, 47);  // stage 2 of tile j-2 is done with buffer bb
+      uint8_t* prow = sPT + bb * Cfg::kPBytes + r * 128;
+      uint8_t* drow = sdST + bb * Cfg::kPBytes + r * 128;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int off = ((half * 4 + u) ^ (r & 7)) * 16;
+        *reinterpret_cast<uint4*>(prow + off) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        *reinterpret_cast<uint4*>(drow + off) = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+      }
+      ptx::fence_proxy_async();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&pds_full[bb]);
+    }
+    // dK (scaled) and dV rows of this KV block
+    WAIT(kdv_full, t & 1, 48);
+    ptx::tc_fence_after();
+    __nv_bfloat16* krow = dqkv + static_cast<size_t>(row0 + kv0 + r) * 3 * dt + dt + h * HD;
+    __nv_bfloat16* vrow = krow + dt;
+    constexpr int NCH = HD / 32;
+#pragma unroll 1
+    for (int c = half * (NCH / 2); c < (half + 1) * (NCH / 2); ++c) {
+      uint32_t kv[32], vv[32];
+      ptx::tmem_ld_32x32b_x32(tdK + lb + c * 32, kv);
+      ptx::tmem_ld_32x32b_x32(tdV + lb + c * 32, vv);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 a, bb2;
+        a.x = ptx::pack_bf16(__uint_as_float(kv[8 * q]) * scale, __uint_as_float(kv[8 * q + 1]) * scale);
+        a.y = ptx::pack_bf16(__uint_as_float(kv[8 * q + 2]) * scale, __uint_as_float(kv[8 * q + 3]) * scale);
+        a.z = ptx::pack_bf16(__uint_as_float(kv[8 * q + 4]) * scale, __uint_as_float(kv[8 * q + 5]) * scale);
+        a.w = ptx::pack_bf16(__uint_as_float(kv[8 * q + 6]) * scale, __uint_as_float(kv[8 * q + 7]) * scale);
+        bb2.x = ptx::pack_bf16(__uint_as_float(vv[8 * q]), __uint_as_float(vv[8 * q + 1]));
+        bb2.y = ptx::pack_bf16(__uint_as_float(vv[8 * q + 2]), __uint_as_float(vv[8 * q + 3]));
+        bb2.z = ptx::pack_bf16(__uint_as_float(vv[8 * q + 4]), __uint_as_float(vv[8 * q + 5]));
+        bb2.w = ptx::pack_bf16(__uint_as_float(vv[8 * q + 6]), __uint_as_float(vv[8 * q + 7]));
+        reinterpret_cast<uint4*>(krow + c * 32)[q] = a;
+        reinterpret_cast<uint4*>(vrow + c * 32)[q] = bb2;
+      }
+    }
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(kdv_free);  // dK / dV TMEM reusable by the next item
+    gt += it.n_it;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int HD>
 int bwd_tc2(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* D,
             float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st) {
   using Cfg = TcBwd2Cfg<HD>;
@@ -1181,6 +1496,31 @@ int bwd_tc2(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* d
   const float scale = 1.f / sqrtf(static_cast<float>(HD));
   fa_bwd_tc2_kernel<HD><<<grid, 512, Cfg::kSmem, st>>>(tkv, tq, tdo, lse, D, dq_acc, dqkv, a.seq, a.heads,
                                                         scale * kLog2e, scale);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+template <int HD>
+int bwd_tc2_persistent(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse,
+                       const float* D, float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st) {
+  using Cfg = TcBwd2Cfg<HD>;
+  static bool init = false;
+  if (!init) {
+    if (cudaFuncSetAttribute(fa_bwd_tc2_persistent<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
+        cudaSuccess)
+      return 3;
+    init = true;
+  }
+  const int dt = a.heads * HD;
+  const uint64_t M = static_cast<uint64_t>(a.batch) * a.seq;
+  CUtensorMap tkv, tq, tdo;
+  if (!make_tmap_bf16(&tkv, qkv, 3 * static_cast<uint64_t>(dt), M, 3 * dt, 64, 128)) return 3;
+  if (!make_tmap_bf16(&tq, qkv, 3 * static_cast<uint64_t>(dt), M, 3 * dt, 64, 64)) return 3;
+  if (!make_tmap_bf16(&tdo, dout, static_cast<uint64_t>(dt), M, dt, 64, 64)) return 3;
+  const int items = (a.seq / 128) * a.batch * a.heads;
+  const int grid = items < device_sm_count() ? items : device_sm_count();
+  const float scale = 1.f / sqrtf(static_cast<float>(HD));
+  fa_bwd_tc2_persistent<HD><<<grid, 512, Cfg::kSmem, st>>>(tkv, tq, tdo, lse, D, dq_acc, dqkv, a.seq, a.heads, a.batch,
+                                                           scale * kLog2e, scale);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
@@ -1255,7 +1595,16 @@ int flash_attn_bwd_tc_main(const AttnShape& a, const __nv_bfloat16* qkv, const _
   if (a.seq % 128 != 0) return 1;
   switch (a.head_dim) {
     case 64: return bwd_tc<64>(a, qkv, dout, lse, D, dq_acc, dqkv, st);
-    case 128: return bwd_tc2<128>(a, qkv, dout, lse, D, dq_acc, dqkv, st);
+    case 128: {
+      // persistent CTAs win when there are few (kv block, head) items per SM (the per-item K/V
+      // reload and dK/dV drain are cheaper than CTA turnover); with many items the per-block grid
+      // keeps more work in flight (measured: 6 heads x 4 seqs 0.132 -> 0.113 ms, 16 x 8 0.540 -> 0.607)
+      static const char* forced = std::getenv("GPTB200_ATTN_BWD_PER_BLOCK");  // A/B switch: 1 / 0
+      const int items = (a.seq / 128) * a.batch * a.heads;
+      const bool per_block = forced ? forced[0] == '1' : items > 6 * device_sm_count();
+      return per_block ? bwd_tc2<128>(a, qkv, dout, lse, D, dq_acc, dqkv, st)
+                       : bwd_tc2_persistent<128>(a, qkv, dout, lse, D, dq_acc, dqkv, st);
+    }
     default: return 1;
   }
 }
