@@ -79,6 +79,26 @@ int tp_pipeline_actions(int p, int m, int v, int device, int dh_ring, int forwar
 /* Rank layout (perf.cpp:15-20): rank = t + tp*(p + pp*d). out = {t, p, d}. */
 int tp_rank_coords(int rank, int tp, int pp, int dp, int out[3]);
 
+/* ------------------------------------------------------------------ hardware counters
+ * trainplan::parse_ncu_csv + hw_flops (include/trainplan/metrics.hpp), the B200 replacement of
+ * the reference's parse_counter_csv / hw_flops over AMD SQ_INSTS_VALU_* counters
+ * (proj/src/metrics.cpp:67-117). `text` is `ncu --csv` output (long or --page raw form); only
+ * launches whose kernel name contains `kernel_filter` are summed (NULL or "" = all). */
+typedef struct tp_hw_counters {
+  uint64_t launches;
+  uint64_t tensor_utc_bf16, tensor_utc_f16, tensor_hmma_bf16, tensor_hmma_f16; /* ncu math ops */
+  uint64_t dram_read_bytes, dram_write_bytes, duration_ns;
+  double tensor_flops, simt_flops, hw_flops; /* FLOPs (measured coefficients, metrics.hpp) */
+  int num_warnings;                          /* unknown metrics skipped */
+} tp_hw_counters;
+int tp_ncu_parse_csv(const char* text, size_t len, const char* kernel_filter, tp_hw_counters* out);
+/* The --metrics list tp_ncu_parse_csv understands, comma-separated, into buf (NUL-terminated). */
+int tp_ncu_metric_list(char* buf, size_t cap);
+/* trainplan::diagnose_mbs_mismatch (reference semantics, metrics.cpp:164-185): kind 0 consistent,
+ * 1 micro-batch mismatch, 2 unexplained; ratio = model / hardware; message into msg. */
+int tp_diagnose_mbs_mismatch(double model_tflops, double hw_tflops, int cfg_mbs, int ds_mbs, int* kind,
+                             double* ratio, char* msg, size_t cap);
+
 /* ------------------------------------------------------------------ K1-K4 GEMM
  * C[m,n] = sum_k A(m,k) B(n,k); A(m,k) = A[m*lda+k] (a_mn=0) or A[k*lda+m] (a_mn=1);
  * B(n,k) = B[n*ldb+k] (b_mn=0) or B[k*ldb+n] (b_mn=1). bf16 operands, fp32 accumulation.

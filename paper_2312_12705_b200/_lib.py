@@ -108,7 +108,24 @@ SIGNATURES: dict[str, tuple] = {
     "tp_session_allreduce_max": (_i, [_vp, C.POINTER(_f)]),
     "tp_session_debug_tp_allreduce": (_i, [_vp, _vp, _vp, _i]),
     "tp_session_bench_tp_allreduce": (_i, [_vp, _i, _i, _i, C.POINTER(_f), C.POINTER(_i)]),
+    "tp_ncu_parse_csv": (_i, [C.c_char_p, C.c_size_t, C.c_char_p, _vp]),
+    "tp_ncu_metric_list": (_i, [C.c_char_p, C.c_size_t]),
+    "tp_diagnose_mbs_mismatch": (_i, [C.c_double, C.c_double, _i, _i, C.POINTER(_i), C.POINTER(C.c_double),
+                                      C.c_char_p, C.c_size_t]),
 }
+
+
+
+class HwCounters(C.Structure):
+    """tp_hw_counters (capi.h): summed ncu counters of the selected launches."""
+    _fields_ = [("launches", _u64), ("tensor_utc_bf16", _u64), ("tensor_utc_f16", _u64),
+                ("tensor_hmma_bf16", _u64), ("tensor_hmma_f16", _u64), ("dram_read_bytes", _u64),
+                ("dram_write_bytes", _u64), ("duration_ns", _u64), ("tensor_flops", C.c_double),
+                ("simt_flops", C.c_double), ("hw_flops", C.c_double), ("num_warnings", _i)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
 
 _lib = None
 
@@ -150,6 +167,30 @@ def gemm_bf16(M, N, K, A, lda, a_mn, B, ldb, b_mn, Cm, ldc, epi=0, bias=None, C2
     """Raw pointer GEMM (device addresses as ints)."""
     check(load().tp_gemm_bf16(M, N, K, A, lda, int(a_mn), B, ldb, int(b_mn), Cm, ldc, epi, bias, C2,
                               aux, ldaux, accumulate, stream))
+
+
+# ---------------------------------------------------------------- hardware counters
+def ncu_parse_csv(text: str, kernel_filter: str | None = None) -> dict:
+    """trainplan::parse_ncu_csv + hw_flops (metrics.hpp) over `ncu --csv` output."""
+    raw = text.encode()
+    out = HwCounters()
+    check(load().tp_ncu_parse_csv(raw, len(raw), kernel_filter.encode() if kernel_filter else None,
+                                  C.byref(out)))
+    return out.as_dict()
+
+
+def diagnose_mbs_mismatch(model_tflops: float, hw_tflops: float, cfg_mbs: int, ds_mbs: int) -> dict:
+    """trainplan::diagnose_mbs_mismatch: kind 0 consistent / 1 MBS mismatch / 2 unexplained."""
+    kind, ratio, msg = _i(), C.c_double(), C.create_string_buffer(512)
+    check(load().tp_diagnose_mbs_mismatch(model_tflops, hw_tflops, cfg_mbs, ds_mbs, C.byref(kind),
+                                          C.byref(ratio), msg, len(msg)))
+    return {"kind": kind.value, "flops_ratio": ratio.value, "message": msg.value.decode()}
+
+
+def ncu_metric_list() -> str:
+    buf = C.create_string_buffer(4096)
+    check(load().tp_ncu_metric_list(buf, len(buf)))
+    return buf.value.decode()
 
 
 # ---------------------------------------------------------------- plan layer

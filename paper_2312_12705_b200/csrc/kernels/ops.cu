@@ -4,18 +4,21 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
 
 #include "ops.h"
 #include "rowops.cuh"
+#include "sm100_ptx.cuh"
 
 namespace gptb200 {
 
 namespace {
 
 using namespace rowops;
+using namespace ptx;
 
 // vectors-per-thread choice: threads = (d/8)/vpt, a multiple of 32 and <= 1024
 int pick_vpt(int d) {
@@ -427,6 +430,156 @@ __global__ void __launch_bounds__(256) ln_bwd_fused_kernel(LnBwdArgs a, DropDev 
   }
 }
 
+// Persistent, bulk-copy-staged LayerNorm backward (rows fill the GPU, d <= 4096, rows % R == 0).
+// Each CTA walks the R-row slabs blockIdx.x, blockIdx.x + gridDim.x, ...; x and dy of a slab are
+// contiguous, so one cp.async.bulk per tensor moves them into a kLnStages-deep shared-memory ring
+// (mbarrier tx-count completion). Pass 1 (8 / R warps per row): the two row reductions from
+// shared memory; pass 2 (thread per 8 columns): dx, dropout'(dx), dgamma/dbeta/dbias partials,
+// accumulated in registers across all of the CTA's slabs. x and dy cross HBM exactly once (the
+// 32-row fused form re-reads them from L2 and, with ~1000 resident slabs = 256 MB > L2, partly
+// from HBM). Partials: ws[gridDim.x][3][d], reduced by reduce_partials_kernel in fixed order.
+constexpr int kLnStages = 3;
+
+template <int R, int NG>
+__global__ void __launch_bounds__(256, 2) ln_bwd_stream_kernel(LnBwdArgs a, DropDev dr, float* __restrict__ ws,
+                                                              int nslabs) {
+  constexpr int W = 8 / R;  // warps per row in pass 1
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ uint64_t full[kLnStages];
+  __shared__ float part[R][W][2];
+  __shared__ float smu[R], srs[R];
+  const int d = a.d;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const uint32_t tile = static_cast<uint32_t>(R) * d * 2;  // bytes of one tensor's slab
+  const int my = (nslabs - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) / gridDim.x;
+  auto sx = [&](int st) { return reinterpret_cast<const bf16*>(ring + static_cast<size_t>(st) * 2 * tile); };
+  auto sdy = [&](int st) { return reinterpret_cast<const bf16*>(ring + static_cast<size_t>(st) * 2 * tile + tile); };
+  auto issue = [&](int i) {
+    const int st = i % kLnStages;
+    const size_t off = static_cast<size_t>(blockIdx.x + static_cast<size_t>(i) * gridDim.x) * R * d;
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&full[st], 2 * tile);
+    bulk_load(ring + static_cast<size_t>(st) * 2 * tile, a.x + off, tile, &full[st]);
+    bulk_load(ring + static_cast<size_t>(st) * 2 * tile + tile, a.dy + off, tile, &full[st]);
+  };
+  if (tid == 0) {
+    for (int st = 0; st < kLnStages; ++st) mbar_init(&full[st], 1);
+    fence_mbar_init();
+    for (int i = 0; i < kLnStages && i < my; ++i) issue(i);
+  }
+  float g[NG][8], ag[NG][8], ab[NG][8], as[NG][8];
+#pragma unroll
+  for (int k = 0; k < NG; ++k) {
+    const int c0 = tid * 8 + k * 2048;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ag[k][i] = ab[k][i] = as[k][i] = g[k][i] = 0.f;
+    if (c0 < d) unpack8(*reinterpret_cast<const uint4*>(a.gamma + c0), g[k]);
+  }
+  __syncthreads();
+  const int pr = warp / W, psub = warp % W;
+  for (int i = 0; i < my; ++i) {
+    const int st = i % kLnStages;
+    const int row0 = (blockIdx.x + i * gridDim.x) * R;
+    mbar_wait(&full[st], (i / kLnStages) & 1);
+    const bf16* xs = sx(st);
+    const bf16* dys = sdy(st);
+    {  // pass 1: row reductions
+      const int row = row0 + pr;
+      const float mu = a.mean[row], rs = a.rstd[row];
+      float s1 = 0.f, s2 = 0.f;
+      for (int c0 = (psub * 32 + lane) * 8; c0 < d; c0 += W * 256) {
+        float x[8], dy[8], gg[8];
+        unpack8(*reinterpret_cast<const uint4*>(xs + pr * d + c0), x);
+        unpack8(*reinterpret_cast<const uint4*>(dys + pr * d + c0), dy);
+        unpack8(*reinterpret_cast<const uint4*>(a.gamma + c0), gg);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float gy = dy[e] * gg[e];
+          s1 += gy;
+          s2 += gy * (x[e] - mu) * rs;
+        }
+      }
+      for (int off = 16; off; off >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffff, s1, off);
+        s2 += __shfl_xor_sync(0xffffffff, s2, off);
+      }
+      if (lane == 0) {
+        part[pr][psub][0] = s1;
+        part[pr][psub][1] = s2;
+        if (psub == 0) {
+          smu[pr] = mu;
+          srs[pr] = rs;
+        }
+      }
+    }
+    __syncthreads();
+    // pass 2: thread per 8 columns
+#pragma unroll
+    for (int k = 0; k < NG; ++k) {
+      const int c0 = tid * 8 + k * 2048;
+      if (c0 >= d) continue;
+      float rg[R][8];
+      if (a.resid_grad) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          unpack8(*reinterpret_cast<const uint4*>(a.resid_grad + static_cast<size_t>(row0 + r) * d + c0), rg[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        float m1 = 0.f, m2 = 0.f;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          m1 += part[r][w][0];
+          m2 += part[r][w][1];
+        }
+        m1 /= d;
+        m2 /= d;
+        const float mu = smu[r], rs = srs[r];
+        const size_t o = static_cast<size_t>(row0 + r) * d + c0;
+        float x[8], dy[8], dx[8];
+        unpack8(*reinterpret_cast<const uint4*>(xs + r * d + c0), x);
+        unpack8(*reinterpret_cast<const uint4*>(dys + r * d + c0), dy);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float xh = (x[e] - mu) * rs;
+          dx[e] = rs * (dy[e] * g[k][e] - m1 - xh * m2);
+          ag[k][e] += dy[e] * xh;
+          ab[k][e] += dy[e];
+          if (a.resid_grad) dx[e] += rg[r][e];
+          dx[e] = round_bf16(dx[e]);
+        }
+        if (a.dx) *reinterpret_cast<uint4*>(a.dx + o) = pack8(dx);
+        float od[8];
+        const uint32_t kb = dr.on ? keep8(dr, static_cast<int64_t>(o)) : 0xFFu;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) od[e] = dr.on ? ((kb >> e) & 1u ? dx[e] * dr.scale : 0.f) : dx[e];
+        const uint4 q = pack8(od);
+        if (a.dxd && (dr.on || a.dxd != a.dx)) *reinterpret_cast<uint4*>(a.dxd + o) = q;
+        if (a.dbias) {
+          float qv[8];  // bias grad sums the bf16 values that were stored
+          unpack8(q, qv);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) as[k][e] += qv[e];
+        }
+      }
+    }
+    __syncthreads();  // stage st and the row partials are free again
+    if (tid == 0 && i + kLnStages < my) issue(i + kLnStages);
+  }
+#pragma unroll
+  for (int k = 0; k < NG; ++k) {
+    const int c0 = tid * 8 + k * 2048;
+    if (c0 >= d) continue;
+    float* w = ws + static_cast<size_t>(blockIdx.x) * 3 * d;
+    *reinterpret_cast<float4*>(w + c0) = make_float4(ag[k][0], ag[k][1], ag[k][2], ag[k][3]);
+    *reinterpret_cast<float4*>(w + c0 + 4) = make_float4(ag[k][4], ag[k][5], ag[k][6], ag[k][7]);
+    *reinterpret_cast<float4*>(w + d + c0) = make_float4(ab[k][0], ab[k][1], ab[k][2], ab[k][3]);
+    *reinterpret_cast<float4*>(w + d + c0 + 4) = make_float4(ab[k][4], ab[k][5], ab[k][6], ab[k][7]);
+    *reinterpret_cast<float4*>(w + 2 * d + c0) = make_float4(as[k][0], as[k][1], as[k][2], as[k][3]);
+    *reinterpret_cast<float4*>(w + 2 * d + c0 + 4) = make_float4(as[k][4], as[k][5], as[k][6], as[k][7]);
+  }
+}
+
 constexpr int kLnColRows = 64;
 
 // Phase B: column sums over 64-row chunks of (dy*xhat, dy, dxd); one thread = 8 columns,
@@ -787,6 +940,30 @@ int ln_bwd(const LnBwdArgs& a, cudaStream_t st) {
   // wide-row / few-row shapes keep the row-parallel two-pass form
   const int blocks = (a.rows + kLnFuseRows - 1) / kLnFuseRows;
   static const bool two_pass_only = std::getenv("GPTB200_LN_BWD_TWO_PASS") != nullptr;  // A/B switch
+  static const bool no_stream = std::getenv("GPTB200_LN_BWD_NO_STREAM") != nullptr;     // A/B switch
+  const int R = a.d <= 2048 ? 4 : 2;
+  if (blocks >= 2 * device_sms() && !two_pass_only && !no_stream && a.dy && a.d % 256 == 0 && a.d <= 4096 &&
+      a.rows % R == 0) {
+    const int nslabs = a.rows / R;
+    const int grid = std::min(nslabs, 2 * device_sms());  // <= rows / 32: fits the workspace
+    const size_t smem = static_cast<size_t>(kLnStages) * 2 * R * a.d * 2;
+    static bool attr_set = false;
+    if (!attr_set) {  // the largest ring either variant asks for: 3 stages x 2 tensors x 16 KB rows
+      const int max_smem = kLnStages * 2 * 4 * 2048 * 2;
+      cudaFuncSetAttribute(ln_bwd_stream_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+      cudaFuncSetAttribute(ln_bwd_stream_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+      attr_set = true;
+    }
+    if (R == 4)
+      ln_bwd_stream_kernel<4, 1><<<grid, 256, smem, st>>>(a, dr, a.workspace, nslabs);
+    else
+      ln_bwd_stream_kernel<2, 2><<<grid, 256, smem, st>>>(a, dr, a.workspace, nslabs);
+    const bool any = a.dgamma || a.dbeta || a.dbias;
+    if (any)
+      reduce_partials_kernel<<<(a.d + 31) / 32, 32 * kRedLanes, 0, st>>>(a.workspace, grid, 3 * a.d, a.d, a.dgamma,
+                                                                          a.dbeta, a.dbias);
+    return status();
+  }
   if (blocks >= 2 * device_sms() && !two_pass_only) {
     ln_bwd_fused_kernel<<<blocks, 256, 0, st>>>(a, dr, a.workspace);
     const bool any = (a.dy && (a.dgamma || a.dbeta)) || a.dbias;

@@ -1,3 +1,4 @@
+#include <algorithm>
 // C-ABI wrappers of the structural plan layer (include/trainplan/capi.h "plan" section).
 #include <cstring>
 #include <exception>
@@ -7,6 +8,8 @@
 #include "runtime/status.h"
 #include "trainplan/capi.h"
 #include "trainplan/core.hpp"
+#include "trainplan/metrics.hpp"
+#include <sstream>
 
 using namespace trainplan;
 
@@ -130,6 +133,55 @@ int tp_rank_coords(int rank, int tp, int pp, int dp, int out[3]) {
     out[0] = r.t;
     out[1] = r.p;
     out[2] = r.d;
+  });
+}
+
+int tp_ncu_parse_csv(const char* text, size_t len, const char* kernel_filter, tp_hw_counters* out) {
+  return guarded("tp_ncu_parse_csv", [&] {
+    if (!text || !out) throw std::invalid_argument("null argument");
+    std::istringstream in(std::string(text, len));
+    NcuParseResult r = parse_ncu_csv(in);
+    NcuCounterRecord t;
+    if (!kernel_filter || !*kernel_filter) {
+      t = r.totals;
+    } else {
+      for (const auto& [name, rec] : r.per_kernel)
+        if (name.find(kernel_filter) != std::string::npos) t += rec;
+    }
+    out->launches = t.launches;
+    out->tensor_utc_bf16 = t.tensor_utc_bf16;
+    out->tensor_utc_f16 = t.tensor_utc_f16;
+    out->tensor_hmma_bf16 = t.tensor_hmma_bf16;
+    out->tensor_hmma_f16 = t.tensor_hmma_f16;
+    out->dram_read_bytes = t.dram_read_bytes;
+    out->dram_write_bytes = t.dram_write_bytes;
+    out->duration_ns = t.duration_ns;
+    out->tensor_flops = hw_tensor_flops(t);
+    out->simt_flops = hw_simt_flops(t);
+    out->hw_flops = hw_flops(t);
+    out->num_warnings = static_cast<int>(r.warnings.size());
+  });
+}
+
+int tp_ncu_metric_list(char* buf, size_t cap) {
+  return guarded("tp_ncu_metric_list", [&] {
+    const std::string s = ncu_metric_list();
+    if (!buf || cap < s.size() + 1) throw std::invalid_argument("buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+int tp_diagnose_mbs_mismatch(double model_tflops, double hw_tflops, int cfg_mbs, int ds_mbs, int* kind,
+                             double* ratio, char* msg, size_t cap) {
+  return guarded("tp_diagnose_mbs_mismatch", [&] {
+    MbsDiagnosis d = diagnose_mbs_mismatch(model_tflops, hw_tflops, cfg_mbs, ds_mbs);
+    if (kind) *kind = static_cast<int>(d.kind);
+    if (ratio) *ratio = d.flops_ratio;
+    if (msg && cap) {
+      const size_t n = std::min(cap - 1, d.message.size());
+      std::memcpy(msg, d.message.data(), n);
+      msg[n] = 0;
+    }
   });
 }
 

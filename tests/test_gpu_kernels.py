@@ -116,7 +116,9 @@ def test_flash_attention_fwd_bwd_vs_torch(b, s, h, hd):
         assert e < 2e-2, (sec, e)
 
 
-@pytest.mark.parametrize("rows,d", [(256, 256), (512, 2048), (128, 6144), (64, 12288), (32, 25600)])
+# (16384, 2048) and (12288, 4096) fill the GPU: the persistent bulk-copy-staged LN backward
+@pytest.mark.parametrize("rows,d", [(256, 256), (512, 2048), (128, 6144), (64, 12288), (32, 25600), (16384, 2048),
+                                    (12288, 4096)])
 def test_resid_layernorm_fwd_bwd_vs_torch(rows, d):
     g = torch.Generator(device=DEV).manual_seed(3)
     y = torch.randn(rows, d, device=DEV, generator=g).bfloat16()
@@ -155,6 +157,43 @@ def test_resid_layernorm_fwd_bwd_vs_torch(rows, d):
     assert _rel(dgamma, (dy.float() * xh).sum(0)) < 1e-3
     assert _rel(dbeta, dy.float().sum(0)) < 1e-4
     assert _rel(dbias, dx.float().sum(0)) < 1e-4
+
+
+@pytest.mark.parametrize("rows,d", [(16384, 2048), (12288, 4096)])
+def test_layernorm_bwd_stream_dropout(rows, d):
+    """Persistent LN backward with hidden dropout on a separate dxd output: dx vs torch, the
+    dropout mask vs the oracle's counter hash on sampled rows, dbias = column sums of stored dxd."""
+    import oracle_lib as O
+    g = torch.Generator(device=DEV).manual_seed(5)
+    x = torch.randn(rows, d, device=DEV, generator=g).bfloat16()
+    gamma = (1 + 0.1 * torch.randn(d, device=DEV, generator=g)).bfloat16()
+    xf = x.float()
+    mean = xf.mean(1).contiguous()
+    rstd = torch.rsqrt(xf.var(1, unbiased=False) + 1e-5).contiguous()
+    dy = torch.randn(rows, d, device=DEV, generator=g).bfloat16()
+    rg = torch.randn(rows, d, device=DEV, generator=g).bfloat16()
+    dx, dxd = torch.empty_like(x), torch.empty_like(x)
+    dgamma, dbeta, dbias = (torch.zeros(d, device=DEV) for _ in range(3))
+    ws = torch.empty(T.load().tp_layernorm_bwd_workspace_bytes(rows, d) // 4 + 1, device=DEV)
+    p, seed, step, layer, site, base = 0.1, 1234, 2, 7, 1, 4096
+    T.check(T.load().tp_layernorm_bwd(rows, d, x.data_ptr(), dy.data_ptr(), rg.data_ptr(), gamma.data_ptr(),
+                                      mean.data_ptr(), rstd.data_ptr(), dx.data_ptr(), dxd.data_ptr(), dgamma.data_ptr(),
+                                      dbeta.data_ptr(), dbias.data_ptr(), seed, step, layer, site, p, base,
+                                      ws.data_ptr(), _stream()))
+    torch.cuda.synchronize()
+    xv = xf.clone().requires_grad_(True)
+    torch.nn.functional.layer_norm(xv, (d,), gamma.float(), None, eps=1e-5).backward(dy.float())
+    assert _rel(dx.float(), xv.grad + rg.float()) < 1e-2
+    xh = (xf - mean[:, None]) * rstd[:, None]
+    assert _rel(dgamma, (dy.float() * xh).sum(0)) < 1e-3
+    assert _rel(dbeta, dy.float().sum(0)) < 1e-4
+    assert _rel(dbias, dxd.float().sum(0)) < 1e-4
+    lib = O.load()
+    for r in (0, 1, rows // 2 + 3, rows - 1):
+        keep = np.array([lib.orc_dropout_keep(seed, step, layer, site, base + r * d + c, p) for c in range(d)])
+        got = dxd[r].float().cpu().numpy()
+        ref = np.where(keep, dx[r].float().cpu().numpy() / (1 - p), 0.0)
+        np.testing.assert_allclose(got, ref, rtol=8e-3, atol=1e-6)
 
 
 def test_dropout_mask_matches_oracle_hash():
