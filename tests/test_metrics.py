@@ -46,7 +46,7 @@ def test_parse_long_form(native_lib):
     assert t["dram_read_bytes"] == 1_234_500_000 and t["dram_write_bytes"] == 1000
     assert t["tensor_utc_bf16"] == 68_719_476_736 + 1000 and t["tensor_hmma_bf16"] == 10
     assert t["duration_ns"] == 110_500 + 2500
-    assert t["tensor_flops"] == pytest.approx(2.0 * (68_719_476_736 + 1000 + 10))
+    assert t["tensor_flops"] == pytest.approx(1.0 * (68_719_476_736 + 1000 + 10))
     # FFMA 2, FADD 1, FFMA2 4, HFMA2 4 FLOPs per thread instruction
     assert t["simt_flops"] == 2 * 100 + 10 + 4 * 5 + 4 * 3
     assert t["hw_flops"] == pytest.approx(t["tensor_flops"] + t["simt_flops"])
@@ -145,3 +145,26 @@ def test_executed_flops_model():
     dense_fwd = 16 * 16 * 24 * 4 * 2048 * 2048 * 128
     assert e["attention_fwd"] == pytest.approx(dense_fwd * 136 / 256)
     assert e["attention_bwd"] == pytest.approx(2.5 * dense_fwd * 272 / 512)
+
+
+def test_measured_step_counters_match_executed_flops(native_lib):
+    """The ncu capture of one GPT-1.4B MBS-16 train step on a B200 (profiles/, application replay,
+    cuProfilerStart/Stop around exactly one step): the tcgen05 tensor FLOPs the hardware counted
+    equal, to the FLOP, every GEMM's 2*M*N*K plus the causal attention tiles the kernels visit;
+    the model FLOPs of the reference formula agree with the hardware FLOPs (diagnose: consistent)."""
+    import gzip
+    import sys
+    sys.path.insert(0, str(ROOT / "tools"))
+    import hw_counters as H
+    gemm = T.ncu_parse_csv((ROOT / "profiles" / "r01_hwc_gemm_4096.csv").read_text())
+    assert gemm["launches"] == 1 and gemm["tensor_utc_bf16"] == 2 * 4096 ** 3
+    text = gzip.open(ROOT / "profiles" / "r01_hwc_step_gpt1.4b.csv.gz", "rt").read()
+    step = T.ncu_parse_csv(text)
+    exp = H.executed_tensor_flops(24, 2048, 16, 51200, 2048, 16, False)
+    assert step["tensor_flops"] == exp["total"]
+    assert T.ncu_parse_csv(text, "gemm_sm100")["tensor_flops"] == exp["gemm"]
+    assert T.ncu_parse_csv(text, "fa_fwd")["tensor_flops"] == exp["attention_fwd"]
+    assert T.ncu_parse_csv(text, "fa_bwd")["tensor_flops"] == exp["attention_bwd"]
+    model = T.model_flops(T.ModelSpec(24, 2048, 16, 51200, 2048), 16, False)
+    d = T.diagnose_mbs_mismatch(model, step["hw_flops"], 16, 16)
+    assert d["kind"] == 0, d
