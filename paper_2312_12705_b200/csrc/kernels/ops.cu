@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(256) ln_bwd_fused_kernel(LnBwdArgs a, DropDev 
 
 // Persistent, bulk-copy-staged LayerNorm backward (rows fill the GPU, d <= 4096, rows % R == 0).
 // Each CTA walks the R-row slabs blockIdx.x, blockIdx.x + gridDim.x, ...; x and dy of a slab are
-// contiguous, so one cp.async.bulk per tensor moves them into a kLnStages-deep shared-memory ring
+// contiguous, so one cp.async.bulk per tensor (x, dy and resid_grad) moves them into a shared-memory ring
 // (mbarrier tx-count completion). Pass 1 (8 / R warps per row): the two row reductions from
 // shared memory; pass 2 (thread per 8 columns): dx, dropout'(dx), dgamma/dbeta/dbias partials,
 // accumulated in registers across all of the CTA's slabs. x and dy cross HBM exactly once (the
@@ -442,30 +442,34 @@ constexpr int kLnStages = 3;
 
 template <int R, int NG>
 __global__ void __launch_bounds__(256, 2) ln_bwd_stream_kernel(LnBwdArgs a, DropDev dr, float* __restrict__ ws,
-                                                              int nslabs) {
+                                                              int nslabs, int nst) {
   constexpr int W = 8 / R;  // warps per row in pass 1
   extern __shared__ __align__(128) uint8_t ring[];
-  __shared__ uint64_t full[kLnStages];
+  __shared__ uint64_t full[kLnStages];  // nst <= kLnStages stages in use
   __shared__ float part[R][W][2];
   __shared__ float smu[R], srs[R];
   const int d = a.d;
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const uint32_t tile = static_cast<uint32_t>(R) * d * 2;  // bytes of one tensor's slab
   const int my = (nslabs - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) / gridDim.x;
-  auto sx = [&](int st) { return reinterpret_cast<const bf16*>(ring + static_cast<size_t>(st) * 2 * tile); };
-  auto sdy = [&](int st) { return reinterpret_cast<const bf16*>(ring + static_cast<size_t>(st) * 2 * tile + tile); };
+  const int ntens = a.resid_grad ? 3 : 2;  // x, dy (, resid_grad) slabs per stage
+  const size_t stage_bytes = static_cast<size_t>(ntens) * tile;
+  auto sx = [&](int st) { return reinterpret_cast<const bf16*>(ring + st * stage_bytes); };
+  auto sdy = [&](int st) { return reinterpret_cast<const bf16*>(ring + st * stage_bytes + tile); };
+  auto srg = [&](int st) { return reinterpret_cast<const bf16*>(ring + st * stage_bytes + 2 * tile); };
   auto issue = [&](int i) {
-    const int st = i % kLnStages;
+    const int st = i % nst;
     const size_t off = static_cast<size_t>(blockIdx.x + static_cast<size_t>(i) * gridDim.x) * R * d;
     fence_proxy_async();
-    mbar_arrive_expect_tx(&full[st], 2 * tile);
-    bulk_load(ring + static_cast<size_t>(st) * 2 * tile, a.x + off, tile, &full[st]);
-    bulk_load(ring + static_cast<size_t>(st) * 2 * tile + tile, a.dy + off, tile, &full[st]);
+    mbar_arrive_expect_tx(&full[st], ntens * tile);
+    bulk_load(ring + st * stage_bytes, a.x + off, tile, &full[st]);
+    bulk_load(ring + st * stage_bytes + tile, a.dy + off, tile, &full[st]);
+    if (a.resid_grad) bulk_load(ring + st * stage_bytes + 2 * tile, a.resid_grad + off, tile, &full[st]);
   };
   if (tid == 0) {
-    for (int st = 0; st < kLnStages; ++st) mbar_init(&full[st], 1);
+    for (int st = 0; st < nst; ++st) mbar_init(&full[st], 1);
     fence_mbar_init();
-    for (int i = 0; i < kLnStages && i < my; ++i) issue(i);
+    for (int i = 0; i < nst && i < my; ++i) issue(i);
   }
   float g[NG][8], ag[NG][8], ab[NG][8], as[NG][8];
 #pragma unroll
@@ -478,9 +482,9 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_stream_kernel(LnBwdArgs a, Drop
   __syncthreads();
   const int pr = warp / W, psub = warp % W;
   for (int i = 0; i < my; ++i) {
-    const int st = i % kLnStages;
+    const int st = i % nst;
     const int row0 = (blockIdx.x + i * gridDim.x) * R;
-    mbar_wait(&full[st], (i / kLnStages) & 1);
+    mbar_wait(&full[st], (i / nst) & 1);
     const bf16* xs = sx(st);
     const bf16* dys = sdy(st);
     {  // pass 1: row reductions
@@ -518,12 +522,6 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_stream_kernel(LnBwdArgs a, Drop
     for (int k = 0; k < NG; ++k) {
       const int c0 = tid * 8 + k * 2048;
       if (c0 >= d) continue;
-      float rg[R][8];
-      if (a.resid_grad) {
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-          unpack8(*reinterpret_cast<const uint4*>(a.resid_grad + static_cast<size_t>(row0 + r) * d + c0), rg[r]);
-      }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         float m1 = 0.f, m2 = 0.f;
@@ -536,16 +534,17 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_stream_kernel(LnBwdArgs a, Drop
         m2 /= d;
         const float mu = smu[r], rs = srs[r];
         const size_t o = static_cast<size_t>(row0 + r) * d + c0;
-        float x[8], dy[8], dx[8];
+        float x[8], dy[8], dx[8], rg[8];
         unpack8(*reinterpret_cast<const uint4*>(xs + r * d + c0), x);
         unpack8(*reinterpret_cast<const uint4*>(dys + r * d + c0), dy);
+        if (a.resid_grad) unpack8(*reinterpret_cast<const uint4*>(srg(st) + r * d + c0), rg);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const float xh = (x[e] - mu) * rs;
           dx[e] = rs * (dy[e] * g[k][e] - m1 - xh * m2);
           ag[k][e] += dy[e] * xh;
           ab[k][e] += dy[e];
-          if (a.resid_grad) dx[e] += rg[r][e];
+          if (a.resid_grad) dx[e] += rg[e];
           dx[e] = round_bf16(dx[e]);
         }
         if (a.dx) *reinterpret_cast<uint4*>(a.dx + o) = pack8(dx);
@@ -564,7 +563,7 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_stream_kernel(LnBwdArgs a, Drop
       }
     }
     __syncthreads();  // stage st and the row partials are free again
-    if (tid == 0 && i + kLnStages < my) issue(i + kLnStages);
+    if (tid == 0 && i + nst < my) issue(i + nst);
   }
 #pragma unroll
   for (int k = 0; k < NG; ++k) {
@@ -946,18 +945,21 @@ int ln_bwd(const LnBwdArgs& a, cudaStream_t st) {
       a.rows % R == 0) {
     const int nslabs = a.rows / R;
     const int grid = std::min(nslabs, 2 * device_sms());  // <= rows / 32: fits the workspace
-    const size_t smem = static_cast<size_t>(kLnStages) * 2 * R * a.d * 2;
+    // ~96 KB ring (2 CTAs per SM): 3 stages of x/dy, or 2 stages of x/dy/resid_grad
+    const int ntens = a.resid_grad ? 3 : 2;
+    const int nst = a.resid_grad ? 2 : 3;
+    const size_t smem = static_cast<size_t>(nst) * ntens * R * a.d * 2;
     static bool attr_set = false;
-    if (!attr_set) {  // the largest ring either variant asks for: 3 stages x 2 tensors x 16 KB rows
-      const int max_smem = kLnStages * 2 * 4 * 2048 * 2;
+    if (!attr_set) {  // the largest ring either variant asks for
+      const int max_smem = 3 * 2 * 4 * 2048 * 2;
       cudaFuncSetAttribute(ln_bwd_stream_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
       cudaFuncSetAttribute(ln_bwd_stream_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
       attr_set = true;
     }
     if (R == 4)
-      ln_bwd_stream_kernel<4, 1><<<grid, 256, smem, st>>>(a, dr, a.workspace, nslabs);
+      ln_bwd_stream_kernel<4, 1><<<grid, 256, smem, st>>>(a, dr, a.workspace, nslabs, nst);
     else
-      ln_bwd_stream_kernel<2, 2><<<grid, 256, smem, st>>>(a, dr, a.workspace, nslabs);
+      ln_bwd_stream_kernel<2, 2><<<grid, 256, smem, st>>>(a, dr, a.workspace, nslabs, nst);
     const bool any = a.dgamma || a.dbeta || a.dbias;
     if (any)
       reduce_partials_kernel<<<(a.d + 31) / 32, 32 * kRedLanes, 0, st>>>(a.workspace, grid, 3 * a.d, a.d, a.dgamma,

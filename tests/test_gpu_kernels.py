@@ -133,7 +133,7 @@ def test_resid_layernorm_fwd_bwd_vs_torch(rows, d):
     T.check(T.load().tp_resid_layernorm_fwd(rows, d, y.data_ptr(), bias.data_ptr(), resid.data_ptr(), h.data_ptr(),
                                             gamma.data_ptr(), beta.data_ptr(), ln.data_ptr(), mean.data_ptr(),
                                             rstd.data_ptr(), 0, 0, 0, 0, 0.0, 0, _stream()))
-    href = (resid.float() + y.float() + bias.float()).bfloat16().float()
+    href = (resid.float() + (y.float() + bias.float())).bfloat16().float()  # h = r + (y + b), as the oracle
     torch.cuda.synchronize()
     assert torch.equal(h.float(), href)
     x = href.clone().requires_grad_(True)

@@ -40,8 +40,10 @@ def run(rows, d, p=0.1, iters=20):
 
 
 if __name__ == "__main__":
+    run(32768, 2048)  # the 1.4B MBS-16 step's shape
     run(16384, 2048)
     run(16384, 2048, p=0.0)
+    run(12288, 4096)
     run(2048, 6144)
     run(2048, 12288)
     run(2048, 25600)
