@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include "attention.h"
+#include "pdl.cuh"
 #include "sm100_ptx.cuh"
 #include "tma_host.h"
 
@@ -393,6 +394,8 @@ __global__ void __launch_bounds__(TcFwdCfg<HD>::kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  pdl_trigger();  // prologue (smem / TMEM / barriers) done: see pdl.cuh
+  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -953,6 +956,8 @@ __global__ void __launch_bounds__(512, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
+  pdl_trigger();  // prologue (smem / TMEM / barriers) done: see pdl.cuh
+  pdl_wait();
   // TMEM: S^T [2][64] | dP^T [64] (released as soon as it is loaded) | dQ^T [64] | dV | dK
   const uint32_t tS = tmem, tdP = tmem + 128, tDQ = tmem + 192, tdV = tmem + 256, tdK = tmem + 256 + HD;
   const int wg = warp / 4;
@@ -1246,6 +1251,8 @@ __global__ void __launch_bounds__(512, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
+  pdl_trigger();  // prologue (smem / TMEM / barriers) done: see pdl.cuh
+  pdl_wait();
   // TMEM: S^T [2][64] | dP^T [64] (released as soon as it is loaded) | dQ^T [64] | dV | dK
   const uint32_t tS = tmem, tdP = tmem + 128, tDQ = tmem + 192, tdV = tmem + 256, tdK = tmem + 256 + HD;
   const int wg = warp / 4;
@@ -1494,8 +1501,8 @@ int bwd_tc2(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* d
   if (!make_tmap_bf16(&tdo, dout, static_cast<uint64_t>(dt), M, dt, 64, 64)) return 3;
   dim3 grid(a.seq / 128, a.batch * a.heads);
   const float scale = 1.f / sqrtf(static_cast<float>(HD));
-  fa_bwd_tc2_kernel<HD><<<grid, 512, Cfg::kSmem, st>>>(tkv, tq, tdo, lse, D, dq_acc, dqkv, a.seq, a.heads,
-                                                        scale * kLog2e, scale);
+  launch_pdl(fa_bwd_tc2_kernel<HD>, grid, dim3(512), Cfg::kSmem, st, tkv, tq, tdo, lse, D, dq_acc, dqkv, a.seq,
+             a.heads, scale * kLog2e, scale);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
@@ -1519,8 +1526,8 @@ int bwd_tc2_persistent(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_
   const int items = (a.seq / 128) * a.batch * a.heads;
   const int grid = items < device_sm_count() ? items : device_sm_count();
   const float scale = 1.f / sqrtf(static_cast<float>(HD));
-  fa_bwd_tc2_persistent<HD><<<grid, 512, Cfg::kSmem, st>>>(tkv, tq, tdo, lse, D, dq_acc, dqkv, a.seq, a.heads, a.batch,
-                                                           scale * kLog2e, scale);
+  launch_pdl(fa_bwd_tc2_persistent<HD>, dim3(grid), dim3(512), Cfg::kSmem, st, tkv, tq, tdo, lse, D, dq_acc, dqkv,
+             a.seq, a.heads, a.batch, scale * kLog2e, scale);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
@@ -1563,8 +1570,8 @@ int fwd_tc_persistent(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat1
     return 3;
   const int items = (a.seq / kBM) * a.batch * a.heads;
   const int grid = items < device_sm_count() ? items : device_sm_count();
-  fa_fwd_tc_persistent<HD><<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(tm, out, lse, a.seq, a.heads, a.batch,
-                                                                    kLog2e / sqrtf(static_cast<float>(HD)));
+  launch_pdl(fa_fwd_tc_persistent<HD>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, tm, out, lse, a.seq, a.heads,
+             a.batch, kLog2e / sqrtf(static_cast<float>(HD)));
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 

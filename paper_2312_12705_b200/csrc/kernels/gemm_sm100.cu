@@ -18,6 +18,7 @@
 #include <cstdio>
 
 #include "gemm.h"
+#include "pdl.cuh"
 #include "sm100_ptx.cuh"
 #include "tma_host.h"
 
@@ -138,6 +139,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
+  // prologue done (smem / TMEM / barriers only): let the next kernel in the stream be scheduled,
+  // then wait for the previous one before the first global-memory access
+  pdl_trigger();
+  pdl_wait();
 
   const int num_m = p.M / kTileM;
   const int num_n = p.N / BN;
@@ -556,13 +561,15 @@ int launch(const GemmParams& p, cudaStream_t stream) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = Cfg::kSmemBytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see pdl.cuh
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   if (cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tc2, p) != cudaSuccess) return kGemmErrCuda;
   return cudaGetLastError() == cudaSuccess ? kGemmOk : kGemmErrCuda;
 }

@@ -11,6 +11,7 @@
 
 #include "ops.h"
 #include "rowops.cuh"
+#include "pdl.cuh"
 #include "sm100_ptx.cuh"
 
 namespace gptb200 {
@@ -109,6 +110,8 @@ __global__ void resid_ln_kernel(ResidLnArgs a, DropDev dr) {
 // (v*32 + lane)*8; both row reductions are warp shuffles (no block barriers).
 template <int VPL>
 __global__ void __launch_bounds__(256, 2) resid_ln_warp_kernel(ResidLnArgs a, DropDev dr) {
+  pdl_trigger();  // launched through launch_pdl (pdl.cuh)
+  pdl_wait();
   const int row = blockIdx.x * 8 + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   if (row >= a.rows) return;
@@ -451,6 +454,8 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_stream_kernel(LnBwdArgs a, Drop
   const int d = a.d;
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const uint32_t tile = static_cast<uint32_t>(R) * d * 2;  // bytes of one tensor's slab
+  pdl_trigger();  // launched through launch_pdl (pdl.cuh): barrier init below is smem-only, but keep it simple
+  pdl_wait();
   const int my = (nslabs - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) / gridDim.x;
   const int ntens = a.resid_grad ? 3 : 2;  // x, dy (, resid_grad) slabs per stage
   const size_t stage_bytes = static_cast<size_t>(ntens) * tile;
@@ -631,6 +636,8 @@ __global__ void __launch_bounds__(32 * kRedLanes) reduce_partials_kernel(const f
                                                                           int stride, int n, float* out0, float* out1,
                                                                           float* out2) {
   __shared__ float red[3][kRedLanes][33];
+  pdl_trigger();  // launched through launch_pdl (pdl.cuh)
+  pdl_wait();
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + tx;
   float s0 = 0.f, s1 = 0.f, s2 = 0.f;
@@ -908,7 +915,7 @@ int resid_ln_fwd(const ResidLnArgs& a, cudaStream_t st) {
   if (a.d % 256 == 0 && a.d <= 4096) {
     const int blocks = (a.rows + 7) / 8;
     switch (a.d / 256) {
-#define WCASE(V) case V: resid_ln_warp_kernel<V><<<blocks, 256, 0, st>>>(a, dr); return status();
+#define WCASE(V) case V: launch_pdl(resid_ln_warp_kernel<V>, dim3(blocks), dim3(256), 0, st, a, dr); return status();
       WCASE(1) WCASE(2) WCASE(3) WCASE(4) WCASE(5) WCASE(6) WCASE(7) WCASE(8)
       WCASE(9) WCASE(10) WCASE(11) WCASE(12) WCASE(13) WCASE(14) WCASE(15) WCASE(16)
 #undef WCASE
@@ -957,12 +964,12 @@ int ln_bwd(const LnBwdArgs& a, cudaStream_t st) {
       attr_set = true;
     }
     if (R == 4)
-      ln_bwd_stream_kernel<4, 1><<<grid, 256, smem, st>>>(a, dr, a.workspace, nslabs, nst);
+      launch_pdl(ln_bwd_stream_kernel<4, 1>, dim3(grid), dim3(256), smem, st, a, dr, a.workspace, nslabs, nst);
     else
-      ln_bwd_stream_kernel<2, 2><<<grid, 256, smem, st>>>(a, dr, a.workspace, nslabs, nst);
+      launch_pdl(ln_bwd_stream_kernel<2, 2>, dim3(grid), dim3(256), smem, st, a, dr, a.workspace, nslabs, nst);
     const bool any = a.dgamma || a.dbeta || a.dbias;
     if (any)
-      reduce_partials_kernel<<<(a.d + 31) / 32, 32 * kRedLanes, 0, st>>>(a.workspace, grid, 3 * a.d, a.d, a.dgamma,
+      launch_pdl(reduce_partials_kernel, dim3((a.d + 31) / 32), dim3(32 * kRedLanes), 0, st, a.workspace, grid, 3 * a.d, a.d, a.dgamma,
                                                                           a.dbeta, a.dbias);
     return status();
   }
@@ -970,7 +977,7 @@ int ln_bwd(const LnBwdArgs& a, cudaStream_t st) {
     ln_bwd_fused_kernel<<<blocks, 256, 0, st>>>(a, dr, a.workspace);
     const bool any = (a.dy && (a.dgamma || a.dbeta)) || a.dbias;
     if (any)
-      reduce_partials_kernel<<<(a.d + 31) / 32, 32 * kRedLanes, 0, st>>>(a.workspace, blocks, 3 * a.d, a.d,
+      launch_pdl(reduce_partials_kernel, dim3((a.d + 31) / 32), dim3(32 * kRedLanes), 0, st, a.workspace, blocks, 3 * a.d, a.d,
                                                                 a.dy ? a.dgamma : nullptr, a.dy ? a.dbeta : nullptr,
                                                                 a.dbias);
     return status();
@@ -1013,7 +1020,7 @@ int ln_bwd_cols(const LnBwdArgs& a, const bf16* dbias_src, cudaStream_t st) {
   const int chunks = (a.rows + kLnColRows - 1) / kLnColRows;
   dim3 grid((a.d / 8 + 255) / 256, chunks);
   ln_bwd_cols_kernel<<<grid, 256, 0, st>>>(a, a.dbias ? dbias_src : nullptr, a.workspace);
-  reduce_partials_kernel<<<(a.d + 31) / 32, 32 * kRedLanes, 0, st>>>(a.workspace, chunks, 3 * a.d, a.d,
+  launch_pdl(reduce_partials_kernel, dim3((a.d + 31) / 32), dim3(32 * kRedLanes), 0, st, a.workspace, chunks, 3 * a.d, a.d,
                                                             a.dy ? a.dgamma : nullptr, a.dy ? a.dbeta : nullptr,
                                                             a.dbias ? a.dbias : nullptr);
   return status();
@@ -1021,7 +1028,7 @@ int ln_bwd_cols(const LnBwdArgs& a, const bf16* dbias_src, cudaStream_t st) {
 
 int reduce_col_partials(const float* partial, int nblocks, int n, float* out, cudaStream_t st) {
   if (nblocks <= 0 || n <= 0) return 1;
-  reduce_partials_kernel<<<(n + 31) / 32, 32 * kRedLanes, 0, st>>>(partial, nblocks, n, n, out, nullptr, nullptr);
+  launch_pdl(reduce_partials_kernel, dim3((n + 31) / 32), dim3(32 * kRedLanes), 0, st, partial, nblocks, n, n, out, nullptr, nullptr);
   return status();
 }
 
@@ -1034,7 +1041,7 @@ int colsum_bf16(const bf16* X, int rows, int n, float* out, float* ws, cudaStrea
   const int splits = (rows + kColsumRows - 1) / kColsumRows;
   dim3 grid((n / 2 + 255) / 256, splits);
   colsum_kernel<<<grid, 256, 0, st>>>(X, rows, n, ws);
-  reduce_partials_kernel<<<(n + 31) / 32, 32 * kRedLanes, 0, st>>>(ws, splits, n, n, out, nullptr, nullptr);
+  launch_pdl(reduce_partials_kernel, dim3((n + 31) / 32), dim3(32 * kRedLanes), 0, st, ws, splits, n, n, out, nullptr, nullptr);
   return status();
 }
 
