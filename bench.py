@@ -5,8 +5,8 @@
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
 
 One process per GPU. Default workload = BASELINE config 2: GPT 1.4B (24 layers, hidden 2048,
-16 heads, seq 2048, V 51200), bf16 with fp32 master weights/grads, flash attention, MBS 8 per GPU,
-data parallel with ZeRO-1 over N GPUs (weak scaling: GBS = 8*N), hidden dropout 0.1, no
+16 heads, seq 2048, V 51200), bf16 with fp32 master weights/grads, flash attention, MBS 32 per GPU,
+data parallel with ZeRO-1 over N GPUs (weak scaling: GBS = 32*N), hidden dropout 0.1, no
 activation checkpointing. A step = one full iteration: forward, backward, DP reduce-scatter,
 ZeRO-1 Adam, parameter allgather.
 
@@ -39,13 +39,14 @@ FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_g
 
 WORKLOADS = {
     # name: (L, d, heads, V, s, mbs, tp, pp, ckpt, dropout, microbatches per DP replica)
-    # BASELINE config 2 (headline): 1.4B on 1 GPU, DP = N with ZeRO-1 beyond. Micro-batch 16 is the
-    # B200 choice from the sweep below (4: 927, 8: 1020, 16: 1062-1075, 32: 1085 TFLOPS/GPU at 138 GB;
-    # 16 keeps half the HBM free) — the reference's own search tunes mbs the same way.
-    "gpt-1.4b": (24, 2048, 16, 51200, 2048, 16, 1, 1, False, 0.1, 1),
+    # BASELINE config 2 (headline): 1.4B on 1 GPU, DP = N with ZeRO-1 beyond. Micro-batch 32 is the
+    # B200 choice from the sweep below (4: 927, 8: 1020, 16: 1062-1095, 32: 1085-1116 TFLOPS/GPU; the
+    # final A/B on one box: 16 -> 1093 / 1096, 32 -> 1113 / 1116; 138 GB of the 180 GB HBM) — the
+    # reference's own search tunes mbs the same way.
+    "gpt-1.4b": (24, 2048, 16, 51200, 2048, 32, 1, 1, False, 0.1, 1),
+    "gpt-1.4b-mbs16": (24, 2048, 16, 51200, 2048, 16, 1, 1, False, 0.1, 1),
     "gpt-1.4b-mbs4": (24, 2048, 16, 51200, 2048, 4, 1, 1, False, 0.1, 1),
     "gpt-1.4b-mbs8": (24, 2048, 16, 51200, 2048, 8, 1, 1, False, 0.1, 1),
-    "gpt-1.4b-mbs32": (24, 2048, 16, 51200, 2048, 32, 1, 1, False, 0.1, 1),
     # BASELINE config 1 shape (tiny GPT) — smoke-sized.
     "gpt-tiny": (2, 256, 4, 51200, 128, 1, 1, 1, False, 0.0, 1),
     # BASELINE config 3: 22B shape with TP = 2/4/8 and activation checkpointing, MBS 1, m = 8.

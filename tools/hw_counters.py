@@ -11,10 +11,10 @@ C-ABI tp_ncu_parse_csv):
   M=$(python tools/hw_counters.py metrics)
   ncu --replay-mode application --profile-from-start off --metrics $M --csv --print-units base \\
       --log-file gpurun_out/hwc_gemm.csv python tools/hw_counters.py run-gemm 4096 4096 4096
-  ncu ... --log-file gpurun_out/hwc_step.csv python tools/hw_counters.py run-step --workload gpt-1.4b
+  ncu ... --log-file gpurun_out/hwc_step.csv python tools/hw_counters.py run-step --workload gpt-1.4b-mbs16
   # anywhere
   python tools/hw_counters.py analyze --gemm-csv gpurun_out/hwc_gemm.csv --gemm 4096 4096 4096 \\
-      --step-csv gpurun_out/hwc_step.csv --workload gpt-1.4b > profiles/r01_hw_counters.json
+      --step-csv gpurun_out/hwc_step.csv --workload gpt-1.4b-mbs16 > profiles/r01_hw_counters.json
 
 `run-*` bracket exactly the measured work with cuProfilerStart/Stop (one GEMM launch; one full
 train step after two warm-up steps), so the CSV holds nothing else.
@@ -158,12 +158,12 @@ def main():
     g.add_argument("N", type=int)
     g.add_argument("K", type=int)
     r = sub.add_parser("run-step")
-    r.add_argument("--workload", default="gpt-1.4b")
+    r.add_argument("--workload", default="gpt-1.4b-mbs16")
     an = sub.add_parser("analyze")
     an.add_argument("--gemm-csv")
     an.add_argument("--gemm", type=int, nargs=3, default=[4096, 4096, 4096])
     an.add_argument("--step-csv")
-    an.add_argument("--workload", default="gpt-1.4b")
+    an.add_argument("--workload", default="gpt-1.4b-mbs16")
     args = ap.parse_args()
     if args.cmd == "metrics":
         print(T.ncu_metric_list())
