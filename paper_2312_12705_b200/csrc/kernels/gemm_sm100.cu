@@ -306,6 +306,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c2 = ehalf * (BN / 128); c2 < (ehalf + 1) * (BN / 128); ++c2) {  // 64-column units
             uint32_t g[2][16];
             float rowdot = 0.f;
+            // dGeLU: this row's 64 pre-activation values are loaded before the TMEM reads so the
+            // two latencies overlap (the epilogue bounds the dgrad GEMM's tensor-pipe activity)
+            uint4 auxv[2][4];
+            if constexpr (EPI == EPI_DGELU) {
+              const uint4* h4 = reinterpret_cast<const uint4*>(p.aux + static_cast<size_t>(row) * p.ldaux + nb * BN +
+                                                               c2 * 64);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) auxv[j / 4][j % 4] = h4[j];
+            }
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
               const int c = 2 * c2 + hh;
@@ -333,10 +342,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
               }
               if constexpr (EPI == EPI_DGELU) {
-                const uint4* h4 = reinterpret_cast<const uint4*>(p.aux + static_cast<size_t>(row) * p.ldaux + n);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                  uint4 hv = h4[j];
+                  const uint4 hv = auxv[hh][j];
                   uint32_t w[4] = {hv.x, hv.y, hv.z, hv.w};
 #pragma unroll
                   for (int e = 0; e < 4; ++e) {
