@@ -443,6 +443,38 @@ __global__ void __launch_bounds__(256) ln_bwd_fused_kernel(LnBwdArgs a, DropDev 
 // from HBM). Partials: ws[gridDim.x][3][d], reduced by reduce_partials_kernel in fixed order.
 constexpr int kLnStages = 3;
 
+// Paired fp32 arithmetic (sm_100 FFMA2 / FMUL2 / FADD2: two fp32 lanes per instruction). The
+// LayerNorm backward is instruction-bound at d = 2048, so its per-element math runs in pairs.
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2unpack(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2mul(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// two packed bf16 -> an fp32 pair
+__device__ __forceinline__ uint64_t bf2_to_f2(uint32_t w) {
+  return f2pack(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+}
+
 template <int R, int NG>
 __global__ void __launch_bounds__(256, 2) ln_bwd_stream_kernel(LnBwdArgs a, DropDev dr, float* __restrict__ ws,
                                                               int nslabs, int nst) {
@@ -476,13 +508,21 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_stream_kernel(LnBwdArgs a, Drop
     fence_mbar_init();
     for (int i = 0; i < nst && i < my; ++i) issue(i);
   }
-  float g[NG][8], ag[NG][8], ab[NG][8], as[NG][8];
+  uint64_t g2[NG][4], AG[NG][4], AB[NG][4];  // gamma and the dgamma / dbeta partials, fp32 pairs
+  float as[NG][8];
 #pragma unroll
   for (int k = 0; k < NG; ++k) {
     const int c0 = tid * 8 + k * 2048;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) ag[k][i] = ab[k][i] = as[k][i] = g[k][i] = 0.f;
-    if (c0 < d) unpack8(*reinterpret_cast<const uint4*>(a.gamma + c0), g[k]);
+    for (int i = 0; i < 8; ++i) as[k][i] = 0.f;
+    uint4 gv = make_uint4(0u, 0u, 0u, 0u);
+    if (c0 < d) gv = *reinterpret_cast<const uint4*>(a.gamma + c0);
+    const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w};
+#pragma unroll
+    for (int e2 = 0; e2 < 4; ++e2) {
+      g2[k][e2] = bf2_to_f2(gw[e2]);
+      AG[k][e2] = AB[k][e2] = f2pack(0.f, 0.f);
+    }
   }
   __syncthreads();
   const int pr = warp / W, psub = warp % W;
@@ -495,19 +535,23 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_stream_kernel(LnBwdArgs a, Drop
     {  // pass 1: row reductions
       const int row = row0 + pr;
       const float mu = a.mean[row], rs = a.rstd[row];
-      float s1 = 0.f, s2 = 0.f;
+      const uint64_t RS = f2pack(rs, rs), NMR = f2pack(-mu * rs, -mu * rs);
+      uint64_t S1 = f2pack(0.f, 0.f), S2 = S1;
       for (int c0 = (psub * 32 + lane) * 8; c0 < d; c0 += W * 256) {
-        float x[8], dy[8], gg[8];
-        unpack8(*reinterpret_cast<const uint4*>(xs + pr * d + c0), x);
-        unpack8(*reinterpret_cast<const uint4*>(dys + pr * d + c0), dy);
-        unpack8(*reinterpret_cast<const uint4*>(a.gamma + c0), gg);
+        const uint4 xv = *reinterpret_cast<const uint4*>(xs + pr * d + c0);
+        const uint4 dv = *reinterpret_cast<const uint4*>(dys + pr * d + c0);
+        const uint4 gv = *reinterpret_cast<const uint4*>(a.gamma + c0);
+        const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w}, dw[4] = {dv.x, dv.y, dv.z, dv.w};
+        const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w};
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float gy = dy[e] * gg[e];
-          s1 += gy;
-          s2 += gy * (x[e] - mu) * rs;
+        for (int e2 = 0; e2 < 4; ++e2) {
+          const uint64_t GY = f2mul(bf2_to_f2(dw[e2]), bf2_to_f2(gw[e2]));
+          S1 = f2add(S1, GY);
+          S2 = f2fma(GY, f2fma(bf2_to_f2(xw[e2]), RS, NMR), S2);
         }
       }
+      const float2 s1p = f2unpack(S1), s2p = f2unpack(S2);
+      float s1 = s1p.x + s1p.y, s2 = s2p.x + s2p.y;
       for (int off = 16; off; off >>= 1) {
         s1 += __shfl_xor_sync(0xffffffff, s1, off);
         s2 += __shfl_xor_sync(0xffffffff, s2, off);
@@ -539,18 +583,27 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_stream_kernel(LnBwdArgs a, Drop
         m2 /= d;
         const float mu = smu[r], rs = srs[r];
         const size_t o = static_cast<size_t>(row0 + r) * d + c0;
-        float x[8], dy[8], dx[8], rg[8];
-        unpack8(*reinterpret_cast<const uint4*>(xs + r * d + c0), x);
-        unpack8(*reinterpret_cast<const uint4*>(dys + r * d + c0), dy);
-        if (a.resid_grad) unpack8(*reinterpret_cast<const uint4*>(srg(st) + r * d + c0), rg);
+        // dx = rs * (dy*g - xh*m2) - m1*rs, xh = x*rs - mu*rs; dgamma += dy*xh, dbeta += dy
+        const uint64_t RS = f2pack(rs, rs), NMR = f2pack(-mu * rs, -mu * rs), NM2 = f2pack(-m2, -m2);
+        const uint64_t NM1RS = f2pack(-m1 * rs, -m1 * rs);
+        const uint4 xv = *reinterpret_cast<const uint4*>(xs + r * d + c0);
+        const uint4 dv = *reinterpret_cast<const uint4*>(dys + r * d + c0);
+        uint4 rv = make_uint4(0u, 0u, 0u, 0u);
+        if (a.resid_grad) rv = *reinterpret_cast<const uint4*>(srg(st) + r * d + c0);
+        const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w}, dw[4] = {dv.x, dv.y, dv.z, dv.w};
+        const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
+        float dx[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float xh = (x[e] - mu) * rs;
-          dx[e] = rs * (dy[e] * g[k][e] - m1 - xh * m2);
-          ag[k][e] += dy[e] * xh;
-          ab[k][e] += dy[e];
-          if (a.resid_grad) dx[e] += rg[e];
-          dx[e] = round_bf16(dx[e]);
+        for (int e2 = 0; e2 < 4; ++e2) {
+          const uint64_t DY = bf2_to_f2(dw[e2]);
+          const uint64_t XH = f2fma(bf2_to_f2(xw[e2]), RS, NMR);
+          uint64_t DX = f2fma(f2fma(XH, NM2, f2mul(DY, g2[k][e2])), RS, NM1RS);
+          AG[k][e2] = f2fma(DY, XH, AG[k][e2]);
+          AB[k][e2] = f2add(AB[k][e2], DY);
+          if (a.resid_grad) DX = f2add(DX, bf2_to_f2(rw[e2]));
+          const float2 dxp = f2unpack(DX);
+          dx[2 * e2] = round_bf16(dxp.x);
+          dx[2 * e2 + 1] = round_bf16(dxp.y);
         }
         if (a.dx) *reinterpret_cast<uint4*>(a.dx + o) = pack8(dx);
         float od[8];
@@ -575,10 +628,19 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_stream_kernel(LnBwdArgs a, Drop
     const int c0 = tid * 8 + k * 2048;
     if (c0 >= d) continue;
     float* w = ws + static_cast<size_t>(blockIdx.x) * 3 * d;
-    *reinterpret_cast<float4*>(w + c0) = make_float4(ag[k][0], ag[k][1], ag[k][2], ag[k][3]);
-    *reinterpret_cast<float4*>(w + c0 + 4) = make_float4(ag[k][4], ag[k][5], ag[k][6], ag[k][7]);
-    *reinterpret_cast<float4*>(w + d + c0) = make_float4(ab[k][0], ab[k][1], ab[k][2], ab[k][3]);
-    *reinterpret_cast<float4*>(w + d + c0 + 4) = make_float4(ab[k][4], ab[k][5], ab[k][6], ab[k][7]);
+    float ag[8], ab[8];
+#pragma unroll
+    for (int e2 = 0; e2 < 4; ++e2) {
+      const float2 gp = f2unpack(AG[k][e2]), bp = f2unpack(AB[k][e2]);
+      ag[2 * e2] = gp.x;
+      ag[2 * e2 + 1] = gp.y;
+      ab[2 * e2] = bp.x;
+      ab[2 * e2 + 1] = bp.y;
+    }
+    *reinterpret_cast<float4*>(w + c0) = make_float4(ag[0], ag[1], ag[2], ag[3]);
+    *reinterpret_cast<float4*>(w + c0 + 4) = make_float4(ag[4], ag[5], ag[6], ag[7]);
+    *reinterpret_cast<float4*>(w + d + c0) = make_float4(ab[0], ab[1], ab[2], ab[3]);
+    *reinterpret_cast<float4*>(w + d + c0 + 4) = make_float4(ab[4], ab[5], ab[6], ab[7]);
     *reinterpret_cast<float4*>(w + 2 * d + c0) = make_float4(as[k][0], as[k][1], as[k][2], as[k][3]);
     *reinterpret_cast<float4*>(w + 2 * d + c0 + 4) = make_float4(as[k][4], as[k][5], as[k][6], as[k][7]);
   }
