@@ -21,6 +21,39 @@ namespace {
 using namespace rowops;
 using namespace ptx;
 
+// Paired fp32 arithmetic (sm_100 FFMA2 / FMUL2 / FADD2: two fp32 lanes per instruction). The
+// LayerNorm backward is instruction-bound at d = 2048, so its per-element math runs in pairs.
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2unpack(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2mul(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// two packed bf16 -> an fp32 pair
+__device__ __forceinline__ uint64_t bf2_to_f2(uint32_t w) {
+  return f2pack(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+}
+
+
 // vectors-per-thread choice: threads = (d/8)/vpt, a multiple of 32 and <= 1024
 int pick_vpt(int d) {
   const int nvec = d / 8;
@@ -125,7 +158,7 @@ __global__ void __launch_bounds__(256, 2) resid_ln_warp_kernel(ResidLnArgs a, Dr
     hp[v] = *reinterpret_cast<const uint4*>(rsrc + c0);
     if (a.y) yv[v] = *reinterpret_cast<const uint4*>(a.y + roff + c0);
   }
-  float sum = 0.f;
+  uint64_t S = f2pack(0.f, 0.f);  // running row sum, fp32 pair
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
     const int c0 = (v * 32 + lane) * 8;
@@ -156,40 +189,50 @@ __global__ void __launch_bounds__(256, 2) resid_ln_warp_kernel(ResidLnArgs a, Dr
       hp[v] = pack8(r);
       if (a.h_out) *reinterpret_cast<uint4*>(a.h_out + roff + c0) = hp[v];
     }
-    float h[8];
-    unpack8(hp[v], h);
+    const uint32_t hw[4] = {hp[v].x, hp[v].y, hp[v].z, hp[v].w};
 #pragma unroll
-    for (int i = 0; i < 8; ++i) sum += h[i];
+    for (int e2 = 0; e2 < 4; ++e2) S = f2add(S, bf2_to_f2(hw[e2]));
   }
   if (!a.gamma) return;
+  const float2 sp = f2unpack(S);
+  float sum = sp.x + sp.y;
   for (int off = 16; off; off >>= 1) sum += __shfl_xor_sync(0xffffffff, sum, off);
   const float mean = sum / d;
-  float q = 0.f;
+  const uint64_t NMEAN = f2pack(-mean, -mean);
+  uint64_t Q = f2pack(0.f, 0.f);
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
-    float h[8];
-    unpack8(hp[v], h);
+    const uint32_t hw[4] = {hp[v].x, hp[v].y, hp[v].z, hp[v].w};
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float t = h[i] - mean;
-      q += t * t;
+    for (int e2 = 0; e2 < 4; ++e2) {
+      const uint64_t T = f2add(bf2_to_f2(hw[e2]), NMEAN);
+      Q = f2fma(T, T, Q);
     }
   }
+  const float2 qp = f2unpack(Q);
+  float q = qp.x + qp.y;
   for (int off = 16; off; off >>= 1) q += __shfl_xor_sync(0xffffffff, q, off);
   const float rstd = rsqrtf(q / d + 1e-5f);
   if (lane == 0) {
     a.mean[row] = mean;
     a.rstd[row] = rstd;
   }
+  const uint64_t RS = f2pack(rstd, rstd), NMR = f2pack(-mean * rstd, -mean * rstd);
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
     const int c0 = (v * 32 + lane) * 8;
-    float h[8], g[8], b[8], o[8];
-    unpack8(hp[v], h);
-    unpack8(*reinterpret_cast<const uint4*>(a.gamma + c0), g);
-    unpack8(*reinterpret_cast<const uint4*>(a.beta + c0), b);
+    const uint4 gv = *reinterpret_cast<const uint4*>(a.gamma + c0);
+    const uint4 bv = *reinterpret_cast<const uint4*>(a.beta + c0);
+    const uint32_t hw[4] = {hp[v].x, hp[v].y, hp[v].z, hp[v].w};
+    const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w}, bw[4] = {bv.x, bv.y, bv.z, bv.w};
+    float o[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) o[i] = (h[i] - mean) * rstd * g[i] + b[i];
+    for (int e2 = 0; e2 < 4; ++e2) {  // (h*rstd - mean*rstd) * g + b
+      const uint64_t O = f2fma(f2fma(bf2_to_f2(hw[e2]), RS, NMR), bf2_to_f2(gw[e2]), bf2_to_f2(bw[e2]));
+      const float2 op = f2unpack(O);
+      o[2 * e2] = op.x;
+      o[2 * e2 + 1] = op.y;
+    }
     *reinterpret_cast<uint4*>(a.ln_out + roff + c0) = pack8(o);
   }
 }
@@ -442,38 +485,6 @@ __global__ void __launch_bounds__(256) ln_bwd_fused_kernel(LnBwdArgs a, DropDev 
 // 32-row fused form re-reads them from L2 and, with ~1000 resident slabs = 256 MB > L2, partly
 // from HBM). Partials: ws[gridDim.x][3][d], reduced by reduce_partials_kernel in fixed order.
 constexpr int kLnStages = 3;
-
-// Paired fp32 arithmetic (sm_100 FFMA2 / FMUL2 / FADD2: two fp32 lanes per instruction). The
-// LayerNorm backward is instruction-bound at d = 2048, so its per-element math runs in pairs.
-__device__ __forceinline__ uint64_t f2pack(float a, float b) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ float2 f2unpack(uint64_t v) {
-  float2 r;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
-  return r;
-}
-__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ uint64_t f2mul(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ uint64_t f2add(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-// two packed bf16 -> an fp32 pair
-__device__ __forceinline__ uint64_t bf2_to_f2(uint32_t w) {
-  return f2pack(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
-}
 
 template <int R, int NG>
 __global__ void __launch_bounds__(256, 2) ln_bwd_stream_kernel(LnBwdArgs a, DropDev dr, float* __restrict__ ws,
