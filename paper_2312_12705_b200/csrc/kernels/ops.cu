@@ -520,19 +520,17 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_stream_kernel(LnBwdArgs a, Drop
     for (int i = 0; i < nst && i < my; ++i) issue(i);
   }
   uint64_t g2[NG][4], AG[NG][4], AB[NG][4];  // gamma and the dgamma / dbeta partials, fp32 pairs
-  float as[NG][8];
+  uint64_t AS[NG][4];  // dbias partials
 #pragma unroll
   for (int k = 0; k < NG; ++k) {
     const int c0 = tid * 8 + k * 2048;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) as[k][i] = 0.f;
     uint4 gv = make_uint4(0u, 0u, 0u, 0u);
     if (c0 < d) gv = *reinterpret_cast<const uint4*>(a.gamma + c0);
     const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w};
 #pragma unroll
     for (int e2 = 0; e2 < 4; ++e2) {
       g2[k][e2] = bf2_to_f2(gw[e2]);
-      AG[k][e2] = AB[k][e2] = f2pack(0.f, 0.f);
+      AG[k][e2] = AB[k][e2] = AS[k][e2] = f2pack(0.f, 0.f);
     }
   }
   __syncthreads();
@@ -603,7 +601,7 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_stream_kernel(LnBwdArgs a, Drop
         if (a.resid_grad) rv = *reinterpret_cast<const uint4*>(srg(st) + r * d + c0);
         const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w}, dw[4] = {dv.x, dv.y, dv.z, dv.w};
         const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
-        float dx[8];
+        uint32_t dxw[4];
 #pragma unroll
         for (int e2 = 0; e2 < 4; ++e2) {
           const uint64_t DY = bf2_to_f2(dw[e2]);
@@ -613,21 +611,24 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_stream_kernel(LnBwdArgs a, Drop
           AB[k][e2] = f2add(AB[k][e2], DY);
           if (a.resid_grad) DX = f2add(DX, bf2_to_f2(rw[e2]));
           const float2 dxp = f2unpack(DX);
-          dx[2 * e2] = round_bf16(dxp.x);
-          dx[2 * e2 + 1] = round_bf16(dxp.y);
+          dxw[e2] = pack_bf16(dxp.x, dxp.y);  // round-to-nearest bf16 pair (what is stored)
         }
-        if (a.dx) *reinterpret_cast<uint4*>(a.dx + o) = pack8(dx);
-        float od[8];
-        const uint32_t kb = dr.on ? keep8(dr, static_cast<int64_t>(o)) : 0xFFu;
+        if (a.dx) *reinterpret_cast<uint4*>(a.dx + o) = make_uint4(dxw[0], dxw[1], dxw[2], dxw[3]);
+        uint32_t odw[4] = {dxw[0], dxw[1], dxw[2], dxw[3]};
+        if (dr.on) {
+          const uint32_t kb = keep8(dr, static_cast<int64_t>(o));
 #pragma unroll
-        for (int e = 0; e < 8; ++e) od[e] = dr.on ? ((kb >> e) & 1u ? dx[e] * dr.scale : 0.f) : dx[e];
-        const uint4 q = pack8(od);
-        if (a.dxd && (dr.on || a.dxd != a.dx)) *reinterpret_cast<uint4*>(a.dxd + o) = q;
-        if (a.dbias) {
-          float qv[8];  // bias grad sums the bf16 values that were stored
-          unpack8(q, qv);
+          for (int e2 = 0; e2 < 4; ++e2) {
+            const float2 f = unpack_bf16(dxw[e2]);
+            odw[e2] = pack_bf16((kb >> (2 * e2)) & 1u ? f.x * dr.scale : 0.f,
+                                (kb >> (2 * e2 + 1)) & 1u ? f.y * dr.scale : 0.f);
+          }
+        }
+        if (a.dxd && (dr.on || a.dxd != a.dx))
+          *reinterpret_cast<uint4*>(a.dxd + o) = make_uint4(odw[0], odw[1], odw[2], odw[3]);
+        if (a.dbias) {  // bias grad sums the bf16 values that were stored
 #pragma unroll
-          for (int e = 0; e < 8; ++e) as[k][e] += qv[e];
+          for (int e2 = 0; e2 < 4; ++e2) AS[k][e2] = f2add(AS[k][e2], bf2_to_f2(odw[e2]));
         }
       }
     }
@@ -639,21 +640,23 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_stream_kernel(LnBwdArgs a, Drop
     const int c0 = tid * 8 + k * 2048;
     if (c0 >= d) continue;
     float* w = ws + static_cast<size_t>(blockIdx.x) * 3 * d;
-    float ag[8], ab[8];
+    float ag[8], ab[8], as[8];
 #pragma unroll
     for (int e2 = 0; e2 < 4; ++e2) {
-      const float2 gp = f2unpack(AG[k][e2]), bp = f2unpack(AB[k][e2]);
+      const float2 gp = f2unpack(AG[k][e2]), bp = f2unpack(AB[k][e2]), sp = f2unpack(AS[k][e2]);
       ag[2 * e2] = gp.x;
       ag[2 * e2 + 1] = gp.y;
       ab[2 * e2] = bp.x;
       ab[2 * e2 + 1] = bp.y;
+      as[2 * e2] = sp.x;
+      as[2 * e2 + 1] = sp.y;
     }
     *reinterpret_cast<float4*>(w + c0) = make_float4(ag[0], ag[1], ag[2], ag[3]);
     *reinterpret_cast<float4*>(w + c0 + 4) = make_float4(ag[4], ag[5], ag[6], ag[7]);
     *reinterpret_cast<float4*>(w + d + c0) = make_float4(ab[0], ab[1], ab[2], ab[3]);
     *reinterpret_cast<float4*>(w + d + c0 + 4) = make_float4(ab[4], ab[5], ab[6], ab[7]);
-    *reinterpret_cast<float4*>(w + 2 * d + c0) = make_float4(as[k][0], as[k][1], as[k][2], as[k][3]);
-    *reinterpret_cast<float4*>(w + 2 * d + c0 + 4) = make_float4(as[k][4], as[k][5], as[k][6], as[k][7]);
+    *reinterpret_cast<float4*>(w + 2 * d + c0) = make_float4(as[0], as[1], as[2], as[3]);
+    *reinterpret_cast<float4*>(w + 2 * d + c0 + 4) = make_float4(as[4], as[5], as[6], as[7]);
   }
 }
 
