@@ -34,6 +34,7 @@ extern "C" {
 #define TP_ERR_NCCL 4
 #define TP_ERR_INTERNAL 5
 #define TP_ERR_UNSUPPORTED 6
+#define TP_ERR_TIMEOUT 7 /* watchdog: a host wait exceeded the session timeout; communicators aborted */
 
 /* Last error message of the calling thread ("" when none). */
 const char* tp_last_error(void);
@@ -209,6 +210,34 @@ typedef struct tp_kernel_times {
 /* Runs `steps` iterations on the uploaded tokens between two CUDA events on the session stream;
  * *ms = device time. With profile != 0 every launch is bracketed by events into *kt. */
 int tp_session_time_steps(tp_session* s, int steps, int profile, float* ms, tp_kernel_times* kt);
+/* Watchdog for every host wait of the session (sync, loss read, timed steps): after `seconds`
+ * without progress the session aborts its NCCL communicators (ncclCommAbort) and the call returns
+ * TP_ERR_TIMEOUT (trainplan::FailureKind::Timeout, search.hpp:59); the session is unusable
+ * afterwards and the process should exit (a kernel spinning on a dead peer cannot be cancelled).
+ * seconds <= 0 waits forever. Default: $GPTB200_TIMEOUT_S, else 0. */
+int tp_session_set_timeout(tp_session* s, double seconds);
+
+/* Measured per-GPU footprint of the session in the categories of trainplan::MemoryReport
+ * (memory.hpp:47-55): params = bf16 working copy + fp32 master (ZeRO shard), gradients = fp32
+ * main grads, optimizer = Adam m + v (ZeRO shard), activations = stored / recomputed per-microbatch
+ * tensors, workspace = per-op scratch; window = the NVLS symmetric window (TP > 1; the buffers
+ * carved from it are also counted in their category); total = all device allocations + window. */
+typedef struct tp_memory_report {
+  uint64_t params_bytes, gradient_bytes, optimizer_bytes, activation_bytes, workspace_bytes;
+  uint64_t window_bytes, total_bytes;
+  int zero_stage; /* in effect: 1 sharded optimizer state, 0 replicated */
+} tp_memory_report;
+int tp_session_memory(tp_session* s, tp_memory_report* out);
+
+/* Process-wide launch-variant counters of the kernel dispatchers (all sessions and devices):
+ * 0 GEMM single-CTA tiles, 1 GEMM CTA-pair 256x256, 2 GEMM CTA-pair 256x512, 3 K-sliced fp32
+ * GEMM, 4 attention fwd persistent, 5 attention fwd per-block, 6 attention bwd per-block,
+ * 7 attention bwd persistent, 8 attention bwd hd 64, 9 attention bwd hd 160, 10 LayerNorm bwd
+ * persistent bulk-copy, 11 LayerNorm bwd 32-row fused, 12 LayerNorm bwd two-pass. */
+#define TP_KERNEL_VARIANTS 13
+int tp_variant_counts(int64_t out[TP_KERNEL_VARIANTS]);
+int tp_variant_counts_reset(void);
+
 /* Max over all ranks of *v (NCCL on the world communicator); identity when world == 1. */
 int tp_session_allreduce_max(tp_session* s, float* v);
 /* TP allreduce of one [mbs*s, d] bf16 activation buffer (the Megatron f/g operator), for tests and

@@ -10,11 +10,15 @@
 #include <array>
 #include <cstdint>
 #include <optional>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "trainplan/b200.hpp"
 #include "trainplan/capi.h"
-#include "trainplan/core.hpp"
+#include "trainplan/memory.hpp"
+#include "trainplan/perf.hpp"
+#include "trainplan/search.hpp"
 
 namespace trainplan {
 
@@ -33,9 +37,17 @@ struct DistributedContext {
 
 std::array<unsigned char, 128> nccl_unique_id();
 
+// A host wait of the session exceeded its watchdog timeout (TP_ERR_TIMEOUT): the NCCL
+// communicators were aborted and the session is unusable; the process should exit. Maps to
+// FailureKind::Timeout (search.hpp:59) in the measured evaluator.
+class StepTimeout : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
 // RAII owner of one rank's train-step session. Throws std::invalid_argument for an invalid
-// configuration and std::runtime_error for CUDA/NCCL failures; std::bad_alloc when the
-// configuration does not fit in HBM.
+// configuration, std::bad_alloc when the configuration does not fit in HBM, StepTimeout when the
+// watchdog fires and std::runtime_error for other CUDA/NCCL failures.
 class TrainSession {
  public:
   TrainSession(const ModelSpec& model, const ParallelConfig& cfg, const TrainOptions& opts = {},
@@ -54,6 +66,13 @@ class TrainSession {
   // Device time (ms) of `steps` iterations; per-kernel-class timing when kt != nullptr.
   float time_steps(int steps, tp_kernel_times* kt = nullptr);
   float allreduce_max(float v);
+  // Watchdog for host waits (seconds <= 0: none); see tp_session_set_timeout.
+  void set_timeout(double seconds);
+  // MEASURED per-GPU footprint in the categories of the reference's MemoryReport (memory.hpp):
+  // params = bf16 working copy + fp32 master (ZeRO shard), gradients = fp32 main grads, optimizer
+  // = Adam m + v (ZeRO shard), activations = stored / recomputed per-microbatch tensors,
+  // overhead = per-op workspace + the unused part of the NVLS window; fits vs mem_per_gpu.
+  MemoryReport memory_report(std::uint64_t mem_per_gpu = 0);
   tp_session* handle() { return s_; }
 
  private:
@@ -63,29 +82,44 @@ class TrainSession {
 struct MeasureOptions {
   int warmup = 3;
   int steps = 5;
+  double timeout_s = 0.0;  // watchdog for every host wait (0: none)
   TrainOptions train;
   DistributedContext dist;
 };
 
 // Measured counterpart of estimate(): validates like estimate() (std::invalid_argument on an
-// invalid configuration; OOM is a reported state, est.oom = true), runs warmup + timed steps on
+// invalid configuration; OOM anywhere — allocation, init, steps — is a reported state, est.oom =
+// true; StepTimeout when the watchdog fires), runs warmup + timed steps on
 // synthetic tokens (std::mt19937_64(seed), uniform over the vocabulary) and fills
 //   iter_time      device seconds per iteration (max over ranks)
 //   flops_per_gpu  model_flops_per_iteration(model, gbs, ckpt) / (iter_time * world)
 //   peak_fraction  flops_per_gpu / cluster.peak_flops_per_gpu
-//   breakdown      compute / tp_comm / pp_comm / dp_comm from CUDA events around every launch,
+//   breakdown      compute / tp_comm / pp_comm from CUDA events around every launch on the step
+//                  stream; dp_comm = the EXPOSED data-parallel tail (the step waiting for the
+//                  comm-stream reduce-scatter / Adam / allgather pipeline after the last
+//                  backward op; the DP collectives themselves overlap the backward, so the
+//                  reference's serial dp_time, perf.cpp:88-102, is an upper bound of this);
 //                  bubble = iter_time - the rest (pipeline idle + launch gaps)
 // Multi-GPU: every rank calls measure() with its DistributedContext.
 ThroughputEstimate measure(const ModelSpec& model, const ParallelConfig& cfg, const ClusterSpec& cluster,
                            const MeasureOptions& opts = {});
+
+// Allocates the session for (model, cfg) on this process's GPU without running a step and
+// returns its measured footprint (TrainSession::memory_report); fits = false and all-zero bytes
+// when it does not fit (the allocation failed). Compare with memory_per_gpu (the model).
+MemoryReport measured_memory_per_gpu(const ModelSpec& model, const ParallelConfig& cfg, const ClusterSpec& cluster,
+                                     const DistributedContext& dist = {});
 
 // The configuration a search point denotes (reference semantics, perf.cpp:161-181: gbs = mbs *
 // gas * dp, activation checkpointing and flash attention on) computed in bf16.
 std::optional<ParallelConfig> measured_config_from_point(const SearchPoint& point, const ClusterSpec& cluster);
 
 // Evaluator that runs the point on this process's GPU(s) instead of modelling it: Invalid for
-// configurations that do not factor or validate, Oom when they do not fit, objective = measured
-// model TFLOPS/GPU. Not thread-safe: use run_search(..., workers = 1).
+// configurations that do not factor or validate (including the kernels' constraints) or fail to
+// run, Oom when they do not fit, Timeout when the watchdog (opts.timeout_s) fires; objective =
+// measured model TFLOPS/GPU; wall_time = host seconds spent on the point. zero1 = false runs
+// replicated data parallelism (ZeRO-0: gradient allreduce, full optimizer state per rank).
+// Not thread-safe: use run_search(..., workers = 1).
 Evaluator make_measured_evaluator(const ModelSpec& model, const ClusterSpec& cluster,
                                   const MeasureOptions& opts = {});
 

@@ -108,12 +108,42 @@ SIGNATURES: dict[str, tuple] = {
     "tp_session_allreduce_max": (_i, [_vp, C.POINTER(_f)]),
     "tp_session_debug_tp_allreduce": (_i, [_vp, _vp, _vp, _i]),
     "tp_session_bench_tp_allreduce": (_i, [_vp, _i, _i, _i, C.POINTER(_f), C.POINTER(_i)]),
+    "tp_session_set_timeout": (_i, [_vp, C.c_double]),
+    "tp_session_memory": (_i, [_vp, _vp]),
+    "tp_variant_counts": (_i, [C.POINTER(_i64)]),
+    "tp_variant_counts_reset": (_i, []),
     "tp_ncu_parse_csv": (_i, [C.c_char_p, C.c_size_t, C.c_char_p, _vp]),
     "tp_ncu_metric_list": (_i, [C.c_char_p, C.c_size_t]),
     "tp_diagnose_mbs_mismatch": (_i, [C.c_double, C.c_double, _i, _i, C.POINTER(_i), C.POINTER(C.c_double),
                                       C.c_char_p, C.c_size_t]),
 }
 
+
+
+class MemoryReport(C.Structure):
+    """tp_memory_report (capi.h): measured per-category device bytes of a session."""
+    _fields_ = [("params_bytes", _u64), ("gradient_bytes", _u64), ("optimizer_bytes", _u64),
+                ("activation_bytes", _u64), ("workspace_bytes", _u64), ("window_bytes", _u64),
+                ("total_bytes", _u64), ("zero_stage", _i)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+VARIANTS = ["gemm_single", "gemm_pair_256", "gemm_pair_512", "gemm_ksplit", "attn_fwd_persistent",
+            "attn_fwd_per_block", "attn_bwd_per_block", "attn_bwd_persistent", "attn_bwd_hd64",
+            "attn_bwd_hd160", "ln_bwd_stream", "ln_bwd_fused", "ln_bwd_two_pass"]
+
+
+def variant_counts() -> dict:
+    """Process-wide launch counts per kernel variant (tp_variant_counts)."""
+    out = (_i64 * len(VARIANTS))()
+    check(load().tp_variant_counts(out))
+    return dict(zip(VARIANTS, list(out)))
+
+
+def variant_counts_reset() -> None:
+    check(load().tp_variant_counts_reset())
 
 
 class HwCounters(C.Structure):
@@ -366,6 +396,14 @@ class Session:
         n = _i()
         check(self._lib.tp_session_buckets(self.h, buf, 4096, C.byref(n)))
         return [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]) for i in range(n.value)]
+
+    def set_timeout(self, seconds: float) -> None:
+        check(self._lib.tp_session_set_timeout(self.h, float(seconds)))
+
+    def memory(self) -> dict:
+        rep = MemoryReport()
+        check(self._lib.tp_session_memory(self.h, C.byref(rep)))
+        return rep.as_dict()
 
     def info(self) -> dict:
         out = (_i64 * 8)()

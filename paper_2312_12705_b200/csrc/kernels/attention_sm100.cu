@@ -1486,13 +1486,8 @@ template <int HD>
 int bwd_tc2(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* D,
             float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st) {
   using Cfg = TcBwd2Cfg<HD>;
-  static bool init = false;
-  if (!init) {
-    if (cudaFuncSetAttribute(fa_bwd_tc2_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
-        cudaSuccess)
-      return 3;
-    init = true;
-  }
+  if (ensure_dynamic_smem(reinterpret_cast<const void*>(fa_bwd_tc2_kernel<HD>), Cfg::kSmem) != 0) return 3;
+  count_variant(KV_ATTN_BWD_PER_BLOCK);
   const int dt = a.heads * HD;
   const uint64_t M = static_cast<uint64_t>(a.batch) * a.seq;
   CUtensorMap tkv, tq, tdo;
@@ -1510,13 +1505,8 @@ template <int HD>
 int bwd_tc2_persistent(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse,
                        const float* D, float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st) {
   using Cfg = TcBwd2Cfg<HD>;
-  static bool init = false;
-  if (!init) {
-    if (cudaFuncSetAttribute(fa_bwd_tc2_persistent<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
-        cudaSuccess)
-      return 3;
-    init = true;
-  }
+  if (ensure_dynamic_smem(reinterpret_cast<const void*>(fa_bwd_tc2_persistent<HD>), Cfg::kSmem) != 0) return 3;
+  count_variant(KV_ATTN_BWD_PERSISTENT);
   const int dt = a.heads * HD;
   const uint64_t M = static_cast<uint64_t>(a.batch) * a.seq;
   CUtensorMap tkv, tq, tdo;
@@ -1535,13 +1525,8 @@ template <int HD>
 int bwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* D,
            float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st) {
   using Cfg = TcBwdCfg<HD>;
-  static bool init = false;
-  if (!init) {
-    if (cudaFuncSetAttribute(fa_bwd_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
-        cudaSuccess)
-      return 3;
-    init = true;
-  }
+  if (ensure_dynamic_smem(reinterpret_cast<const void*>(fa_bwd_tc_kernel<HD>), Cfg::kSmem) != 0) return 3;
+  count_variant(KV_ATTN_BWD_HD64);
   const int dt = a.heads * HD;
   const uint64_t M = static_cast<uint64_t>(a.batch) * a.seq;
   CUtensorMap tq, tdo;
@@ -1557,13 +1542,8 @@ int bwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* do
 template <int HD>
 int fwd_tc_persistent(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, cudaStream_t st) {
   using Cfg = TcFwdCfg<HD>;
-  static bool init = false;
-  if (!init) {
-    if (cudaFuncSetAttribute(fa_fwd_tc_persistent<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
-        cudaSuccess)
-      return 3;
-    init = true;
-  }
+  if (ensure_dynamic_smem(reinterpret_cast<const void*>(fa_fwd_tc_persistent<HD>), Cfg::kSmem) != 0) return 3;
+  count_variant(KV_ATTN_FWD_PERSISTENT);
   const int dt = a.heads * HD;
   CUtensorMap tm;
   if (!make_tmap_bf16(&tm, qkv, 3 * static_cast<uint64_t>(dt), static_cast<uint64_t>(a.batch) * a.seq, 3 * dt, 64, 128))
@@ -1578,13 +1558,8 @@ int fwd_tc_persistent(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat1
 template <int HD>
 int fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, cudaStream_t st) {
   using Cfg = TcFwdCfg<HD>;
-  static bool init = false;
-  if (!init) {
-    if (cudaFuncSetAttribute(fa_fwd_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
-        cudaSuccess)
-      return 3;
-    init = true;
-  }
+  if (ensure_dynamic_smem(reinterpret_cast<const void*>(fa_fwd_tc_kernel<HD>), Cfg::kSmem) != 0) return 3;
+  count_variant(KV_ATTN_FWD_PER_BLOCK);
   const int dt = a.heads * HD;
   CUtensorMap tm;
   if (!make_tmap_bf16(&tm, qkv, 3 * static_cast<uint64_t>(dt), static_cast<uint64_t>(a.batch) * a.seq, 3 * dt, 64, 128))

@@ -540,13 +540,9 @@ template <int BN, int CG, bool A_MN, bool B_MN, int EPI>
 int launch(const GemmParams& p, cudaStream_t stream) {
   using Cfg = GemmCfg<BN, CG>;
   auto kern = gemm_sm100_kernel<BN, CG, A_MN, B_MN, EPI>;
-  static bool attr_set = false;  // per instantiation; set once per process (single device)
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Cfg::kSmemBytes) != cudaSuccess)
-      return kGemmErrCuda;
-    attr_set = true;
-  }
+  if (ensure_dynamic_smem(reinterpret_cast<const void*>(kern), Cfg::kSmemBytes) != 0) return kGemmErrCuda;
+  count_variant(CG == 1 ? KV_GEMM_SINGLE : (BN == 512 ? KV_GEMM_PAIR_512 : KV_GEMM_PAIR_256));
+  if (p.split_k > 1) count_variant(KV_GEMM_KSPLIT);
   CUtensorMap ta, tb;
   bool ok = A_MN ? make_tmap(&ta, p.A, p.M, p.K, p.lda, 64)
                  : make_tmap(&ta, p.A, p.K, p.M, p.lda, kBM);

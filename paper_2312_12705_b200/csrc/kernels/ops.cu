@@ -13,6 +13,7 @@
 #include "rowops.cuh"
 #include "pdl.cuh"
 #include "sm100_ptx.cuh"
+#include "tma_host.h"
 
 namespace gptb200 {
 
@@ -961,15 +962,7 @@ __global__ void accumulate_sum_kernel(const float* __restrict__ x, int n, float*
   if (threadIdx.x == 0) *acc += v[0];
 }
 
-int device_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return n;
-}
+int device_sms() { return device_sm_count(); }
 
 int grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
@@ -1032,13 +1025,12 @@ int ln_bwd(const LnBwdArgs& a, cudaStream_t st) {
     const int ntens = a.resid_grad ? 3 : 2;
     const int nst = a.resid_grad ? 2 : 3;
     const size_t smem = static_cast<size_t>(nst) * ntens * R * a.d * 2;
-    static bool attr_set = false;
-    if (!attr_set) {  // the largest ring either variant asks for
-      const int max_smem = 3 * 2 * 4 * 2048 * 2;
-      cudaFuncSetAttribute(ln_bwd_stream_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-      cudaFuncSetAttribute(ln_bwd_stream_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-      attr_set = true;
-    }
+    // the largest ring either variant asks for
+    constexpr int max_smem = 3 * 2 * 4 * 2048 * 2;
+    if (ensure_dynamic_smem(reinterpret_cast<const void*>(ln_bwd_stream_kernel<4, 1>), max_smem) != 0 ||
+        ensure_dynamic_smem(reinterpret_cast<const void*>(ln_bwd_stream_kernel<2, 2>), max_smem) != 0)
+      return 3;
+    count_variant(KV_LN_BWD_STREAM);
     if (R == 4)
       launch_pdl(ln_bwd_stream_kernel<4, 1>, dim3(grid), dim3(256), smem, st, a, dr, a.workspace, nslabs, nst);
     else
@@ -1050,6 +1042,7 @@ int ln_bwd(const LnBwdArgs& a, cudaStream_t st) {
     return status();
   }
   if (blocks >= 2 * device_sms() && !two_pass_only) {
+    count_variant(KV_LN_BWD_FUSED);
     ln_bwd_fused_kernel<<<blocks, 256, 0, st>>>(a, dr, a.workspace);
     const bool any = (a.dy && (a.dgamma || a.dbeta)) || a.dbias;
     if (any)
@@ -1058,6 +1051,7 @@ int ln_bwd(const LnBwdArgs& a, cudaStream_t st) {
                                                                 a.dbias);
     return status();
   }
+  count_variant(KV_LN_BWD_TWO_PASS);
   // phase A: dx (+ dropout'(dx)) per row
   if (a.dx || a.dxd) {
     if (a.d % 256 == 0 && a.d <= 4096) {

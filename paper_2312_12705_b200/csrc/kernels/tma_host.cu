@@ -3,7 +3,10 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <mutex>
+#include <set>
+#include <utility>
 
 namespace gptb200 {
 
@@ -48,14 +51,51 @@ bool make_tmap_f32(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t out
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+namespace {
+constexpr int kMaxDevices = 64;
+std::atomic<int> g_sms[kMaxDevices];
+std::mutex g_attr_mu;
+std::set<std::pair<const void*, int>> g_attr_done;
+std::atomic<int64_t> g_variants[KV_NUM];
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+}  // namespace
+
 int device_sm_count() {
-  static int n = 0;
+  const int dev = current_device();
+  if (dev < 0 || dev >= kMaxDevices) return 148;
+  int n = g_sms[dev].load(std::memory_order_relaxed);
   if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    g_sms[dev].store(n, std::memory_order_relaxed);
   }
   return n;
+}
+
+int ensure_dynamic_smem(const void* kernel, int bytes) {
+  const auto key = std::make_pair(kernel, current_device());
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if (g_attr_done.count(key)) return 0;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  g_attr_done.insert(key);
+  return 0;
+}
+
+void count_variant(int v) {
+  if (v >= 0 && v < KV_NUM) g_variants[v].fetch_add(1, std::memory_order_relaxed);
+}
+
+void read_variants(int64_t* out, int n) {
+  for (int i = 0; i < n; ++i) out[i] = i < KV_NUM ? g_variants[i].load(std::memory_order_relaxed) : 0;
+}
+
+void reset_variants() {
+  for (auto& v : g_variants) v.store(0, std::memory_order_relaxed);
 }
 
 }  // namespace gptb200

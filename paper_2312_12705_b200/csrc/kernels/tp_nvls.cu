@@ -16,6 +16,11 @@ struct NvlsContext {
   ncclDevComm dev{};
   int max_ctas = 0;
   int nranks = 1;
+  int device = 0;
+  // Deadlock-free grid caps per VPT instantiation (0 = not computed yet), see sp_grid().
+  int fwd_cap[17] = {};
+  int bwd_cap[17] = {};
+  int ar_cap = 0;
 };
 
 namespace {
@@ -249,6 +254,7 @@ NvlsContext* nvls_create(ncclComm_t comm, size_t bytes, int max_ctas) {
   auto* c = new NvlsContext;
   c->nranks = n;
   c->max_ctas = max_ctas;
+  cudaGetDevice(&c->device);
   c->bytes = (bytes + (2u << 20) - 1) / (2u << 20) * (2u << 20);
   if (ncclMemAlloc(&c->base, c->bytes) != ncclSuccess) {
     delete c;
@@ -290,7 +296,40 @@ int64_t nvls_offset(const NvlsContext* c, const void* p) {
 }
 
 namespace {
-int sp_grid(const NvlsContext* c, int nrows) { return nrows < c->max_ctas ? nrows : c->max_ctas; }
+// Every CTA of an SP kernel waits at an LSA barrier for the CTA with the same index on every peer,
+// so a kernel only makes progress once ALL its CTAs are resident on every rank. Kernels of the two
+// barrier sets (step / SP stream and the recompute stream) and NCCL's own spin-waiting kernels
+// (DP reduce-scatter / allgather, TP grad allreduce on the comm stream) can be in flight together:
+// if one rank's SMs fill with set-0 CTAs while a peer's fill with set-1 or NCCL CTAs, the wait is
+// cyclic. Cap each set at half of the CTAs the GPU can hold for this kernel outside a reserve of
+// SMs for NCCL, so all concurrently active spin-waiting grids are co-resident whatever the order.
+constexpr int kNcclReservedSms = 24;
+
+template <typename Kernel>
+int deadlock_free_cap(Kernel k, int device, int threads = kSpThreads) {
+  int sms = 0, per_sm = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || sms <= 0) return 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, 0) != cudaSuccess || per_sm <= 0)
+    per_sm = 1;
+  const int usable = sms > 2 * kNcclReservedSms ? sms - kNcclReservedSms : sms / 2;
+  return per_sm * (usable / kNvlsBarrierSets) > 0 ? per_sm * (usable / kNvlsBarrierSets) : 1;
+}
+
+int sp_grid(NvlsContext* c, int nrows, int vpt, bool fwd) {
+  int& cap = fwd ? c->fwd_cap[vpt] : c->bwd_cap[vpt];
+  if (cap == 0) {
+    switch (vpt) {
+#define CAP(V) \
+  case V: cap = fwd ? deadlock_free_cap(sp_ln_fwd_kernel<V>, c->device) : deadlock_free_cap(sp_ln_bwd_kernel<V>, c->device); break;
+      CAP(1) CAP(2) CAP(3) CAP(4) CAP(5) CAP(6) CAP(7) CAP(8) CAP(9) CAP(10) CAP(11) CAP(12) CAP(13) CAP(14)
+      CAP(15) CAP(16)
+#undef CAP
+      default: cap = 1;
+    }
+    if (cap > c->max_ctas) cap = c->max_ctas;
+  }
+  return nrows < cap ? nrows : cap;
+}
 }  // namespace
 
 int sp_ln_fwd(NvlsContext* c, const SpLnFwdArgs& a_in, cudaStream_t st) {
@@ -302,7 +341,7 @@ int sp_ln_fwd(NvlsContext* c, const SpLnFwdArgs& a_in, cudaStream_t st) {
   if (a.gamma && (a.ln_off < 0 || !a.beta || !a.mean || !a.rstd)) return 1;
   const int vpt = (a.d / 8 + kSpThreads - 1) / kSpThreads;
   const DropDev dr = make_drop(a.drop);
-  const int grid = sp_grid(c, a.nrows);
+  const int grid = sp_grid(c, a.nrows, vpt, true);
   switch (vpt) {
 #define SPF(V) case V: sp_ln_fwd_kernel<V><<<grid, kSpThreads, 0, st>>>(c->dev, c->win, a, dr); break;
     SPF(1) SPF(2) SPF(3) SPF(4) SPF(5) SPF(6) SPF(7) SPF(8) SPF(9) SPF(10) SPF(11) SPF(12) SPF(13) SPF(14)
@@ -322,7 +361,7 @@ int sp_ln_bwd(NvlsContext* c, const SpLnBwdArgs& a_in, cudaStream_t st) {
   if (a.dy_off >= 0 && (!a.x || !a.gamma || !a.mean || !a.rstd)) return 1;
   const int vpt = (a.d / 8 + kSpThreads - 1) / kSpThreads;
   const DropDev dr = make_drop(a.drop);
-  const int grid = sp_grid(c, a.nrows);
+  const int grid = sp_grid(c, a.nrows, vpt, false);
   switch (vpt) {
 #define SPB(V) case V: sp_ln_bwd_kernel<V><<<grid, kSpThreads, 0, st>>>(c->dev, c->win, a, dr); break;
     SPB(1) SPB(2) SPB(3) SPB(4) SPB(5) SPB(6) SPB(7) SPB(8) SPB(9) SPB(10) SPB(11) SPB(12) SPB(13) SPB(14)
@@ -359,7 +398,11 @@ int nvls_allreduce_bf16(NvlsContext* c, void* buf, size_t n, cudaStream_t st, in
       n % (8 * static_cast<size_t>(c->nranks)))
     return 1;
   const size_t vec_per_rank = n / 8 / c->nranks;
-  if (ctas <= 0 || ctas > c->max_ctas) ctas = c->max_ctas;
+  if (c->ar_cap == 0) {
+    c->ar_cap = deadlock_free_cap(nvls_allreduce_kernel, c->device, kThreads);
+    if (c->ar_cap > c->max_ctas) c->ar_cap = c->max_ctas;
+  }
+  if (ctas <= 0 || ctas > c->ar_cap) ctas = c->ar_cap;
   nvls_allreduce_kernel<<<ctas, kThreads, 0, st>>>(c->dev, c->win, off, vec_per_rank);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }

@@ -3,7 +3,7 @@
 // Reference roles: CounterRecord / hw_flops / parse_counter_csv (proj/src/metrics.cpp:67-117,
 // AMD SQ_INSTS_VALU_*), diagnose_mbs_mismatch / roofline / weak_scaling / strong_scaling
 // (proj/src/metrics.cpp:164-240).
-#include "trainplan/metrics.hpp"
+#include "trainplan/b200_metrics.hpp"
 
 #include <array>
 #include <charconv>

@@ -8,7 +8,7 @@
 #include "runtime/status.h"
 #include "trainplan/capi.h"
 #include "trainplan/core.hpp"
-#include "trainplan/metrics.hpp"
+#include "trainplan/b200_metrics.hpp"
 #include <sstream>
 
 using namespace trainplan;

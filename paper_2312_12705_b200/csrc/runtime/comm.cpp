@@ -8,7 +8,22 @@ void nccl_check(ncclResult_t r, const char* what) {
   if (r != ncclSuccess) throw CommError{TP_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r)};
 }
 
+void Comms::abort() {
+  if (aborted) return;
+  aborted = true;
+  tp_nvls = nullptr;
+  for (ncclComm_t& c : links_in_order) ncclCommAbort(c);
+  links_in_order.clear();
+  link_send[0] = link_send[1] = link_recv[0] = link_recv[1] = nullptr;
+  for (ncclComm_t* c : {&emb_comm, &dp_comm, &tp_comm, &world_comm})
+    if (*c) {
+      ncclCommAbort(*c);
+      *c = nullptr;
+    }
+}
+
 Comms::~Comms() {
+  if (aborted) return;
   if (tp_nvls) {
     nvls_destroy(tp_nvls, tp_comm);
     tp_nvls = nullptr;
@@ -96,6 +111,11 @@ void Comms::dp_allgather_bf16(void* buf, size_t n, cudaStream_t st) const {
   if (dp == 1) return;
   auto* b = static_cast<uint16_t*>(buf);
   nccl_check(ncclAllGather(b + static_cast<size_t>(me.d) * n, b, n, ncclBfloat16, dp_comm, st), "dp allgather");
+}
+
+void Comms::dp_allreduce_f32(float* buf, size_t n, cudaStream_t st) const {
+  if (dp == 1) return;
+  nccl_check(ncclAllReduce(buf, buf, n, ncclFloat, ncclSum, dp_comm, st), "dp allreduce");
 }
 
 void Comms::emb_allreduce_f32(float* buf, size_t n, cudaStream_t st) const {

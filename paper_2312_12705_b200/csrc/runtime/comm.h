@@ -29,6 +29,11 @@ class Comms {
 
   // world_size == 1 creates no NCCL communicators at all.
   void init(const trainplan::ParallelConfig& cfg, int rank, int world, const ncclUniqueId* id);
+  // Watchdog path: ncclCommAbort every communicator (no peer synchronisation, so it returns even
+  // when a peer is dead or stuck); the NVLS window is leaked (its device state may be in use by a
+  // kernel that never finishes). The process should exit afterwards.
+  void abort();
+  bool aborted = false;
 
   int rank = 0, world = 1;
   trainplan::RankCoords me;
@@ -58,6 +63,7 @@ class Comms {
   void tp_allgather_f32(const float* send, float* recv, size_t n_per_rank, cudaStream_t st) const;
   void dp_reduce_scatter_f32(float* buf, size_t n_per_rank, cudaStream_t st) const;  // in place
   void dp_allgather_bf16(void* buf, size_t n_per_rank, cudaStream_t st) const;       // in place
+  void dp_allreduce_f32(float* buf, size_t n, cudaStream_t st) const;                 // ZeRO-0
   void emb_allreduce_f32(float* buf, size_t n, cudaStream_t st) const;
   void world_allreduce_f32(float* buf, size_t n, cudaStream_t st) const;
   // Pipeline p2p over the ring links: dir 0 = activations (to p+1 / from p-1), dir 1 = gradients

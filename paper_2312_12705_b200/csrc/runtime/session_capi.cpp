@@ -5,6 +5,7 @@
 #include <exception>
 #include <memory>
 
+#include "kernels/tma_host.h"
 #include "runtime/stage.h"
 #include "runtime/status.h"
 #include "trainplan/capi.h"
@@ -190,6 +191,33 @@ int tp_session_time_steps(tp_session* s, int steps, int profile, float* ms, tp_k
       }
     }
   });
+}
+
+int tp_session_set_timeout(tp_session* s, double seconds) {
+  return run("tp_session_set_timeout", [&] { s->stage->set_timeout(seconds); });
+}
+
+int tp_session_memory(tp_session* s, tp_memory_report* out) {
+  return run("tp_session_memory", [&] {
+    const Stage& st = *s->stage;
+    out->params_bytes = st.category_bytes(MEM_PARAMS);
+    out->gradient_bytes = st.category_bytes(MEM_GRADS);
+    out->optimizer_bytes = st.category_bytes(MEM_OPTIMIZER);
+    out->activation_bytes = st.category_bytes(MEM_ACTIVATIONS);
+    out->workspace_bytes = st.category_bytes(MEM_WORKSPACE);
+    out->window_bytes = st.window_bytes();
+    out->total_bytes = st.device_bytes() + st.window_bytes();
+    out->zero_stage = st.zero_stage();
+  });
+}
+
+int tp_variant_counts(int64_t out[TP_KERNEL_VARIANTS]) {
+  static_assert(KV_NUM == TP_KERNEL_VARIANTS, "variant count");
+  return run("tp_variant_counts", [&] { read_variants(out, TP_KERNEL_VARIANTS); });
+}
+
+int tp_variant_counts_reset(void) {
+  return run("tp_variant_counts_reset", [&] { reset_variants(); });
 }
 
 int tp_session_allreduce_max(tp_session* s, float* v) {

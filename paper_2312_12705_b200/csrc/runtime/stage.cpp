@@ -7,8 +7,10 @@
 //        allreduce of its input gradient (Megatron f/g operators).
 #include "runtime/stage.h"
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 
@@ -39,7 +41,8 @@ void Stage::ck(int status, const char* what) {
   }
 }
 
-Stage::KScope::KScope(Stage* st, int kind, double flops, double bytes) : s(st), k(kind), idx(0) {
+Stage::KScope::KScope(Stage* st, int kind, double flops, double bytes, cudaStream_t on)
+    : s(st), k(kind), idx(0), stream(on ? on : st->st_) {
   if (!s->profile_) return;
   if (s->ev_used_ == s->ev_pool_.size()) {
     cudaEvent_t a, b;
@@ -53,12 +56,12 @@ Stage::KScope::KScope(Stage* st, int kind, double flops, double bytes) : s(st), 
   s->prof_acc_.launches[kind] += 1;
   s->prof_acc_.flops[kind] += flops;
   s->prof_acc_.bytes[kind] += bytes;
-  cudaEventRecord(s->ev_pool_[idx].first, s->st_);
+  cudaEventRecord(s->ev_pool_[idx].first, stream);
 }
 
 Stage::KScope::~KScope() {
   if (!s->profile_) return;
-  cudaEventRecord(s->ev_pool_[idx].second, s->st_);
+  cudaEventRecord(s->ev_pool_[idx].second, stream);
 }
 
 Stage::Stage(const trainplan::ModelSpec& model, const trainplan::ParallelConfig& cfg, const TrainOptions& opts,
@@ -89,6 +92,8 @@ Stage::Stage(const trainplan::ModelSpec& model, const trainplan::ParallelConfig&
   first_ = comms_.me.p == 0;
   last_ = comms_.me.p == cfg.pp - 1;
   ckpt_ = cfg.checkpoint_activations;
+  zero_ = cfg.zero_stage >= 1 ? 1 : 0;
+  if (const char* t = std::getenv("GPTB200_TIMEOUT_S")) timeout_s_ = std::atof(t);
   plan_ = pipeline_actions(cfg.pp, m_, v_, comms_.me.p, kDhRing, false);
   eval_plan_ = pipeline_actions(cfg.pp, m_, v_, comms_.me.p, kDhRing, true);
   nslots_ = pipeline_slots(plan_);
@@ -97,6 +102,7 @@ Stage::Stage(const trainplan::ModelSpec& model, const trainplan::ParallelConfig&
 }
 
 Stage::~Stage() {
+  if (poisoned_) return;  // a kernel may still spin on a dead peer: leak rather than hang
   if (st_) cudaStreamSynchronize(st_);
   for (int i = 0; i < 2; ++i)
     if (send_st_[i]) {
@@ -134,7 +140,7 @@ Stage::~Stage() {
   if (st_) cudaStreamDestroy(st_);
 }
 
-void* Stage::alloc(size_t bytes) {
+void* Stage::alloc(size_t bytes, int cat) {
   void* p = nullptr;
   bytes = (bytes + 255) / 256 * 256;
   cudaError_t e = cudaMalloc(&p, bytes);
@@ -145,6 +151,7 @@ void* Stage::alloc(size_t bytes) {
   }
   allocations_.push_back(p);
   dev_bytes_ += bytes;
+  cat_bytes_[cat] += bytes;
   return p;
 }
 
@@ -181,7 +188,7 @@ void Stage::build_layout() {
     Bucket b;
     b.off = bucket_start;
     b.len = off - bucket_start;
-    b.master_off = buckets_.empty() ? 0 : buckets_.back().master_off + buckets_.back().len / cfg_.dp;
+    b.master_off = buckets_.empty() ? 0 : buckets_.back().master_off + own_len(buckets_.back());
     buckets_.push_back(b);
     bucket_start = off;
   };
@@ -210,18 +217,18 @@ void Stage::build_layout() {
     layer_bucket_.push_back(static_cast<int>(buckets_.size()) - 1);
   }
   P_ = off;
-  shard_ = P_ / cfg_.dp;
+  shard_ = zero_ ? P_ / cfg_.dp : P_;
   slot_index_.assign(2 + kPerLayer * L_ + 2, -1);
   for (size_t i = 0; i < slots_.size(); ++i) slot_index_[slots_[i].tensor_id] = static_cast<int>(i);
 }
 
 void Stage::allocate() {
   const size_t M = M_, d = d_, dt = dt_;
-  params_ = static_cast<bf16*>(alloc(P_ * sizeof(bf16)));
-  grads_ = static_cast<float*>(alloc(P_ * sizeof(float)));
-  master_ = static_cast<float*>(alloc(shard_ * sizeof(float)));
-  adam_m_ = static_cast<float*>(alloc(shard_ * sizeof(float)));
-  adam_v_ = static_cast<float*>(alloc(shard_ * sizeof(float)));
+  params_ = static_cast<bf16*>(alloc(P_ * sizeof(bf16), MEM_PARAMS));
+  grads_ = static_cast<float*>(alloc(P_ * sizeof(float), MEM_GRADS));
+  master_ = static_cast<float*>(alloc(shard_ * sizeof(float), MEM_PARAMS));
+  adam_m_ = static_cast<float*>(alloc(shard_ * sizeof(float), MEM_OPTIMIZER));
+  adam_v_ = static_cast<float*>(alloc(shard_ * sizeof(float), MEM_OPTIMIZER));
   tokens_ = static_cast<int32_t*>(alloc(static_cast<size_t>(cfg_.gbs) * (s_ + 1) * sizeof(int32_t)));
 
   // TP > 1: full-width buffers that a collective reads or writes on every rank live in one NCCL
@@ -243,53 +250,56 @@ void Stage::allocate() {
   Ms_ = sp_ ? M_ / cfg_.tp : M_;
   row0_ = sp_ ? comms_.me.t * Ms_ : 0;
   size_t sym_used = 0;
-  auto full = [&](size_t elems) -> bf16* {  // [M, d]-class buffer: window when SP/NVLS, else HBM
+  window_bytes_ = sym ? nvls_bytes(comms_.tp_nvls) : 0;
+  auto full = [&](size_t elems, int cat) -> bf16* {  // [M, d]-class buffer: window when SP/NVLS, else HBM
     if (sym) {
       bf16* p = reinterpret_cast<bf16*>(sym + sym_used);
       sym_used += (elems * 2 + 255) / 256 * 256;
+      cat_bytes_[cat] += (elems * 2 + 255) / 256 * 256;
       return p;
     }
-    return static_cast<bf16*>(alloc(elems * 2));
+    return static_cast<bf16*>(alloc(elems * 2, cat));
   };
+  constexpr int ACT = MEM_ACTIVATIONS;
   const size_t Ms = Ms_;
   auto layer_acts = [&](LayerActs& A) {
-    A.a = sp_ ? full(Md) : static_cast<bf16*>(alloc(Md * 2));
-    A.qkv = static_cast<bf16*>(alloc(M * 3 * dt * 2));
-    A.o = static_cast<bf16*>(alloc(M * dt * 2));
-    A.hmid = static_cast<bf16*>(alloc(Ms * d * 2));
-    A.m2 = sp_ ? full(Md) : static_cast<bf16*>(alloc(Md * 2));
-    A.u = static_cast<bf16*>(alloc(M * 4 * dt * 2));
-    A.g = static_cast<bf16*>(alloc(M * 4 * dt * 2));
-    A.mu1 = static_cast<float*>(alloc(Ms * 4));
-    A.rs1 = static_cast<float*>(alloc(Ms * 4));
-    A.mu2 = static_cast<float*>(alloc(Ms * 4));
-    A.rs2 = static_cast<float*>(alloc(Ms * 4));
-    A.lse = static_cast<float*>(alloc(static_cast<size_t>(mbs_) * ht_ * s_ * 4));
+    A.a = sp_ ? full(Md, ACT) : static_cast<bf16*>(alloc(Md * 2, ACT));
+    A.qkv = static_cast<bf16*>(alloc(M * 3 * dt * 2, ACT));
+    A.o = static_cast<bf16*>(alloc(M * dt * 2, ACT));
+    A.hmid = static_cast<bf16*>(alloc(Ms * d * 2, ACT));
+    A.m2 = sp_ ? full(Md, ACT) : static_cast<bf16*>(alloc(Md * 2, ACT));
+    A.u = static_cast<bf16*>(alloc(M * 4 * dt * 2, ACT));
+    A.g = static_cast<bf16*>(alloc(M * 4 * dt * 2, ACT));
+    A.mu1 = static_cast<float*>(alloc(Ms * 4, ACT));
+    A.rs1 = static_cast<float*>(alloc(Ms * 4, ACT));
+    A.mu2 = static_cast<float*>(alloc(Ms * 4, ACT));
+    A.rs2 = static_cast<float*>(alloc(Ms * 4, ACT));
+    A.lse = static_cast<float*>(alloc(static_cast<size_t>(mbs_) * ht_ * s_ * 4, ACT));
   };
-  tmp_md_ = full(Md);
-  dm_ = full(Md);
+  tmp_md_ = full(Md, MEM_WORKSPACE);
+  dm_ = full(Md, MEM_WORKSPACE);
   slots_act_.resize(nslots_);
   for (auto& S : slots_act_) {
     S.h.resize(Lc_ + 1);
-    for (auto& h : S.h) h = static_cast<bf16*>(alloc(Ms * d * 2));
+    for (auto& h : S.h) h = static_cast<bf16*>(alloc(Ms * d * 2, ACT));
     if (!ckpt_) {
       S.acts.resize(Lc_);
       for (auto& A : S.acts) layer_acts(A);
     }
-    S.inputs = static_cast<int32_t*>(alloc(M * 4));
-    S.labels = static_cast<int32_t*>(alloc(M * 4));
+    S.inputs = static_cast<int32_t*>(alloc(M * 4, ACT));
+    S.labels = static_cast<int32_t*>(alloc(M * 4, ACT));
   }
   if (ckpt_) layer_acts(scratch_);
   rc_overlap_ = sp_ && rc_overlap;
   if (rc_overlap_) {
     layer_acts(scratch2_);
-    rc_tmp_ = full(Md);
+    rc_tmp_ = full(Md, MEM_WORKSPACE);
     cudaStreamCreateWithFlags(&rc_st_, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&rc_fork_, cudaEventDisableTiming);
     for (auto& e : rc_done_) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   }
   for (auto& b : dh_) b = static_cast<bf16*>(alloc(Ms * d * 2));
-  dy_ = sp_ ? full(Md) : static_cast<bf16*>(alloc(Md * 2));
+  dy_ = sp_ ? full(Md, MEM_WORKSPACE) : static_cast<bf16*>(alloc(Md * 2));
   du_ = static_cast<bf16*>(alloc(M * 4 * dt * 2));
   do_ = static_cast<bf16*>(alloc(M * dt * 2));
   dqkv_ = static_cast<bf16*>(alloc(M * 3 * dt * 2));
@@ -300,10 +310,10 @@ void Stage::allocate() {
   ws_ = static_cast<float*>(alloc(ws * 4));
   colpart_ = static_cast<float*>(alloc(static_cast<size_t>(M_ / 32) * 4 * dt * 4));
   if (last_) {
-    hf_ = sp_ ? full(Md) : static_cast<bf16*>(alloc(Md * 2));
-    muf_ = static_cast<float*>(alloc(Ms * 4));
-    rsf_ = static_cast<float*>(alloc(Ms * 4));
-    logits_ = static_cast<bf16*>(alloc(M * static_cast<size_t>(Vt_) * 2));
+    hf_ = sp_ ? full(Md, ACT) : static_cast<bf16*>(alloc(Md * 2, ACT));
+    muf_ = static_cast<float*>(alloc(Ms * 4, ACT));
+    rsf_ = static_cast<float*>(alloc(Ms * 4, ACT));
+    logits_ = static_cast<bf16*>(alloc(M * static_cast<size_t>(Vt_) * 2, ACT));
     xstats_ = static_cast<float*>(alloc(M * 3 * 4));
     xall_ = static_cast<float*>(alloc(M * 3 * 4 * cfg_.tp));
     row_loss_ = static_cast<float*>(alloc(M * 4));
@@ -376,8 +386,8 @@ void Stage::init_params() {
   }
   ck(cast_f32_bf16(grads_, params_, P_, st_), "cast params");
   for (const Bucket& b : buckets_) {
-    const int64_t n = b.len / cfg_.dp;
-    if (n) cudaMemcpyAsync(master_ + b.master_off, grads_ + b.off + comms_.me.d * n, n * sizeof(float),
+    const int64_t n = own_len(b);
+    if (n) cudaMemcpyAsync(master_ + b.master_off, grads_ + own_offset(b), n * sizeof(float),
                            cudaMemcpyDeviceToDevice, st_);
   }
   cudaMemsetAsync(adam_m_, 0, shard_ * sizeof(float), st_);
@@ -925,13 +935,13 @@ void Stage::sp_bwd(const SpLnBwdArgs& a) {
 // Adam on this rank's slice of one bucket, on `st` (fp32 master/m/v, writes the bf16 copy).
 void Stage::adam_bucket(int bucket, cudaStream_t st) {
   const Bucket& b = buckets_[bucket];
-  const int64_t n = b.len / cfg_.dp;
+  const int64_t n = own_len(b);
   if (!n) return;
   AdamArgs a;
   a.lr = opts_.lr, a.beta1 = opts_.beta1, a.beta2 = opts_.beta2, a.eps = opts_.eps, a.weight_decay = opts_.weight_decay;
   a.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(opts_.beta1), step_no_));
   a.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(opts_.beta2), step_no_));
-  const int64_t own = b.off + comms_.me.d * n;
+  const int64_t own = own_offset(b);
   a.n = n, a.master = master_ + b.master_off, a.m = adam_m_ + b.master_off, a.v = adam_v_ + b.master_off;
   a.grad = grads_ + own, a.param = params_ + own;
   ck(adam_step(a, st), "adam");
@@ -962,9 +972,18 @@ void Stage::grads_ready(int bucket) {
     }
     if (bucket == 0 && cfg_.pp > 1 && (first_ || last_))
       comms_.emb_allreduce_f32(grads_ + slot_offset(0), static_cast<size_t>(Vt_) * d_, comm_st_);
-    if (cfg_.dp > 1) comms_.dp_reduce_scatter_f32(grads_ + b.off, b.len / cfg_.dp, comm_st_);
+    // DP collectives are timed on the comm stream (K_COMM_DP: overlapped with backward; the exposed
+    // part is the K_ADAM tail of step())
+    if (cfg_.dp > 1) {
+      KScope prof(this, K_COMM_DP, 0, (zero_ ? 4.0 : 8.0) * b.len, comm_st_);
+      if (zero_) comms_.dp_reduce_scatter_f32(grads_ + b.off, b.len / cfg_.dp, comm_st_);
+      else comms_.dp_allreduce_f32(grads_ + b.off, b.len, comm_st_);  // ZeRO-0 (perf.cpp:101)
+    }
     adam_bucket(bucket, comm_st_);
-    if (cfg_.dp > 1) comms_.dp_allgather_bf16(params_ + b.off, b.len / cfg_.dp, comm_st_);
+    if (cfg_.dp > 1 && zero_) {
+      KScope prof(this, K_COMM_DP, 0, 2.0 * b.len, comm_st_);
+      comms_.dp_allgather_bf16(params_ + b.off, b.len / cfg_.dp, comm_st_);
+    }
   } catch (const CommError& e) {
     throw StepError{e.code, e.msg};
   }
@@ -1039,7 +1058,7 @@ void Stage::step() {
 float Stage::read_loss() {
   float v = 0.f;
   cudaMemcpyAsync(&v, loss_acc_, sizeof(float), cudaMemcpyDeviceToHost, st_);
-  cudaStreamSynchronize(st_);
+  wait(st_, "read loss");
   return static_cast<float>(v / (static_cast<double>(cfg_.gbs) * s_));
 }
 
@@ -1055,9 +1074,35 @@ float Stage::eval_loss() {
   return read_loss();
 }
 
-void Stage::sync() {
-  cudaError_t e = cudaStreamSynchronize(st_);
-  if (e != cudaSuccess) throw StepError{TP_ERR_CUDA, std::string("stream sync: ") + cudaGetErrorString(e)};
+void Stage::sync() { wait(st_, "stream sync"); }
+
+// Host wait with a watchdog. Spins briefly (the common case: the step is about to finish), then
+// polls with a growing sleep. On timeout the communicators are aborted so peers blocked in NCCL
+// return errors instead of hanging, and the session is marked unusable (a kernel spinning on a
+// dead peer's barrier cannot be cancelled: the process should exit).
+void Stage::wait(cudaStream_t st, const char* what) {
+  if (poisoned_) throw StepError{TP_ERR_TIMEOUT, std::string(what) + ": session aborted by the watchdog"};
+  if (timeout_s_ <= 0) {
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) throw StepError{TP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+    return;
+  }
+  using clock = std::chrono::steady_clock;
+  const auto t0 = clock::now();
+  for (int it = 0;; ++it) {
+    const cudaError_t e = cudaStreamQuery(st);
+    if (e == cudaSuccess) return;
+    if (e != cudaErrorNotReady) throw StepError{TP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+    const double waited = std::chrono::duration<double>(clock::now() - t0).count();
+    if (waited > timeout_s_) {
+      poisoned_ = true;
+      comms_.abort();
+      throw StepError{TP_ERR_TIMEOUT, std::string(what) + ": no progress after " + std::to_string(waited) +
+                                          " s (watchdog); NCCL communicators aborted"};
+    }
+    if (it < 2000) continue;  // ~ the first millisecond: spin
+    std::this_thread::sleep_for(std::chrono::microseconds(it < 4000 ? 20 : 200));
+  }
 }
 
 void Stage::barrier() {
@@ -1077,7 +1122,7 @@ void Stage::barrier() {
 void Stage::read_flat(int which, int64_t offset, int64_t n, float* host) const {
   const int64_t len = (which <= 1) ? P_ : shard_;
   if (offset < 0 || n < 0 || offset + n > len) throw StepError{TP_ERR_INVALID, "read_flat: range out of bounds"};
-  cudaStreamSynchronize(st_);
+  const_cast<Stage*>(this)->wait(st_, "read_flat");
   if (which == 0) {
     std::vector<uint16_t> tmp(n);
     cudaMemcpy(tmp.data(), params_ + offset, n * 2, cudaMemcpyDeviceToHost);
@@ -1095,7 +1140,7 @@ void Stage::read_tensor(int which, int tid, float* host) const {
   const ParamSlot* s = slot(tid);
   if (!s) throw StepError{TP_ERR_INVALID, "tensor " + std::to_string(tid) + " not on this rank"};
   const int64_t n = s->rows * s->cols;
-  cudaStreamSynchronize(st_);
+  const_cast<Stage*>(this)->wait(st_, "read_tensor");
   if (which == 0) {
     std::vector<uint16_t> tmp(n);
     cudaMemcpy(tmp.data(), params_ + s->offset, n * 2, cudaMemcpyDeviceToHost);
@@ -1112,7 +1157,7 @@ void Stage::read_tensor(int which, int tid, float* host) const {
   } else {
     int64_t moff = -1;
     for (const Bucket& b : buckets_) {
-      const int64_t per = b.len / cfg_.dp, own = b.off + comms_.me.d * per;
+      const int64_t per = own_len(b), own = own_offset(b);
       if (off >= own && off + n <= own + per) moff = b.master_off + (off - own);
     }
     if (moff < 0) throw StepError{TP_ERR_INVALID, "tensor outside this rank's ZeRO shard"};

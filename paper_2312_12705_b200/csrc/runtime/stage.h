@@ -60,6 +60,12 @@ struct Bucket {
   int64_t off = 0, len = 0, master_off = 0;
 };
 
+// Device-memory categories of the session (MemoryReport, /root/reference/proj/include/trainplan/
+// memory.hpp:47-55): parameters = bf16 working copy + fp32 master shard, gradients = fp32 main grads,
+// optimizer = Adam m + v shards, activations = everything kept or recomputed per microbatch,
+// workspace = per-op scratch (the reference's framework overhead).
+enum MemCategory { MEM_PARAMS = 0, MEM_GRADS, MEM_OPTIMIZER, MEM_ACTIVATIONS, MEM_WORKSPACE, MEM_NUM };
+
 struct StepTimes {  // milliseconds of the last step on this rank (CUDA events)
   float total = 0, tp_comm = 0, pp_comm = 0, dp_comm = 0, optimizer = 0;
 };
@@ -94,6 +100,19 @@ class Stage {
   int64_t flat_params() const { return P_; }
   int64_t shard_params() const { return shard_; }
   size_t device_bytes() const { return dev_bytes_; }
+  // Bytes per MemCategory (HBM allocations plus buffers carved from the NVLS window) and the window.
+  size_t category_bytes(int c) const { return cat_bytes_[c]; }
+  size_t window_bytes() const { return window_bytes_; }
+  // ZeRO stage in effect: 1 = optimizer state sharded over DP (reduce-scatter + allgather),
+  // 0 = replicated (gradient allreduce, every rank updates every parameter).
+  int zero_stage() const { return zero_; }
+  // This rank's optimizer range of bucket b: flat offset and length.
+  int64_t own_offset(const Bucket& b) const { return zero_ ? b.off + comms_.me.d * (b.len / cfg_.dp) : b.off; }
+  int64_t own_len(const Bucket& b) const { return zero_ ? b.len / cfg_.dp : b.len; }
+  // Watchdog: host waits on the session's streams give up after `seconds` (<= 0: wait forever),
+  // abort the NCCL communicators and throw TP_ERR_TIMEOUT; the session is unusable afterwards.
+  void set_timeout(double seconds) { timeout_s_ = seconds; }
+  bool poisoned() const { return poisoned_; }
   StepTimes last_times() const { return times_; }
   int microbatches() const { return m_; }
   int kernel_launches_per_step() const { return launches_; }
@@ -123,7 +142,8 @@ class Stage {
     int32_t* labels = nullptr;    // [M]
   };
 
-  void* alloc(size_t bytes);
+  void* alloc(size_t bytes, int cat = MEM_WORKSPACE);
+  void wait(cudaStream_t st, const char* what);
   void build_layout();
   void allocate();
   LayerW w(int l) const;
@@ -154,11 +174,12 @@ class Stage {
   void gemm_wgrad(const bf16* dY, const bf16* X, float* dW, int M, int N, int K);
   void ck(int status, const char* what);
   friend struct KScope;
-  struct KScope {
+  struct KScope {  // brackets the enclosed launches on `stream` (default: the step stream)
     Stage* s;
     int k;
     size_t idx;
-    KScope(Stage* st, int kind, double flops = 0, double bytes = 0);
+    cudaStream_t stream;
+    KScope(Stage* st, int kind, double flops = 0, double bytes = 0, cudaStream_t on = nullptr);
     ~KScope();
   };
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool_;
@@ -199,6 +220,11 @@ class Stage {
   cudaStream_t st_ = nullptr;
   std::vector<void*> allocations_;
   size_t dev_bytes_ = 0;
+  size_t cat_bytes_[MEM_NUM] = {};
+  size_t window_bytes_ = 0;
+  int zero_ = 1;
+  double timeout_s_ = 0.0;
+  bool poisoned_ = false;
 
   // shape
   // Ll_ local layers = v_ chunks of Lc_ layers; local layer li is global layer glayer(li).

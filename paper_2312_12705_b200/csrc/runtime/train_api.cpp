@@ -1,6 +1,7 @@
 // C++ drop-in layer (include/trainplan/train.hpp) on top of the C-ABI.
 #include "trainplan/train.hpp"
 
+#include <chrono>
 #include <cstdio>
 #include <new>
 #include <random>
@@ -15,6 +16,7 @@ void throw_for(int rc, const char* where) {
   std::string msg = std::string(where) + ": " + tp_last_error();
   if (rc == TP_ERR_INVALID) throw std::invalid_argument(msg);
   if (rc == TP_ERR_OOM) throw std::bad_alloc();
+  if (rc == TP_ERR_TIMEOUT) throw StepTimeout(msg);
   throw std::runtime_error(msg);
 }
 
@@ -96,6 +98,23 @@ float TrainSession::time_steps(int steps, tp_kernel_times* kt) {
   return ms;
 }
 
+void TrainSession::set_timeout(double seconds) { throw_for(tp_session_set_timeout(s_, seconds), "set_timeout"); }
+
+MemoryReport TrainSession::memory_report(std::uint64_t mem_per_gpu) {
+  tp_memory_report m{};
+  throw_for(tp_session_memory(s_, &m), "memory_report");
+  MemoryReport r;
+  r.params_bytes = m.params_bytes;
+  r.gradient_bytes = m.gradient_bytes;
+  r.optimizer_bytes = m.optimizer_bytes;
+  r.activation_bytes = m.activation_bytes;
+  r.total_bytes = m.total_bytes;
+  const std::uint64_t named = r.params_bytes + r.gradient_bytes + r.optimizer_bytes + r.activation_bytes;
+  r.overhead_bytes = r.total_bytes > named ? r.total_bytes - named : 0;  // workspace + unused window
+  r.fits = mem_per_gpu == 0 || r.total_bytes <= mem_per_gpu;
+  return r;
+}
+
 float TrainSession::allreduce_max(float v) {
   throw_for(tp_session_allreduce_max(s_, &v), "allreduce_max");
   return v;
@@ -108,21 +127,22 @@ ThroughputEstimate measure(const ModelSpec& model, const ParallelConfig& cfg, co
   if (!val.ok) throw std::invalid_argument("unvalidated configuration: " + val.hard_violations().front().message);
   const ParallelConfig rc = val.resolved;
   ThroughputEstimate est;
-  std::optional<TrainSession> sess;
+  float ms = 0.f, ms_prof = 0.f;
+  tp_kernel_times kt{};
   try {
-    sess.emplace(model, rc, opts.train, opts.dist);
+    TrainSession sess(model, rc, opts.train, opts.dist);
+    if (opts.timeout_s > 0) sess.set_timeout(opts.timeout_s);
+    sess.init_params();
+    const auto tokens = synthetic_tokens(opts.train.seed, static_cast<std::int64_t>(rc.gbs) * (model.seq_length + 1),
+                                         model.vocab_size);
+    sess.upload(tokens.data(), tokens.size());
+    if (opts.warmup > 0) sess.time_steps(opts.warmup);
+    ms = sess.allreduce_max(sess.time_steps(opts.steps));
+    ms_prof = sess.time_steps(opts.steps, &kt);
   } catch (const std::bad_alloc&) {
-    est.oom = true;  // a reported state, as in the reference (perf.cpp:49-53)
+    est.oom = true;  // a reported state wherever the allocation failed (perf.cpp:49-53)
     return est;
   }
-  sess->init_params();
-  const auto tokens = synthetic_tokens(opts.train.seed, static_cast<std::int64_t>(rc.gbs) * (model.seq_length + 1),
-                                       model.vocab_size);
-  sess->upload(tokens.data(), tokens.size());
-  if (opts.warmup > 0) sess->time_steps(opts.warmup);
-  const float ms = sess->allreduce_max(sess->time_steps(opts.steps));
-  tp_kernel_times kt{};
-  const float ms_prof = sess->time_steps(opts.steps, &kt);
   est.iter_time = ms / 1e3 / opts.steps;
   const double flops = model_flops_per_iteration(model, rc.gbs, rc.checkpoint_activations);
   est.flops_per_gpu = flops / (est.iter_time * cluster.world_size());
@@ -131,55 +151,69 @@ ThroughputEstimate measure(const ModelSpec& model, const ParallelConfig& cfg, co
   auto sec = [&](int k) { return kt.ms[k] / 1e3 / opts.steps * scale; };
   est.breakdown.tp_comm = sec(5);
   est.breakdown.pp_comm = sec(6);
-  est.breakdown.dp_comm = sec(7);
-  est.breakdown.compute = sec(0) + sec(1) + sec(2) + sec(3) + sec(4) + sec(8);
+  // class 7 (the DP collectives on the comm stream) overlaps backward; what the step waits for is
+  // the exposed optimizer-pipeline tail (class 8), reported as dp_comm when there is a DP group
+  const bool dp_group = rc.dp > 1;
+  est.breakdown.dp_comm = dp_group ? sec(8) : 0.0;
+  est.breakdown.compute = sec(0) + sec(1) + sec(2) + sec(3) + sec(4) + (dp_group ? 0.0 : sec(8));
   est.breakdown.bubble = std::max(0.0, est.iter_time - est.breakdown.compute - est.breakdown.tp_comm -
                                            est.breakdown.pp_comm - est.breakdown.dp_comm);
   return est;
 }
 
+MemoryReport measured_memory_per_gpu(const ModelSpec& model, const ParallelConfig& cfg, const ClusterSpec& cluster,
+                                     const DistributedContext& dist) {
+  ValidationResult val = validate(model, cfg, cluster);
+  if (val.ok) validate_kernels(model, val.resolved, val);
+  if (!val.ok) throw std::invalid_argument("unvalidated configuration: " + val.hard_violations().front().message);
+  try {
+    TrainSession sess(model, val.resolved, TrainOptions{}, dist);
+    return sess.memory_report(cluster.mem_per_gpu);
+  } catch (const std::bad_alloc&) {
+    return MemoryReport{};  // fits = false
+  }
+}
+
 std::optional<ParallelConfig> measured_config_from_point(const SearchPoint& point, const ClusterSpec& base) {
-  ClusterSpec cluster = base;
-  cluster.num_nodes = point.nodes;
-  const long long world = cluster.world_size();
-  const long long shards = static_cast<long long>(point.tp) * point.pp;
-  if (point.tp < 1 || point.pp < 1 || point.mbs < 1 || point.gas < 1 || world % shards != 0) return std::nullopt;
-  ParallelConfig cfg;
-  cfg.tp = point.tp;
-  cfg.pp = point.pp;
-  cfg.dp = static_cast<int>(world / shards);
-  cfg.mbs = point.mbs;
-  cfg.gbs = point.mbs * point.gas * cfg.dp;
-  cfg.zero_stage = point.zero1 ? 1 : 0;
-  cfg.precision = Precision::BF16;
-  cfg.grad_accum_dtype = GradAccumDtype::FP32;
-  cfg.checkpoint_activations = true;
-  cfg.flash_attention = true;
+  auto cfg = config_from_point(point, base);  // the reference's mapping (perf.cpp:161-181) ...
+  if (cfg) {                                  // ... computed in bf16 with fp32 main grads
+    cfg->precision = Precision::BF16;
+    cfg->grad_accum_dtype = GradAccumDtype::FP32;
+  }
   return cfg;
 }
 
 Evaluator make_measured_evaluator(const ModelSpec& model, const ClusterSpec& base, const MeasureOptions& opts) {
   return [model, base, opts](const SearchPoint& point) {
+    const auto t0 = std::chrono::steady_clock::now();
     TrialRecord rec;
     rec.point = point;
     const auto cfg = measured_config_from_point(point, base);
     ClusterSpec cluster = base;
     cluster.num_nodes = point.nodes;
-    if (!cfg || !validate(model, *cfg, cluster).ok) {
-      rec.failure_kind = FailureKind::Invalid;
-      return rec;
+    ValidationResult val;
+    if (cfg) {
+      val = validate(model, *cfg, cluster);
+      if (val.ok) validate_kernels(model, val.resolved, val);
     }
-    try {
-      const ThroughputEstimate est = measure(model, *cfg, cluster, opts);
-      if (est.oom) {
+    if (!cfg || !val.ok) {
+      rec.failure_kind = FailureKind::Invalid;
+    } else {
+      try {
+        const ThroughputEstimate est = measure(model, *cfg, cluster, opts);
+        if (est.oom)
+          rec.failure_kind = FailureKind::Oom;
+        else
+          rec.objective = est.flops_per_gpu / 1e12;
+      } catch (const std::bad_alloc&) {
         rec.failure_kind = FailureKind::Oom;
-        return rec;
+      } catch (const StepTimeout&) {
+        rec.failure_kind = FailureKind::Timeout;
+      } catch (const std::exception&) {  // invalid argument or a CUDA / NCCL failure: the point does not run
+        rec.failure_kind = FailureKind::Invalid;
       }
-      rec.objective = est.flops_per_gpu / 1e12;
-      rec.wall_time = est.iter_time * (opts.warmup + 2 * opts.steps);
-    } catch (const std::invalid_argument&) {
-      rec.failure_kind = FailureKind::Invalid;
     }
+    rec.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return rec;
   };
 }

@@ -9,7 +9,7 @@
 #include <string>
 #include <vector>
 
-#include "trainplan/metrics.hpp"
+#include "trainplan/b200_metrics.hpp"
 
 int main() {
   std::string tag;

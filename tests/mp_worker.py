@@ -43,7 +43,7 @@ def main():
         time.sleep(0.02)
     nid = idf.read_bytes()
     spec = T.ModelSpec(c["L"], c["d"], c["a"], c["V"], c["s"])
-    cfg = T.ParallelConfig(tp=c["tp"], pp=c["pp"], dp=c["dp"], mbs=c["mbs"], gbs=c["gbs"], zero_stage=1,
+    cfg = T.ParallelConfig(tp=c["tp"], pp=c["pp"], dp=c["dp"], mbs=c["mbs"], gbs=c["gbs"], zero_stage=c.get("zero", 1),
                            checkpoint_activations=c.get("ckpt", 0), interleave_v=c.get("v", 1))
     opts = T.TrainOptions(seed=1234, dropout=c.get("dropout", 0.0), lr=1e-3, weight_decay=0.01)
     if c.get("tp_env"):
@@ -52,11 +52,6 @@ def main():
     sess.init_params()
     info = sess.info()
     P, shard = info["flat_params"], info["shard_params"]
-    master0 = sess.read_flat(2, 0, shard)
-    tokens = O.gen_tokens(1234, c["gbs"] * (c["s"] + 1), c["V"]).reshape(c["gbs"], c["s"] + 1)
-    loss = sess.train_step(tokens)
-    grads = sess.read_flat(1, 0, P)
-    master1 = sess.read_flat(2, 0, shard)
     ntens = 2 + 16 * c["L"] + 2
     layout = {}
     for tid in range(ntens):
@@ -64,9 +59,35 @@ def main():
         if ti is not None:
             layout[tid] = ti
     coords = T.rank_coords(a.rank, c["tp"], c["pp"], c["dp"])
-    np.savez(out / f"rank{a.rank}.npz", tp_mode=np.array(info["tp_mode"]), grads=grads, master0=master0, master1=master1, loss=np.array(loss),
-             coords=np.array(coords), P=np.array(P), shard=np.array(shard), layout=json.dumps(layout),
-             buckets=np.array(sess.buckets(), dtype=np.int64).reshape(-1, 3))
+    tokens = O.gen_tokens(1234, c["gbs"] * (c["s"] + 1), c["V"]).reshape(c["gbs"], c["s"] + 1)
+    nsample = c.get("sample", 0)
+    if nsample:
+        # wide layouts (dp == 1): per tensor only `nsample` evenly spaced local rows of the fp32
+        # master before / after the step and of the gradient (host memory stays small at 1T widths)
+        assert c["dp"] == 1
+        rows = {tid: np.unique(np.linspace(0, ti["rows"] - 1, min(ti["rows"], nsample)).astype(np.int64))
+                for tid, ti in layout.items()}
+
+        def sample(which):
+            return {str(tid): np.stack([sess.read_flat(which, ti["offset"] + int(r) * ti["cols"], ti["cols"])
+                                        for r in rows[tid]]) for tid, ti in layout.items()}
+        m0 = sample(2)
+        loss = sess.train_step(tokens)
+        g, m1 = sample(1), sample(2)
+        extra = {f"{k}_{tid}": v for k, d in (("g", g), ("m0", m0), ("m1", m1)) for tid, v in d.items()}
+        extra.update({f"rows_{tid}": r for tid, r in rows.items()})
+        np.savez(out / f"rank{a.rank}.npz", tp_mode=np.array(info["tp_mode"]), loss=np.array(loss),
+                 coords=np.array(coords), P=np.array(P), shard=np.array(shard), layout=json.dumps(layout),
+                 variants=json.dumps(T.variant_counts()), **extra)
+    else:
+        master0 = sess.read_flat(2, 0, shard)
+        loss = sess.train_step(tokens)
+        grads = sess.read_flat(1, 0, P)
+        master1 = sess.read_flat(2, 0, shard)
+        np.savez(out / f"rank{a.rank}.npz", tp_mode=np.array(info["tp_mode"]), grads=grads, master0=master0,
+                 master1=master1, loss=np.array(loss), coords=np.array(coords), P=np.array(P),
+                 shard=np.array(shard), layout=json.dumps(layout), variants=json.dumps(T.variant_counts()),
+                 buckets=np.array(sess.buckets(), dtype=np.int64).reshape(-1, 3))
     sess.barrier()
     sess.close()
 

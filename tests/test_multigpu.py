@@ -44,15 +44,25 @@ def _slice(full, info):
     return full[np.ix_(grow, gcol)] if info["cols"] > 1 else full[grow]
 
 
+def _slice_rows(full, info, local_rows):
+    grow, gcol = T.global_index_map(info)
+    grow = grow[local_rows]
+    return full[np.ix_(grow, gcol)] if info["cols"] > 1 else full[grow]
+
+
 def run_layout(tp, pp, dp, L=2, d=256, a=4, V=1024, s=128, mbs=1, gbs=None, ckpt=0, dropout=0.0, v=1, tp_env=None,
-               want_tp_mode=None):
+               want_tp_mode=None, zero=1, sample=0, want_variants=()):
+    """One train step on tp*pp*dp GPUs against the oracle. zero = ZeRO stage (1 sharded, 0
+    replicated). sample > 0 (dp == 1 only): the ranks return `sample` evenly spaced local rows per
+    tensor instead of their full flat buffers — the wide (22B / 175B / 1T) layouts."""
     world = tp * pp * dp
     if _ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
     gbs = gbs or mbs * dp * 2
     c = dict(L=L, d=d, a=a, V=V, s=s, tp=tp, pp=pp, dp=dp, mbs=mbs, gbs=gbs, ckpt=ckpt, dropout=dropout, v=v,
-             tp_env=tp_env or {})
-    with tempfile.TemporaryDirectory() as td:
+             tp_env=tp_env or {}, zero=zero, sample=sample)
+    (ROOT / ".mp_tmp").mkdir(exist_ok=True)  # not /tmp: the 1T-width dumps should not sit in a tmpfs
+    with tempfile.TemporaryDirectory(dir=ROOT / ".mp_tmp") as td:
         procs = [subprocess.Popen([sys.executable, str(ROOT / "tests" / "mp_worker.py"), "--cfg", json.dumps(c),
                                    "--rank", str(r), "--world", str(world), "--out", td],
                                   stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
@@ -60,7 +70,7 @@ def run_layout(tp, pp, dp, L=2, d=256, a=4, V=1024, s=128, mbs=1, gbs=None, ckpt
         outs = []
         for p in procs:
             try:
-                outs.append(p.communicate(timeout=300)[0])
+                outs.append(p.communicate(timeout=600)[0])
             except subprocess.TimeoutExpired:
                 for q in procs:
                     q.kill()
@@ -85,40 +95,60 @@ def run_layout(tp, pp, dp, L=2, d=256, a=4, V=1024, s=128, mbs=1, gbs=None, ckpt
     losses = [float(r["loss"]) for r in ranks]
     assert max(losses) - min(losses) < 1e-6, losses
     assert abs(losses[0] - oloss) <= 1e-2 * max(1.0, oloss), (losses[0], oloss)
-    # per (t, p) model shard: assemble the DP-sharded flat buffers
     report = []
     b1, b2, lr, eps, wd = np.float32(0.9), np.float32(0.95), np.float32(1e-3), np.float32(1e-8), np.float32(0.01)
+
+    def check_tensor(t, p, tid, w0, g, w1, init_ref, g_ref):
+        np.testing.assert_array_equal(w0, init_ref, err_msg=f"init tid {tid}")
+        if np.linalg.norm(g_ref) > 1e-6:
+            e, cs = _rel(g, g_ref), _cos(g, g_ref)
+            report.append((t, p, tid, e, cs))
+            assert e < 3e-2 and cs > 0.999, (t, p, tid, e, cs)
+        mh, vh = ((1 - b1) * g) / (1 - b1), ((1 - b2) * g * g) / (1 - b2)
+        ref = w0 - lr * (mh / (np.sqrt(vh) + eps) + wd * w0)
+        np.testing.assert_allclose(w1, ref, rtol=1e-5, atol=1e-7, err_msg=f"adam tid {tid}")
+
     for t in range(tp):
         for p in range(pp):
             members = [r for r in ranks if tuple(r["coords"][:2]) == (t, p)]
             members.sort(key=lambda r: int(r["coords"][2]))
-            P = int(members[0]["P"])
-            red, m0, m1 = np.zeros(P, np.float32), np.zeros(P, np.float32), np.zeros(P, np.float32)
-            for off, ln, moff in members[0]["buckets"]:  # DP rank k owns slice k of every bucket
-                per = ln // dp
-                for k, m in enumerate(members):
-                    lo = off + k * per
-                    red[lo:lo + per] = m["grads"][lo:lo + per]
-                    m0[lo:lo + per] = m["master0"][moff:moff + per]
-                    m1[lo:lo + per] = m["master1"][moff:moff + per]
             layout = {int(k): v for k, v in json.loads(str(members[0]["layout"])).items()}
+            if sample:
+                m = members[0]
+                for tid, info in layout.items():
+                    rows = m[f"rows_{tid}"]
+                    shape = (len(rows), info["cols"]) if info["cols"] > 1 else (len(rows),)
+                    check_tensor(t, p, tid, m[f"m0_{tid}"].reshape(shape), m[f"g_{tid}"].reshape(shape),
+                                 m[f"m1_{tid}"].reshape(shape), _slice_rows(O.tensor(om, params, tid), info, rows),
+                                 _slice_rows(O.tensor(om, grads, tid), info, rows))
+                continue
+            P = int(members[0]["P"])
+            if zero == 0:  # replicated: every DP rank holds the reduced gradients and the full master
+                red, m0, m1 = members[0]["grads"], members[0]["master0"], members[0]["master1"]
+                for other in members[1:]:
+                    np.testing.assert_array_equal(other["master1"], m1)
+            else:
+                red, m0, m1 = np.zeros(P, np.float32), np.zeros(P, np.float32), np.zeros(P, np.float32)
+                for off, ln, moff in members[0]["buckets"]:  # DP rank k owns slice k of every bucket
+                    per = ln // dp
+                    for k, m in enumerate(members):
+                        lo = off + k * per
+                        red[lo:lo + per] = m["grads"][lo:lo + per]
+                        m0[lo:lo + per] = m["master0"][moff:moff + per]
+                        m1[lo:lo + per] = m["master1"][moff:moff + per]
             for tid, info in layout.items():
                 n = info["rows"] * info["cols"]
                 off = info["offset"]
                 shape = (info["rows"], info["cols"]) if info["cols"] > 1 else (info["rows"],)
-                init_ref = _slice(O.tensor(om, params, tid), info)
-                np.testing.assert_array_equal(m0[off:off + n].reshape(shape), init_ref, err_msg=f"init tid {tid}")
-                g_ref = _slice(O.tensor(om, grads, tid), info)
-                g = red[off:off + n].reshape(shape)
-                if np.linalg.norm(g_ref) > 1e-6:
-                    e, cs = _rel(g, g_ref), _cos(g, g_ref)
-                    report.append((t, p, tid, e, cs))
-                    assert e < 3e-2 and cs > 0.999, (t, p, tid, e, cs)
-                w0 = m0[off:off + n]
-                gg = red[off:off + n]
-                mh, vh = ((1 - b1) * gg) / (1 - b1), ((1 - b2) * gg * gg) / (1 - b2)
-                ref = w0 - lr * (mh / (np.sqrt(vh) + eps) + wd * w0)
-                np.testing.assert_allclose(m1[off:off + n], ref, rtol=1e-5, atol=1e-7, err_msg=f"adam tid {tid}")
+                check_tensor(t, p, tid, m0[off:off + n].reshape(shape), red[off:off + n].reshape(shape),
+                             m1[off:off + n].reshape(shape), _slice(O.tensor(om, params, tid), info),
+                             _slice(O.tensor(om, grads, tid), info))
+    for name in want_variants:  # the kernel variants the production layouts rely on ran
+        assert all(json.loads(str(r["variants"]))[name] > 0 for r in ranks), name
+    print(json.dumps({"layout": f"tp{tp}.pp{pp}.dp{dp}", "L": L, "d": d, "a": a, "s": s, "V": V, "loss": losses[0],
+                      "oracle_loss": oloss, "worst_grad_rel": max((r[3] for r in report), default=0.0),
+                      "min_cos": min((r[4] for r in report), default=1.0),
+                      "variants": json.loads(str(ranks[0]["variants"]))}))
     return losses[0], oloss, report
 
 
@@ -185,3 +215,33 @@ def test_pp2_dp2_interleaved_v2():
 def test_config1_tp2_pp2_dp2():
     # BASELINE config 1 layout (needs 8 GPUs)
     run_layout(tp=2, pp=2, dp=2, gbs=8)
+
+
+def test_dp2_zero0_replicated():
+    # zero_stage 0 (search point zero1 = false): gradient allreduce, every rank updates everything
+    run_layout(tp=1, pp=1, dp=2, zero=0, dropout=0.1)
+
+
+# ---- BASELINE widths (TP-rank-local shapes of configs 3-5; reduced depth / sequence / vocab)
+
+def test_tp2_22b_width_ckpt():
+    # config 3 width: d 6144, 48 heads (hd 128), TP2 -> 24 heads / 3072 columns per rank
+    run_layout(tp=2, pp=1, dp=1, L=1, d=6144, a=48, V=1024, s=1024, gbs=2, ckpt=1, dropout=0.1, want_tp_mode=3,
+               want_variants=("gemm_pair_256", "attn_fwd_persistent"))
+
+
+def test_tp4_22b_width_ckpt():
+    run_layout(tp=4, pp=1, dp=1, L=2, d=6144, a=48, V=1024, s=1024, gbs=2, ckpt=1, dropout=0.1, want_tp_mode=3,
+               sample=48)
+
+
+def test_tp2_pp2_175b_width_ckpt():
+    # config 4 width: d 12288, 96 heads, TP2 x PP2 1F1B, 4 microbatches
+    run_layout(tp=2, pp=2, dp=1, L=2, d=12288, a=96, V=1024, s=256, gbs=4, ckpt=1, want_tp_mode=3, sample=32)
+
+
+def test_tp4_1t_width_hd160_ckpt():
+    # config 5 width: d 25600, 160 heads (hd 160), TP4 -> 40 heads / 6400 columns per rank; the SP
+    # LayerNorm kernels at their widest instantiation and the hd-160 attention kernels
+    run_layout(tp=4, pp=1, dp=1, L=1, d=25600, a=160, V=512, s=256, gbs=1, ckpt=1, want_tp_mode=3, sample=24,
+               want_variants=("attn_bwd_hd160",))
