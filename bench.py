@@ -140,14 +140,18 @@ class ClockSampler:
 
 
 def model_flops(L, d, a, V, s, batch, ckpt) -> float:
-    """trainplan::model_flops_per_iteration (proj/src/arch.cpp:64-92), via the C-ABI."""
-    from paper_2312_12705_b200 import _lib as T
-    return T.model_flops(T.ModelSpec(L, d, a, V, s), batch, ckpt)
+    """trainplan::model_flops_per_iteration (proj/src/arch.cpp:64-92) in exact Python integers:
+    24 c B s L d^2 (1 + s/6d + V/16Ld) = c B s d (48 L d + 8 L s + 3 V) / 2, c = 4 with activation
+    checkpointing, else 3. (Pure Python so the reference arm loads nothing from this repo's
+    library; tests/test_bench.py checks it against the C-ABI and the reference's golden.)"""
+    c = 4 if ckpt else 3
+    return float(c * batch * s * d * (48 * L * d + 8 * L * s + 3 * V)) / 2.0
 
 
 def cpu_layer_sample(L, d, a, V, s, threads):
     """Times the CPU oracle (port of the step) on one decoder layer fwd+bwd over one sequence;
-    returns (seconds, layer model-FLOPs, extrapolated full-model tokens/s, model TFLOPS)."""
+    returns (seconds, layer model-FLOPs, full-model tokens/s EXTRAPOLATED at the measured FLOP rate,
+    model TFLOPS)."""
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_lib as O
     lib = O.load()
@@ -159,6 +163,28 @@ def cpu_layer_sample(L, d, a, V, s, threads):
     rate = layer_flops / secs
     per_token_model = model_flops(L, d, a, V, s, 1, False) / s
     return secs, layer_flops, rate / per_token_model, rate / 1e12
+
+
+def cpu_config1_step(threads):
+    """One REAL full train step of BASELINE config 1 (tiny GPT: 2 layers, hidden 256, 4 heads,
+    seq 128, V 51200, GBS 8) on the CPU oracle: 8 sequences fwd+bwd + Adam over every parameter —
+    the unsharded arithmetic of the TP2 x PP2 x DP2 layout. Returns (seconds, tokens/s)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    L, d, a, V, s, gbs = 2, 256, 4, 51200, 128, 8
+    m, o = O.model(L, d, a, V, s), O.opts(seed=1234, lr=1e-4)
+    params = O.init_params(m, 1234)
+    tokens = O.gen_tokens(1234, gbs * (s + 1), V).reshape(gbs, s + 1)
+    mom, var = np.zeros_like(params), np.zeros_like(params)
+    t0 = time.perf_counter()
+    grads = np.zeros_like(params)
+    for i in range(gbs):
+        O.fwd_bwd(m, o, params, tokens[i:i + 1], sample0=i, step=1, loss_scale=1.0 / (gbs * s), grads=grads)
+    import ctypes
+    O.load().orc_adam(params.size, params, mom, var, grads, 1, ctypes.byref(o))
+    secs = time.perf_counter() - t0
+    return secs, gbs * s / secs
 
 
 def run_reference(args, rank, world):
@@ -176,20 +202,40 @@ def run_reference(args, rank, world):
         secs_all.append(secs)
     v = statistics.median(vals)
     gbs = mbs * nmb * max(args.gpus // (tp * pp), 1)
+    c1_secs, c1_tok = cpu_config1_step(threads)
+    sample_ms = 1e3 * statistics.median(secs_all)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * gbs * s / v,
+        "steps": args.steps, "warmup": args.warmup,
+        # a reference-arm step is a bounded sample of the workload (one layer, one sequence): its
+        # measured wall time is the step time; `value` is the workload's tokens/s extrapolated from it
+        "ms_per_step": sample_ms, "value_extrapolated": True,
+        "full_step_ms_extrapolated": 1e3 * gbs * s / v,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(args, world),
-        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port", "extrapolated": True,
                          "sample": f"one decoder layer fwd+bwd (d={d}, s={s}, 1 sequence) of the CPU oracle port "
                                    f"(oracle/gpt_oracle.c; the reference trainplan only models the step), "
-                                   f"{statistics.median(secs_all):.2f}s/sample, extrapolated to the full "
-                                   f"{L}-layer model at the measured FLOP rate"},
+                                   f"{sample_ms / 1e3:.2f}s/sample, extrapolated to the full {L}-layer model at "
+                                   f"the measured FLOP rate",
+                         "config1_full_step": {"seconds": c1_secs, "tokens_per_s": c1_tok, "extrapolated": False,
+                                               "what": "BASELINE config 1 (L2 d256 a4 V51200 s128, GBS 8): one "
+                                                       "complete fwd+bwd+Adam step of the oracle"}},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "native_libs": loaded_native_libs(),
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def loaded_native_libs():
+    """Shared objects of this repo mapped into the process (the reference arm must show only the
+    oracle's)."""
+    try:
+        maps = Path("/proc/self/maps").read_text().splitlines()
+    except OSError:
+        return None
+    return sorted({ln.split()[-1] for ln in maps if str(ROOT) in ln and ln.endswith(".so")})
 
 
 def workload_config(args, world):
@@ -295,12 +341,25 @@ def main():
         gemm_tf = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] else 0.0
         line["roofline"] = {"kernel": "tcgen05 GEMM (all GEMM launches of the step)", "bound": "tensor",
                             "achieved": gemm_tf, "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
-                            "frac": gemm_tf / peaks["bf16_tflops_sustained"], "traffic": gemm_traffic(),
-                            "traffic_algorithmic": gemm_traffic("algorithmic_bytes"),
-                            "traffic_kernel": gemm_traffic("kernel"),
+                            "frac": gemm_tf / peaks["bf16_tflops_sustained"],
+                            "traffic": gemm_traffic(args.workload),
+                            "traffic_algorithmic": gemm_traffic(args.workload, "algorithmic_bytes"),
+                            "traffic_kernel": gemm_traffic(args.workload, "kernel"),
                             "peak_source": peak_src + ", sustained bf16 (kernel timed inside a long step)",
                             "gemm_share_of_step": g["ms"] / ms_prof if ms_prof else None,
                             "algorithmic_flops_per_launch": g["flops"] / max(g["launches"], 1)}
+        # the other kernel families against their own roofline (tensor for attention, HBM for norms)
+        classes = {"attn_fwd": ("tensor", "bf16_tflops_sustained", "TFLOP/s"),
+                   "attn_bwd": ("tensor", "bf16_tflops_sustained", "TFLOP/s"),
+                   "norm": ("hbm", "hbm_gbs", "GB/s"), "adam": ("hbm", "hbm_gbs", "GB/s")}
+        line["roofline_by_class"] = {}
+        for k, (bound, pk, unit) in classes.items():
+            v = kt[k]
+            if not v["ms"]:
+                continue
+            ach = (v["flops"] / (v["ms"] / 1e3) / 1e12) if bound == "tensor" else (v["bytes"] / (v["ms"] / 1e3) / 1e9)
+            line["roofline_by_class"][k] = {"bound": bound, "achieved": ach, "peak": peaks[pk], "unit": unit,
+                                            "frac": ach / peaks[pk], "share_of_step": v["ms"] / ms_prof}
         line["kernels"] = {k: {"ms_per_step": v["ms"] / args.steps, "share": v["ms"] / ms_prof if ms_prof else None,
                                "launches_per_step": v["launches"] / args.steps,
                                **({"tflops": v["flops"] / (v["ms"] / 1e3) / 1e12} if v["flops"] and v["ms"] else {}),
@@ -318,15 +377,20 @@ def main():
     return 0
 
 
-def gemm_traffic(key="bytes_per_launch"):
+def gemm_traffic(workload, key="bytes_per_launch"):
     """Per-launch DRAM bytes (or the algorithmic bytes, key="algorithmic_bytes") of the representative
-    GEMM launch in the committed ncu capture (profiles/gemm_traffic.json), else None."""
+    GEMM launch of THIS workload in the committed ncu capture (profiles/gemm_traffic.json, one
+    entry per workload), else None."""
     p = ROOT / "profiles" / "gemm_traffic.json"
     if p.exists():
         try:
-            return json.loads(p.read_text()).get(key)
-        except (ValueError, KeyError):
+            d = json.loads(p.read_text())
+        except ValueError:
             return None
+        entry = d.get("workloads", {}).get(workload)
+        if entry is None and d.get("workload") == workload:
+            entry = d
+        return entry.get(key) if entry else None
     return None
 
 

@@ -1,4 +1,4 @@
-// Causal flash attention (K5 forward, K6 backward). See attention.cu for layouts.
+// Causal flash attention (K5 forward, K6 backward) on tcgen05 / TMEM / TMA: attention_sm100.cu.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -21,7 +21,7 @@ int flash_attn_fwd(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* 
 int flash_attn_fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse,
                       cudaStream_t st);
 
-// tcgen05 backward main kernel (hd 64/128): dK, dV into dqkv and dQ into the zeroed fp32 dq_acc
+// tcgen05 backward main kernel (hd 64 / 128 / 160): dK, dV into dqkv and dQ into the zeroed fp32 dq_acc
 // (D must already hold rowsum(dO*O)).
 int flash_attn_bwd_tc_main(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout,
                            const float* lse, const float* D, float* dq_acc, __nv_bfloat16* dqkv,

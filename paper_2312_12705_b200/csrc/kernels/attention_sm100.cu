@@ -60,15 +60,21 @@ __device__ __forceinline__ float ex2(float x) {
 
 // P stays in TMEM (bf16 over the S columns it replaces) and PV reads its A operand from TMEM.
 // CS softmax warps per TMEM lane quarter, each owning 128/CS score columns of its 32 query rows.
+// A head of 160 columns is two 64-column SW128 chunks plus a 32-column SW64 tail chunk (its own
+// tensor map), so Q / K / V tiles are 40 KB and K and V stay double-buffered.
 template <int HD>
 struct TcFwdCfg {
   static constexpr int NC = (HD + 63) / 64;             // 64-wide swizzle chunks of the head dim
-  static constexpr int kStages = NC <= 2 ? 3 : 1;       // K ring and V ring depth
+  static constexpr int NF = HD / 64;                    // full SW128 chunks
+  static constexpr int TAIL = HD % 64;                  // 0 or 32: the SW64 tail chunk
+  static_assert(TAIL == 0 || TAIL == 32, "head dim must be a multiple of 64 or 64k + 32");
   static constexpr int CS = 4;                          // column splits (softmax warps per quarter)
   static constexpr int kThreads = 64 + 128 * CS;
   static constexpr int kTileBytes = 128 * 128;          // one [128 rows][64] bf16 chunk
-  static constexpr int kQBytes = NC * kTileBytes;
-  static constexpr int kKVBytes = NC * kTileBytes;
+  static constexpr int kTailBytes = TAIL ? 128 * 64 : 0;  // [128 rows][32] bf16, 64-byte rows
+  static constexpr int kQBytes = NF * kTileBytes + kTailBytes;
+  static constexpr int kKVBytes = NF * kTileBytes + kTailBytes;
+  static constexpr int kStages = NC <= 2 ? 3 : 2;       // K ring and V ring depth
   // dynamic smem is declared __align__(1024) (checked at run time), so no alignment slack
   static constexpr int kSmem = kQBytes + 2 * kStages * kKVBytes + CS * 128 * 4 + 256;
   static_assert(kSmem <= 232448, "fa_fwd smem over the 227 KB opt-in limit");
@@ -77,10 +83,10 @@ struct TcFwdCfg {
 
 template <int HD>
 __global__ void __launch_bounds__(TcFwdCfg<HD>::kThreads, 1)
-    fa_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, __nv_bfloat16* __restrict__ out,
-                     float* __restrict__ lse, int s, int ht, float scale_log2) {
+    fa_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_tail,
+                     __nv_bfloat16* __restrict__ out, float* __restrict__ lse, int s, int ht, float scale_log2) {
   using Cfg = TcFwdCfg<HD>;
-  constexpr int NC = Cfg::NC, ST = Cfg::kStages, CS = Cfg::CS;
+  constexpr int NF = Cfg::NF, TAIL = Cfg::TAIL, ST = Cfg::kStages, CS = Cfg::CS;
   constexpr int CW = kBN / CS;  // score columns per softmax warp
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((ptx::smem_u32(smem_raw) & 1023u) != 0) __trap();  // 128B-swizzle atoms need 1 KB alignment
@@ -111,6 +117,7 @@ __global__ void __launch_bounds__(TcFwdCfg<HD>::kThreads, 1)
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tm_qkv);
+    if constexpr (TAIL != 0) ptx::tma_prefetch_desc(&tm_tail);
     ptx::mbar_init(q_full, 1);
     for (int i = 0; i < ST; ++i) {
       ptx::mbar_init(&k_full[i], 1);
@@ -132,30 +139,33 @@ __global__ void __launch_bounds__(TcFwdCfg<HD>::kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
   const uint32_t tO = tmem + 2 * kBN;
+  pdl_trigger();  // prologue (smem / TMEM / barriers) done: see pdl.cuh
+  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {
+      // a head's columns: NF SW128 chunks, then the SW64 tail chunk
+      auto load_head = [&](uint8_t* dst, uint64_t* bar, int col0, int row) {
+        for (int c = 0; c < NF; ++c) ptx::tma_load_2d(dst + c * Cfg::kTileBytes, &tm_qkv, bar, col0 + 64 * c, row);
+        if constexpr (TAIL != 0) ptx::tma_load_2d(dst + NF * Cfg::kTileBytes, &tm_tail, bar, col0 + 64 * NF, row);
+      };
       ptx::mbar_arrive_expect_tx(q_full, Cfg::kQBytes);
-      for (int c = 0; c < NC; ++c)
-        ptx::tma_load_2d(sQ + c * Cfg::kTileBytes, &tm_qkv, q_full, h * HD + 64 * c, row0 + qb * kBM);
+      load_head(sQ, q_full, h * HD, row0 + qb * kBM);
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j % ST, use = j / ST;
         WAIT(&k_empty[st], (use & 1) ^ 1, 1);
         ptx::mbar_arrive_expect_tx(&k_full[st], Cfg::kKVBytes);
-        for (int c = 0; c < NC; ++c)
-          ptx::tma_load_2d(sK + st * Cfg::kKVBytes + c * Cfg::kTileBytes, &tm_qkv, &k_full[st],
-                           dt + h * HD + 64 * c, row0 + j * kBN);
+        load_head(sK + st * Cfg::kKVBytes, &k_full[st], dt + h * HD, row0 + j * kBN);
         WAIT(&v_empty[st], (use & 1) ^ 1, 2);
         ptx::mbar_arrive_expect_tx(&v_full[st], Cfg::kKVBytes);
-        for (int c = 0; c < NC; ++c)
-          ptx::tma_load_2d(sV + st * Cfg::kKVBytes + c * Cfg::kTileBytes, &tm_qkv, &v_full[st],
-                           2 * dt + h * HD + 64 * c, row0 + j * kBN);
+        load_head(sV + st * Cfg::kKVBytes, &v_full[st], 2 * dt + h * HD, row0 + j * kBN);
       }
     }
   } else if (warp == 1) {
     {  // all 32 lanes: uniform descriptors, one elected lane issues
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBM, kBN, false, false);
-      constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(kBM, HD, false, true);
+      constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(kBM, 64 * NF, false, true);   // O columns of the SW128 chunks
+      constexpr uint32_t idesc_t = ptx::idesc_bf16_f32(kBM, TAIL ? TAIL : 32, false, true);  // tail columns
       const uint32_t q_addr = ptx::smem_u32(sQ);
       WAIT(q_full, 0, 3);
       auto issue_pv = [&](int j) {
@@ -168,6 +178,10 @@ __global__ void __launch_bounds__(TcFwdCfg<HD>::kThreads, 1)
         for (int kk = 0; kk < kBN / 16; ++kk) {  // P: 8 packed bf16x2 TMEM columns per K = 16 step
           const uint64_t bd = ptx::smem_desc_sw128(v_addr + kk * 2048, Cfg::kTileBytes, 1024);
           ptx::mma_bf16_ts_w(tO, tmem + pb * kBN + kk * 8, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          if constexpr (TAIL != 0) {  // O[:, 64 NF ..) from the SW64 tail chunk of V (16 kv rows = 1 KB)
+            const uint64_t bt = ptx::smem_desc_sw64(v_addr + NF * Cfg::kTileBytes + kk * 1024, 512, 512);
+            ptx::mma_bf16_ts_w(tO + 64 * NF, tmem + pb * kBN + kk * 8, bt, idesc_t, (j > 0 || kk > 0) ? 1u : 0u);
+          }
         }
         ptx::mma_commit_w(&pv_done[pb]);
         ptx::mma_commit_w(&v_empty[st]);
@@ -181,9 +195,15 @@ __global__ void __launch_bounds__(TcFwdCfg<HD>::kThreads, 1)
         const uint32_t k_addr = ptx::smem_u32(sK + st * Cfg::kKVBytes);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk / 4) * Cfg::kTileBytes + (kk % 4) * 32;
-          ptx::mma_bf16_ss_w(tmem + buf * kBN, ptx::smem_desc_sw128(q_addr + off, 16, 1024),
-                             ptx::smem_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+          if (kk < 4 * NF) {
+            const uint32_t off = (kk / 4) * Cfg::kTileBytes + (kk % 4) * 32;
+            ptx::mma_bf16_ss_w(tmem + buf * kBN, ptx::smem_desc_sw128(q_addr + off, 16, 1024),
+                               ptx::smem_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+          } else {  // tail chunk: 64-byte rows, 8-row atoms of 512 B
+            const uint32_t off = NF * Cfg::kTileBytes + (kk - 4 * NF) * 32;
+            ptx::mma_bf16_ss_w(tmem + buf * kBN, ptx::smem_desc_sw64(q_addr + off, 16, 512),
+                               ptx::smem_desc_sw64(k_addr + off, 16, 512), idesc_s, 1u);
+          }
         }
         ptx::mma_commit_w(&s_full[buf]);
         ptx::mma_commit_w(&k_empty[st]);
@@ -1482,6 +1502,363 @@ __global__ void __launch_bounds__(512, 1)
   }
 }
 
+// K6 for head dim 160 (the 1T shape) on tcgen05. At 64-query tiles TMEM cannot hold S^T, dP^T
+// and dQ^T next to the 2 x 160 accumulator columns of dV and dK, so the query tile is 32 rows and
+// every transient buffer is double-buffered:
+//   S^T x2 (2x32) | dP^T x2 (2x32) | dQ^T hd 0-127 (32) | dQ^T hd 128-159 (32) | dV (160) | dK (160)
+// = 512 columns. dQ^T = K^T dS^T has M = 160 rows: two M = 128 MMAs, the second over head dims
+// 128..255 of the K tile — rows 160..255 read the next 96 columns of shared memory (the rest of
+// the K tile's third swizzle chunk, then the V tile: finite data) and are never loaded from TMEM.
+// P^T / dS^T tiles are [128 kv][32 q] with 64-byte rows (SWIZZLE_64B), so one buffer serves as the
+// K-major A operand of dV / dK and as the MN-major B operand of dQ^T.
+// Warps: WG0 = TMA producer (warp 0) + MMA issuer (warp 1); WG1 / WG2 = P/dS compute of the even /
+// odd query tiles (each owns one S^T/dP^T TMEM pair and one P^T/dS^T smem pair); WG3 = dQ flush
+// (coalesced fp32 reductions, one per 32 head dims and query). Per tile j the MMA warp issues
+// stage 1 (S^T_j, dP^T_j) and then stage 2 of tile j-1 (dV, dK, dQ^T), so the exp / dS math of one
+// tile overlaps the tensor core on the other.
+template <int HD>
+struct TcBwd3Cfg {
+  static constexpr int NC = (HD + 63) / 64;        // 64-column SW128 chunks of a head (3)
+  static constexpr int QT = 32;                     // query rows per tile
+  static constexpr int kTileBytes = 128 * 128;      // [128 rows][64] bf16 chunk
+  static constexpr int kKVBytes = NC * kTileBytes;  // [128 kv][NC x 64]
+  static constexpr int kQChunk = QT * 128;          // [32 q][64]
+  static constexpr int kQBytes = NC * kQChunk;
+  static constexpr int kPBytes = 128 * QT * 2;      // [128 kv][32 q], 64-byte rows
+  static constexpr int QST = 3;                     // Q / dO / LSE / D ring depth
+  static constexpr int kSmem = 2 * kKVBytes + 2 * QST * kQBytes + 4 * kPBytes + QST * 2 * QT * 4 + 1024 + 256;
+  static_assert(HD > 128 && HD <= 192 && HD % 16 == 0, "two M = 128 dQ^T MMAs cover head dims 0..255");
+  static_assert(kSmem <= 232448, "smem over the 227 KB opt-in limit");
+};
+
+template <int HD>
+__global__ void __launch_bounds__(512, 1)
+    fa_bwd_tc3_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
+                      const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse,
+                      const float* __restrict__ Dg, float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv,
+                      int s, int ht, float scale_log2, float scale) {
+  using Cfg = TcBwd3Cfg<HD>;
+  constexpr int NC = Cfg::NC, TB = Cfg::kTileBytes, QT = Cfg::QT, QST = Cfg::QST;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = ptx::smem_align1024(smem_raw);
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + Cfg::kKVBytes;  // directly after K: the second dQ^T MMA reads past the K tile
+  uint8_t* sQ = sV + Cfg::kKVBytes;         // [QST][NC][32][64]
+  uint8_t* sdO = sQ + QST * Cfg::kQBytes;   // [QST][NC][32][64]
+  uint8_t* sPT = sdO + QST * Cfg::kQBytes;  // [2][128 kv][32 q]
+  uint8_t* sdST = sPT + 2 * Cfg::kPBytes;   // [2][128 kv][32 q]
+  float* sL = reinterpret_cast<float*>(sdST + 2 * Cfg::kPBytes);  // [QST][32]
+  float* sD = sL + QST * QT;                                      // [QST][32]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + QST * QT);
+  uint64_t* kv_full = bars;
+  uint64_t* qdo_full = bars + 1;         // [QST]
+  uint64_t* qdo_empty = qdo_full + QST;  // [QST]
+  uint64_t* s_full = qdo_empty + QST;    // [2] S^T / dP^T of buffer b computed
+  uint64_t* st_free = s_full + 2;        // [2] ... and read out by its compute warpgroup
+  uint64_t* pds_full = st_free + 2;      // [2] P^T / dS^T of buffer b written to smem
+  uint64_t* pds_free = pds_full + 2;     // [2] ... and consumed by stage 2
+  uint64_t* dq_full = pds_free + 2;
+  uint64_t* dq_free = dq_full + 1;
+  uint64_t* kdv_full = dq_free + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kdv_full + 1);
+
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
+  const int kvb = blockIdx.x;
+  const int b = blockIdx.y / ht, h = blockIdx.y % ht;
+  const int dt = ht * HD;
+  const int row0 = b * s;
+  const int kv0 = kvb * 128;
+  const int qt_first = kv0 / QT;  // query tiles at and after the diagonal
+  const int n_it = s / QT - qt_first;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tm_kv);
+    ptx::tma_prefetch_desc(&tm_q);
+    ptx::tma_prefetch_desc(&tm_do);
+    ptx::mbar_init(kv_full, 1);
+    for (int i = 0; i < QST; ++i) {
+      ptx::mbar_init(&qdo_full[i], 1);
+      ptx::mbar_init(&qdo_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&s_full[i], 1);
+      ptx::mbar_init(&st_free[i], 4);
+      ptx::mbar_init(&pds_full[i], 4);
+      ptx::mbar_init(&pds_free[i], 1);
+    }
+    ptx::mbar_init(dq_full, 1);
+    ptx::mbar_init(dq_free, 4);
+    ptx::mbar_init(kdv_full, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  pdl_trigger();
+  pdl_wait();
+  const uint32_t tS = tmem, tdP = tmem + 2 * QT, tDQa = tmem + 4 * QT, tDQb = tmem + 5 * QT, tdV = tmem + 6 * QT,
+                 tdK = tdV + HD;
+  const int wg = warp / 4;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const float* gLq = lse + (static_cast<size_t>(b) * ht + h) * s;
+      const float* gDq = Dg + (static_cast<size_t>(b) * ht + h) * s;
+      ptx::mbar_arrive_expect_tx(kv_full, 2 * Cfg::kKVBytes);
+      for (int c = 0; c < NC; ++c) {
+        ptx::tma_load_2d(sK + c * TB, &tm_kv, kv_full, dt + h * HD + 64 * c, row0 + kv0);
+        ptx::tma_load_2d(sV + c * TB, &tm_kv, kv_full, 2 * dt + h * HD + 64 * c, row0 + kv0);
+      }
+      for (int j = 0; j < n_it; ++j) {
+        const int sq = j % QST;
+        const int q0 = (qt_first + j) * QT;
+        WAIT(&qdo_empty[sq], ((j / QST) & 1) ^ 1, 60);
+        ptx::mbar_arrive_expect_tx(&qdo_full[sq], 2 * Cfg::kQBytes + 2 * QT * 4);
+        for (int c = 0; c < NC; ++c) {
+          ptx::tma_load_2d(sQ + sq * Cfg::kQBytes + c * Cfg::kQChunk, &tm_q, &qdo_full[sq], h * HD + 64 * c, row0 + q0);
+          ptx::tma_load_2d(sdO + sq * Cfg::kQBytes + c * Cfg::kQChunk, &tm_do, &qdo_full[sq], h * HD + 64 * c,
+                           row0 + q0);
+        }
+        ptx::bulk_load(sL + sq * QT, gLq + q0, QT * 4, &qdo_full[sq]);
+        ptx::bulk_load(sD + sq * QT, gDq + q0, QT * 4, &qdo_full[sq]);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, QT, false, false);   // S^T, dP^T
+    constexpr uint32_t id_acc = ptx::idesc_bf16_f32(128, HD, false, true);  // dV, dK
+    constexpr uint32_t id_dq = ptx::idesc_bf16_f32(128, QT, true, true);    // dQ^T halves
+    const uint32_t u0 = (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + 1023u) & ~1023u;
+    const uint32_t aK = u0, aV = u0 + Cfg::kKVBytes;
+    const uint32_t aQ0 = u0 + 2 * Cfg::kKVBytes, adO0 = aQ0 + QST * Cfg::kQBytes;
+    const uint32_t aP0 = adO0 + QST * Cfg::kQBytes, adS0 = aP0 + 2 * Cfg::kPBytes;
+    WAIT(kv_full, 0, 61);
+    auto stage2 = [&](int i) {
+      const int bb = i & 1, sq = i % QST;
+      WAIT(&pds_full[bb], (i >> 1) & 1, 62);
+      ptx::tc_fence_after();
+      const uint32_t aQ = aQ0 + sq * Cfg::kQBytes, adO = adO0 + sq * Cfg::kQBytes;
+      const uint32_t aP = aP0 + bb * Cfg::kPBytes, adS = adS0 + bb * Cfg::kPBytes;
+#pragma unroll
+      for (int kk = 0; kk < QT / 16; ++kk) {  // K = 32 query rows
+        const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+        ptx::mma_bf16_ss_w(tdV, ptx::smem_desc_sw64(aP + kk * 32, 16, 512),
+                           ptx::smem_desc_sw128(adO + kk * 2048, Cfg::kQChunk, 1024), id_acc, acc);
+        ptx::mma_bf16_ss_w(tdK, ptx::smem_desc_sw64(adS + kk * 32, 16, 512),
+                           ptx::smem_desc_sw128(aQ + kk * 2048, Cfg::kQChunk, 1024), id_acc, acc);
+      }
+      if (i > 0) WAIT(dq_free, (i - 1) & 1, 63);  // dQ^T_{i-1} read out of TMEM
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {  // K = 128 kv rows
+        const uint64_t bdesc = ptx::smem_desc_sw64(adS + kk * 1024, 512, 512);
+        ptx::mma_bf16_ss_w(tDQa, ptx::smem_desc_sw128(aK + kk * 2048, TB, 1024), bdesc, id_dq, kk > 0 ? 1u : 0u);
+        ptx::mma_bf16_ss_w(tDQb, ptx::smem_desc_sw128(aK + 2 * TB + kk * 2048, TB, 1024), bdesc, id_dq,
+                           kk > 0 ? 1u : 0u);
+      }
+      ptx::mma_commit_w(dq_full);
+      ptx::mma_commit_w(&qdo_empty[sq]);
+      ptx::mma_commit_w(&pds_free[bb]);
+    };
+    for (int j = 0; j < n_it; ++j) {
+      const int bb = j & 1, sq = j % QST;
+      WAIT(&qdo_full[sq], (j / QST) & 1, 64);
+      if (j >= 2) WAIT(&st_free[bb], ((j - 2) >> 1) & 1, 65);  // tile j-2 read buffer bb out
+      ptx::tc_fence_after();
+      const uint32_t aQ = aQ0 + sq * Cfg::kQBytes, adO = adO0 + sq * Cfg::kQBytes;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const uint32_t ak = (kk / 4) * TB + (kk % 4) * 32, aq = (kk / 4) * Cfg::kQChunk + (kk % 4) * 32;
+        ptx::mma_bf16_ss_w(tS + bb * QT, ptx::smem_desc_sw128(aK + ak, 16, 1024),
+                           ptx::smem_desc_sw128(aQ + aq, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+        ptx::mma_bf16_ss_w(tdP + bb * QT, ptx::smem_desc_sw128(aV + ak, 16, 1024),
+                           ptx::smem_desc_sw128(adO + aq, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+      }
+      ptx::mma_commit_w(&s_full[bb]);
+      if (j > 0) stage2(j - 1);
+    }
+    stage2(n_it - 1);
+    ptx::mma_commit_w(kdv_full);
+  } else if (wg == 3) {
+    // dQ^T (lane = head dim, column = query) -> fp32 reductions into dq_acc; the head dims
+    // 128..159 (lanes 0..31 of the second half) are flushed by the quarter-0 warp.
+    const int quarter = warp & 3;
+    const uint32_t lb = static_cast<uint32_t>(quarter * 32) << 16;
+    for (int i = 0; i < n_it; ++i) {
+      const int q0 = (qt_first + i) * QT;
+      float* dst = dq_acc + static_cast<size_t>(row0 + q0) * dt + h * HD + quarter * 32 + lane;
+      WAIT(dq_full, i & 1, 66);
+      ptx::tc_fence_after();
+      uint32_t va[32], vb[32];
+      ptx::tmem_ld_32x32b_x32(tDQa + lb, va);
+      if (quarter == 0) ptx::tmem_ld_32x32b_x32(tDQb, vb);
+      ptx::tmem_ld_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(dq_free);
+#pragma unroll
+      for (int e = 0; e < QT; ++e) atomicAdd(dst + static_cast<size_t>(e) * dt, __uint_as_float(va[e]));
+      if (quarter == 0) {
+        float* dst_b = dst + 128;
+#pragma unroll
+        for (int e = 0; e < QT; ++e) atomicAdd(dst_b + static_cast<size_t>(e) * dt, __uint_as_float(vb[e]));
+      }
+    }
+  } else {  // wg 1 / 2: P^T, dS^T of the even / odd query tiles
+    const int bb = wg - 1;
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;  // TMEM lane = kv row of this KV block
+    const uint32_t lb = static_cast<uint32_t>(quarter * 32) << 16;
+    const int sw = (r >> 1) & 3;        // SWIZZLE_64B: 16-byte unit u of row r sits at u ^ ((r >> 1) & 3)
+    for (int j = bb; j < n_it; j += 2) {
+      const int sq = j % QST;
+      const int q0 = (qt_first + j) * QT;
+      WAIT(&s_full[bb], (j >> 1) & 1, 67);
+      WAIT(&qdo_full[sq], (j / QST) & 1, 68);  // LSE / D rows of this tile
+      ptx::tc_fence_after();
+      uint32_t sv[32], dv[32];
+      ptx::tmem_ld_32x32b_x32(tS + lb + bb * QT, sv);
+      ptx::tmem_ld_32x32b_x32(tdP + lb + bb * QT, dv);
+      ptx::tmem_ld_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&st_free[bb]);
+      const float4* L4 = reinterpret_cast<const float4*>(sL + sq * QT);
+      const float4* D4 = reinterpret_cast<const float4*>(sD + sq * QT);
+      uint32_t pk[16], dk[16];
+#pragma unroll
+      for (int e4 = 0; e4 < 8; ++e4) {
+        const float4 l4 = L4[e4], d4 = D4[e4];
+        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dvv[4] = {d4.x, d4.y, d4.z, d4.w};
+        float pp[4], ds[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          pp[k] = ex2(fmaf(__uint_as_float(sv[4 * e4 + k]), scale_log2, -lv[k]));
+          ds[k] = pp[k] * (__uint_as_float(dv[4 * e4 + k]) - dvv[k]);
+        }
+        pk[2 * e4] = ptx::pack_bf16(pp[0], pp[1]);
+        pk[2 * e4 + 1] = ptx::pack_bf16(pp[2], pp[3]);
+        dk[2 * e4] = ptx::pack_bf16(ds[0], ds[1]);
+        dk[2 * e4 + 1] = ptx::pack_bf16(ds[2], ds[3]);
+      }
+      if (q0 < kv0 + r) {  // near the diagonal: queries before this kv row see nothing
+#pragma unroll
+        for (int e = 0; e < QT; ++e)
+          if (q0 + e < kv0 + r) {
+            pk[e / 2] &= (e & 1) ? 0x0000FFFFu : 0xFFFF0000u;
+            dk[e / 2] &= (e & 1) ? 0x0000FFFFu : 0xFFFF0000u;
+          }
+      }
+      WAIT(&pds_free[bb], ((j >> 1) & 1) ^ 1, 69);  // stage 2 of tile j-2 done with this buffer
+      uint8_t* prow = sPT + bb * Cfg::kPBytes + r * 64;
+      uint8_t* drow = sdST + bb * Cfg::kPBytes + r * 64;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int off = (u ^ sw) * 16;
+        *reinterpret_cast<uint4*>(prow + off) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        *reinterpret_cast<uint4*>(drow + off) = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+      }
+      ptx::fence_proxy_async();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&pds_full[bb]);
+    }
+    // dK (scaled) and dV rows of this KV block: WG1 columns [0, 96), WG2 [96, 160)
+    WAIT(kdv_full, 0, 70);
+    ptx::tc_fence_after();
+    __nv_bfloat16* krow = dqkv + static_cast<size_t>(row0 + kv0 + r) * 3 * dt + dt + h * HD;
+    __nv_bfloat16* vrow = krow + dt;
+    constexpr int NCH = HD / 32, SPLIT = (NCH + 1) / 2;
+#pragma unroll 1
+    for (int c = bb == 0 ? 0 : SPLIT; c < (bb == 0 ? SPLIT : NCH); ++c) {
+      uint32_t kv[32], vv[32];
+      ptx::tmem_ld_32x32b_x32(tdK + lb + c * 32, kv);
+      ptx::tmem_ld_32x32b_x32(tdV + lb + c * 32, vv);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 a, bb2;
+        a.x = ptx::pack_bf16(__uint_as_float(kv[8 * q]) * scale, __uint_as_float(kv[8 * q + 1]) * scale);
+        a.y = ptx::pack_bf16(__uint_as_float(kv[8 * q + 2]) * scale, __uint_as_float(kv[8 * q + 3]) * scale);
+        a.z = ptx::pack_bf16(__uint_as_float(kv[8 * q + 4]) * scale, __uint_as_float(kv[8 * q + 5]) * scale);
+        a.w = ptx::pack_bf16(__uint_as_float(kv[8 * q + 6]) * scale, __uint_as_float(kv[8 * q + 7]) * scale);
+        bb2.x = ptx::pack_bf16(__uint_as_float(vv[8 * q]), __uint_as_float(vv[8 * q + 1]));
+        bb2.y = ptx::pack_bf16(__uint_as_float(vv[8 * q + 2]), __uint_as_float(vv[8 * q + 3]));
+        bb2.z = ptx::pack_bf16(__uint_as_float(vv[8 * q + 4]), __uint_as_float(vv[8 * q + 5]));
+        bb2.w = ptx::pack_bf16(__uint_as_float(vv[8 * q + 6]), __uint_as_float(vv[8 * q + 7]));
+        reinterpret_cast<uint4*>(krow + c * 32)[q] = a;
+        reinterpret_cast<uint4*>(vrow + c * 32)[q] = bb2;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int HD>
+int bwd_tc3(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* D,
+            float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st) {
+  using Cfg = TcBwd3Cfg<HD>;
+  if (ensure_dynamic_smem(reinterpret_cast<const void*>(fa_bwd_tc3_kernel<HD>), Cfg::kSmem) != 0) return 3;
+  count_variant(KV_ATTN_BWD_HD160);
+  const int dt = a.heads * HD;
+  const uint64_t M = static_cast<uint64_t>(a.batch) * a.seq;
+  CUtensorMap tkv, tq, tdo;
+  if (!make_tmap_bf16(&tkv, qkv, 3 * static_cast<uint64_t>(dt), M, 3 * dt, 64, 128)) return 3;
+  if (!make_tmap_bf16(&tq, qkv, 3 * static_cast<uint64_t>(dt), M, 3 * dt, 64, Cfg::QT)) return 3;
+  if (!make_tmap_bf16(&tdo, dout, static_cast<uint64_t>(dt), M, dt, 64, Cfg::QT)) return 3;
+  dim3 grid(a.seq / 128, a.batch * a.heads);
+  const float scale = 1.f / sqrtf(static_cast<float>(HD));
+  launch_pdl(fa_bwd_tc3_kernel<HD>, grid, dim3(512), Cfg::kSmem, st, tkv, tq, tdo, lse, D, dq_acc, dqkv, a.seq,
+             a.heads, scale * kLog2e, scale);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+// Backward preprocessing when D was not produced by the W_o dgrad epilogue: D[b,h,q] =
+// sum_c dO[q,c] * O[q,c] (one warp per (row, head)) and the fp32 dQ accumulator zeroed.
+template <int HD>
+__global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                                    float* __restrict__ D, float* __restrict__ dq_acc, int s, int ht, int M) {
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  const int dt = ht * HD;
+  if (wg >= M * ht) return;
+  const int row = wg / ht, h = wg % ht;
+  const __nv_bfloat16* op = o + static_cast<size_t>(row) * dt + h * HD;
+  const __nv_bfloat16* dp = dout + static_cast<size_t>(row) * dt + h * HD;
+  float acc = 0.f;
+  for (int c = lane * 2; c < HD; c += 64) {
+    const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(op + c));
+    const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dp + c));
+    acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) D[(static_cast<size_t>(row / s) * ht + h) * s + row % s] = acc;
+  float* dqa = dq_acc + static_cast<size_t>(row) * dt + h * HD;
+  for (int c = lane; c < HD; c += 32) dqa[c] = 0.f;
+}
+
+// dQ = scale * dq_acc (fp32) -> bf16 into the q section of dqkv.
+__global__ void attn_dq_convert_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, int M,
+                                       int dt, float scale) {
+  const size_t n = static_cast<size_t>(M) * dt / 4;
+  const int ldq = 3 * dt;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t e = i * 4, row = e / dt, col = e % dt;
+    const float4 v = reinterpret_cast<const float4*>(dq_acc)[i];
+    uint2 pk;
+    pk.x = ptx::pack_bf16(v.x * scale, v.y * scale);
+    pk.y = ptx::pack_bf16(v.z * scale, v.w * scale);
+    *reinterpret_cast<uint2*>(dqkv + row * ldq + col) = pk;
+  }
+}
+
 template <int HD>
 int bwd_tc2(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* D,
             float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st) {
@@ -1561,12 +1938,14 @@ int fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, flo
   if (ensure_dynamic_smem(reinterpret_cast<const void*>(fa_fwd_tc_kernel<HD>), Cfg::kSmem) != 0) return 3;
   count_variant(KV_ATTN_FWD_PER_BLOCK);
   const int dt = a.heads * HD;
-  CUtensorMap tm;
-  if (!make_tmap_bf16(&tm, qkv, 3 * static_cast<uint64_t>(dt), static_cast<uint64_t>(a.batch) * a.seq, 3 * dt, 64, 128))
+  CUtensorMap tm, tt;
+  const uint64_t M = static_cast<uint64_t>(a.batch) * a.seq;
+  if (!make_tmap_bf16(&tm, qkv, 3 * static_cast<uint64_t>(dt), M, 3 * dt, 64, 128)) return 3;
+  if (Cfg::TAIL ? !make_tmap_bf16_sw64(&tt, qkv, 3 * static_cast<uint64_t>(dt), M, 3 * dt, Cfg::TAIL, 128) : (tt = tm, false))
     return 3;
   dim3 grid(a.seq / kBM, a.batch * a.heads);
-  fa_fwd_tc_kernel<HD><<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(tm, out, lse, a.seq, a.heads,
-                                                       kLog2e / sqrtf(static_cast<float>(HD)));
+  launch_pdl(fa_fwd_tc_kernel<HD>, grid, dim3(Cfg::kThreads), Cfg::kSmem, st, tm, tt, out, lse, a.seq, a.heads,
+             kLog2e / sqrtf(static_cast<float>(HD)));
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
@@ -1587,8 +1966,33 @@ int flash_attn_bwd_tc_main(const AttnShape& a, const __nv_bfloat16* qkv, const _
       return per_block ? bwd_tc2<128>(a, qkv, dout, lse, D, dq_acc, dqkv, st)
                        : bwd_tc2_persistent<128>(a, qkv, dout, lse, D, dq_acc, dqkv, st);
     }
+    case 160: return bwd_tc3<160>(a, qkv, dout, lse, D, dq_acc, dqkv, st);
     default: return 1;
   }
+}
+
+int flash_attn_fwd(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, cudaStream_t st) {
+  return flash_attn_fwd_tc(a, qkv, out, lse, st);
+}
+
+int flash_attn_bwd(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout,
+                   const float* lse, float* D, float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st, bool d_ready) {
+  if (a.seq % 128 != 0) return 1;
+  const int hd = a.head_dim;
+  if (hd != 64 && hd != 128 && hd != 160) return 1;
+  const int M = a.batch * a.seq, dt = a.heads * hd;
+  if (d_ready && hd == 128) {
+    cudaMemsetAsync(dq_acc, 0, static_cast<size_t>(M) * dt * sizeof(float), st);
+  } else {
+    const int warps = M * a.heads, grid = (warps + 7) / 8;
+    if (hd == 64) attn_bwd_pre_kernel<64><<<grid, 256, 0, st>>>(out, dout, D, dq_acc, a.seq, a.heads, M);
+    if (hd == 128) attn_bwd_pre_kernel<128><<<grid, 256, 0, st>>>(out, dout, D, dq_acc, a.seq, a.heads, M);
+    if (hd == 160) attn_bwd_pre_kernel<160><<<grid, 256, 0, st>>>(out, dout, D, dq_acc, a.seq, a.heads, M);
+  }
+  const int r = flash_attn_bwd_tc_main(a, qkv, dout, lse, D, dq_acc, dqkv, st);
+  if (r != 0) return r;
+  attn_dq_convert_kernel<<<8 * device_sm_count(), 256, 0, st>>>(dq_acc, dqkv, M, dt, 1.f / sqrtf(static_cast<float>(hd)));
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
 int flash_attn_fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, cudaStream_t st) {

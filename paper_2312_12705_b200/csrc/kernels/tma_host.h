@@ -12,6 +12,10 @@ namespace gptb200 {
 bool make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
                     uint32_t box_inner, uint32_t box_outer);
 
+// Same with 64B swizzle (box_inner * 2 <= 64): the 32-column tail chunk of a 160-wide head.
+bool make_tmap_bf16_sw64(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+                         uint32_t box_inner, uint32_t box_outer);
+
 // 2D fp32 tensor map [outer][inner] (ld in elements), box {box_inner, box_outer}; no swizzle by
 // default, 128B swizzle with sw128 (box_inner * 4 == 128).
 bool make_tmap_f32(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,

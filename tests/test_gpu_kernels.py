@@ -83,7 +83,8 @@ def _attn_ref(qkv, b, s, h, hd):
 
 
 # (8, 2048, 8, 128) has > 6 (kv block, head) items per SM: per-block backward; the others persistent
-@pytest.mark.parametrize("b,s,h,hd", [(2, 128, 4, 64), (1, 512, 2, 128), (2, 256, 2, 160), (1, 2048, 2, 128),
+@pytest.mark.parametrize("b,s,h,hd", [(2, 128, 4, 64), (1, 512, 2, 128), (2, 256, 2, 160), (1, 2048, 4, 160),
+                                      (2, 384, 3, 160), (1, 2048, 2, 128),
                                       (8, 2048, 8, 128)])
 def test_flash_attention_fwd_bwd_vs_torch(b, s, h, hd):
     g = torch.Generator(device=DEV).manual_seed(2)

@@ -42,4 +42,6 @@ if __name__ == "__main__":
     run(which=which)
     run(b=4, s=2048, h=6, hd=128, which=which)
     run(b=2, s=2048, h=5, hd=160, which=which)
+    run(b=1, s=2048, h=40, hd=160, which=which)  # GPT-1T shape, TP4: 40 heads per rank
+    run(b=1, s=2048, h=20, hd=160, which=which)  # GPT-1T shape, TP8
     run(b=2, s=256, h=4, hd=64, which=which)
