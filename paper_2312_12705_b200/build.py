@@ -18,6 +18,13 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = PKG / "build"
 LIB = PKG / "lib" / "libtrainplan_b200.so"
+# Debug variant (experiments only; loaded with GPTB200_LIB=<path>): GPTB200_NVCC_EXTRA="-DGPTB200_DEBUG_HANG"
+# turns every mbarrier wait of the attention kernels into a bounded wait that prints the stuck
+# barrier and traps instead of hanging.
+_EXTRA = os.environ.get("GPTB200_NVCC_EXTRA", "").split()
+if _EXTRA:
+    BUILD = PKG / "build_debug"
+    LIB = PKG / "lib_debug" / "libtrainplan_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
@@ -48,7 +55,7 @@ def _compile(src: Path, hdr_mtime: float) -> Path:
     obj = BUILD / (src.relative_to(CSRC).as_posix().replace("/", "__") + ".o")
     if obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_mtime):
         return obj
-    cmd = [NVCC, *ARCH, *COMMON, "-c", str(src), "-o", str(obj)]
+    cmd = [NVCC, *ARCH, *COMMON, *_EXTRA, "-c", str(src), "-o", str(obj)]
     if src.suffix == ".cpp":
         cmd[1:1] = ["-x", "cu"]
     r = subprocess.run(cmd, capture_output=True, text=True)

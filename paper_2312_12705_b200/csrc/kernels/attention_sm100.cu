@@ -1505,7 +1505,7 @@ __global__ void __launch_bounds__(512, 1)
 // K6 for head dim 160 (the 1T shape) on tcgen05. At 64-query tiles TMEM cannot hold S^T, dP^T
 // and dQ^T next to the 2 x 160 accumulator columns of dV and dK, so the query tile is 32 rows and
 // every transient buffer is double-buffered:
-//   S^T x2 (2x32) | dP^T x2 (2x32) | dQ^T hd 0-127 (32) | dQ^T hd 128-159 (32) | dV (160) | dK (160)
+//   dV (0..159) | S^T x2 | dQ^T hd 0-127 || dK (256..415) | dP^T x2 | dQ^T hd 128-159
 // = 512 columns. dQ^T = K^T dS^T has M = 160 rows: two M = 128 MMAs, the second over head dims
 // 128..255 of the K tile — rows 160..255 read the next 96 columns of shared memory (the rest of
 // the K tile's third swizzle chunk, then the V tile: finite data) and are never loaded from TMEM.
@@ -1527,7 +1527,7 @@ struct TcBwd3Cfg {
   static constexpr int kPBytes = 128 * QT * 2;      // [128 kv][32 q], 64-byte rows
   static constexpr int QST = 3;                     // Q / dO / LSE / D ring depth
   static constexpr int kSmem = 2 * kKVBytes + 2 * QST * kQBytes + 4 * kPBytes + QST * 2 * QT * 4 + 1024 + 256;
-  static_assert(HD > 128 && HD <= 192 && HD % 16 == 0, "two M = 128 dQ^T MMAs cover head dims 0..255");
+  static_assert(HD > 128 && HD <= 160 && HD % 32 == 0, "two M = 128 dQ^T MMAs cover head dims 0..255; TMEM map");
   static_assert(kSmem <= 232448, "smem over the 227 KB opt-in limit");
 };
 
@@ -1598,8 +1598,9 @@ __global__ void __launch_bounds__(512, 1)
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   pdl_trigger();
   pdl_wait();
-  const uint32_t tS = tmem, tdP = tmem + 2 * QT, tDQa = tmem + 4 * QT, tDQb = tmem + 5 * QT, tdV = tmem + 6 * QT,
-                 tdK = tdV + HD;
+  // accumulators on 256-column boundaries, the 32-column transients in the gaps
+  const uint32_t tdV = tmem, tdK = tmem + 256, tS = tmem + HD, tDQa = tmem + HD + 2 * QT, tdP = tmem + 256 + HD,
+                 tDQb = tmem + 256 + HD + 2 * QT;
   const int wg = warp / 4;
 
   if (warp == 0) {
@@ -1705,7 +1706,7 @@ __global__ void __launch_bounds__(512, 1)
         for (int e = 0; e < QT; ++e) atomicAdd(dst_b + static_cast<size_t>(e) * dt, __uint_as_float(vb[e]));
       }
     }
-  } else {  // wg 1 / 2: P^T, dS^T of the even / odd query tiles
+  } else if (wg == 1 || wg == 2) {  // P^T, dS^T of the even / odd query tiles (warps 2-3 idle)
     const int bb = wg - 1;
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;  // TMEM lane = kv row of this KV block
@@ -1813,9 +1814,10 @@ int bwd_tc3(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* d
   if (!make_tmap_bf16(&tdo, dout, static_cast<uint64_t>(dt), M, dt, 64, Cfg::QT)) return 3;
   dim3 grid(a.seq / 128, a.batch * a.heads);
   const float scale = 1.f / sqrtf(static_cast<float>(HD));
-  launch_pdl(fa_bwd_tc3_kernel<HD>, grid, dim3(512), Cfg::kSmem, st, tkv, tq, tdo, lse, D, dq_acc, dqkv, a.seq,
-             a.heads, scale * kLog2e, scale);
-  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+  const cudaError_t e = launch_pdl(fa_bwd_tc3_kernel<HD>, grid, dim3(512), Cfg::kSmem, st, tkv, tq, tdo, lse, D,
+                                   dq_acc, dqkv, a.seq, a.heads, scale * kLog2e, scale);
+  if (e != cudaSuccess) std::fprintf(stderr, "fa_bwd_tc3 launch: %s\n", cudaGetErrorString(e));
+  return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
 // Backward preprocessing when D was not produced by the W_o dgrad epilogue: D[b,h,q] =
@@ -1989,8 +1991,17 @@ int flash_attn_bwd(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bflo
     if (hd == 128) attn_bwd_pre_kernel<128><<<grid, 256, 0, st>>>(out, dout, D, dq_acc, a.seq, a.heads, M);
     if (hd == 160) attn_bwd_pre_kernel<160><<<grid, 256, 0, st>>>(out, dout, D, dq_acc, a.seq, a.heads, M);
   }
+  static const bool dbg = std::getenv("GPTB200_ATTN_SYNC_DEBUG") != nullptr;  // locate a faulting launch
+  if (dbg && cudaStreamSynchronize(st) != cudaSuccess) {
+    std::fprintf(stderr, "attention bwd: preprocessing failed: %s\n", cudaGetErrorString(cudaGetLastError()));
+    return 3;
+  }
   const int r = flash_attn_bwd_tc_main(a, qkv, dout, lse, D, dq_acc, dqkv, st);
   if (r != 0) return r;
+  if (dbg && cudaStreamSynchronize(st) != cudaSuccess) {
+    std::fprintf(stderr, "attention bwd: main kernel failed: %s\n", cudaGetErrorString(cudaGetLastError()));
+    return 3;
+  }
   attn_dq_convert_kernel<<<8 * device_sm_count(), 256, 0, st>>>(dq_acc, dqkv, M, dt, 1.f / sqrtf(static_cast<float>(hd)));
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }

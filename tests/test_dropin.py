@@ -96,7 +96,7 @@ def test_measured_evaluator_drives_reference_search(tmp_path, native_lib):
     assert out["best_objective"] == max(h["objective"] for h in ok)
     # the reference's calibrate fitted to measured B200 points
     assert out["observations"] == len(ok)
-    assert 0.05 <= out["calibrated_kernel_efficiency"] <= 1.0
+    assert 0.2 <= out["calibrated_kernel_efficiency"] <= 1.0
     assert out["oom_failure"] == "oom"
     P = out["executed_params"]
     meas = out["measured_mem"]
