@@ -16,3 +16,11 @@ if [ "$N" -ge 4 ] && [ -n "${LOOP_1T:-}" ]; then
     tail -c 600 gpurun_out/${tag}_1t_$i.json
   done
 fi
+if [ -n "${NCU_ATTN:-}" ]; then
+  python tools/run_attn_shape.py 1 2048 40 160 bwd 2 && python tools/run_attn_shape.py 8 2048 16 128 bwd 2 && \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:fa_bwd -c 2 -o gpurun_out/${NCU_ATTN}_hd160 \
+     python tools/run_attn_shape.py 1 2048 40 160 bwd 2 > gpurun_out/${NCU_ATTN}_hd160.log 2>&1 && \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:fa_bwd -c 2 -o gpurun_out/${NCU_ATTN}_hd128 \
+     python tools/run_attn_shape.py 8 2048 16 128 bwd 2 > gpurun_out/${NCU_ATTN}_hd128.log 2>&1
+  echo "ncu rc $?"
+fi
