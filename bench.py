@@ -351,7 +351,7 @@ def main():
         # the other kernel families against their own roofline (tensor for attention, HBM for norms)
         classes = {"attn_fwd": ("tensor", "bf16_tflops_sustained", "TFLOP/s"),
                    "attn_bwd": ("tensor", "bf16_tflops_sustained", "TFLOP/s"),
-                   "norm": ("hbm", "hbm_gbs", "GB/s"), "adam": ("hbm", "hbm_gbs", "GB/s")}
+                   "norm": ("hbm", "hbm_gbs", "GB/s")}
         line["roofline_by_class"] = {}
         for k, (bound, pk, unit) in classes.items():
             v = kt[k]

@@ -15,7 +15,10 @@
  *     search.hpp:59 FailureKind::Oom).
  *   - Kernel-level entries take device pointers and a cudaStream_t passed as void*; they are
  *     stream-ordered and asynchronous. Session entries own their device memory and streams.
- *   - A session is bound to one host thread and one GPU (one process per GPU).
+ *   - A session is bound to one host thread and one GPU (one process per GPU is the supported
+ *     layout). Per-kernel attributes and SM counts are cached per device (thread-safe), so sessions
+ *     on different GPUs of one process also work; the launch-variant counters and the GEMM
+ *     tile-choice test hook (tp_gemm_force_cta_group) are process-wide.
  */
 #ifndef TRAINPLAN_CAPI_H_
 #define TRAINPLAN_CAPI_H_
