@@ -23,8 +23,9 @@ LIB = PKG / "lib" / "libtrainplan_b200.so"
 # barrier and traps instead of hanging.
 _EXTRA = os.environ.get("GPTB200_NVCC_EXTRA", "").split()
 if _EXTRA:
-    BUILD = PKG / "build_debug"
-    LIB = PKG / "lib_debug" / "libtrainplan_b200.so"
+    _DBG = os.environ.get("GPTB200_DEBUG_DIR", "lib_debug")
+    BUILD = PKG / f"build_{_DBG}"
+    LIB = PKG / _DBG / "libtrainplan_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",

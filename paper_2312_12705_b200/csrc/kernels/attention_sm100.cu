@@ -20,6 +20,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 namespace gptb200 {
 
@@ -46,6 +47,23 @@ __device__ __forceinline__ void dwait(uint64_t* bar, uint32_t parity, int id) {
 #define WAIT(bar, par, id) dwait(bar, par, id)
 #else
 #define WAIT(bar, par, id) ptx::mbar_wait(bar, par)
+#endif
+// Timeline instrumentation of the backward kernels (debug builds only, -DGPTB200_ATTN_TRACE):
+// clock64 stamps of one CTA's role events per query tile, dumped by the launcher to
+// $GPTB200_ATTN_TRACE. Compiles to nothing in the release library.
+#ifdef GPTB200_ATTN_TRACE
+__device__ unsigned long long* g_attn_trace = nullptr;
+constexpr int kTraceTiles = 64, kTraceEv = 24;
+#define ATTN_TRACE(ev, j)                                                                              \
+  do {                                                                                                 \
+    if (g_attn_trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 &&   \
+        (j) < kTraceTiles)                                                                             \
+      g_attn_trace[(j) * kTraceEv + (ev)] = clock64();                                                \
+  } while (0)
+#else
+#define ATTN_TRACE(ev, j) \
+  do {                    \
+  } while (0)
 #endif
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -641,6 +659,7 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
 }
 
 
+
 template <int HD>
 __global__ void __launch_bounds__(320, 1)
     fa_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
@@ -907,6 +926,7 @@ struct TcBwd2Cfg {
   static constexpr int kPBytes = 128 * 128;            // [128 kv][64 q]
   static constexpr int QST = 3;                        // Q/dO (+ LSE/D) ring depth
   static constexpr int kSmem = 2 * kKVBytes + 2 * QST * kQBytes + 4 * kPBytes + QST * 2 * 64 * 4 + 1024 + 256;
+  static_assert(kSmem <= 232448, "smem over the 227 KB opt-in limit");
 };
 
 template <int HD>
@@ -1020,7 +1040,9 @@ __global__ void __launch_bounds__(512, 1)
       WAIT(kv_full, 0, 41);
       auto stage2 = [&](int i) {
         const int bb = i & 1, sq = i % QST;
+        ATTN_TRACE(3, i);
         WAIT(&pds_full[bb], (i >> 1) & 1, 42);
+        ATTN_TRACE(4, i);
         ptx::tc_fence_after();
         const uint32_t aQ = aQ0 + sq * Cfg::kQBytes, adO = adO0 + sq * Cfg::kQBytes;
         const uint32_t aP = aP0 + bb * Cfg::kPBytes, adS = adS0 + bb * Cfg::kPBytes;
@@ -1033,6 +1055,7 @@ __global__ void __launch_bounds__(512, 1)
                            ptx::smem_desc_sw128(aQ + kk * 2048, 8192, 1024), id_acc, acc);
         }
         if (i > 0) WAIT(dq_free, (i - 1) & 1, 44);  // dQ^T_{i-1} read out of its TMEM columns
+        ATTN_TRACE(5, i);
         ptx::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // K = 128 kv rows
@@ -1041,13 +1064,16 @@ __global__ void __launch_bounds__(512, 1)
         ptx::mma_commit_w(dq_full);
         ptx::mma_commit_w(&qdo_empty[sq]);
         ptx::mma_commit_w(&pds_free[bb]);
+        ATTN_TRACE(6, i);
       };
       for (int j = 0; j < n_it; ++j) {
         const int bb = j & 1, sq = j % QST;
+        ATTN_TRACE(0, j);
         WAIT(&qdo_full[sq], (j / QST) & 1, 43);
         // S^T_{j-1} and dP^T_{j-1} loaded by the compute warps: dP^T is free, and so is S^T[bb]
         // (its previous tile j-2 was loaded before j-1)
         if (j >= 1) WAIT(&st_free[(j - 1) & 1], ((j - 1) >> 1) & 1, 50);
+        ATTN_TRACE(1, j);
         ptx::tc_fence_after();
         const uint32_t aQ = aQ0 + sq * Cfg::kQBytes, adO = adO0 + sq * Cfg::kQBytes;
 #pragma unroll
@@ -1059,6 +1085,7 @@ __global__ void __launch_bounds__(512, 1)
                            ptx::smem_desc_sw128(adO + aq, 16, 1024), id_s, kk > 0 ? 1u : 0u);
         }
         ptx::mma_commit_w(&s_full[bb]);
+        ATTN_TRACE(2, j);
         if (j > 0) stage2(j - 1);
       }
       stage2(n_it - 1);
@@ -1071,10 +1098,10 @@ __global__ void __launch_bounds__(512, 1)
     const int quarter = warp & 3;
     const uint32_t lb = static_cast<uint32_t>(quarter * 32) << 16;
     for (int i = 0; i < n_it; ++i) {
-      const int bb = i & 1;
       const int q0 = (qt_first + i) * 64;
-      float* dst = dq_acc + static_cast<size_t>(row0 + q0) * dt + h * HD + quarter * 32 + lane;
+      float* dst = dq_acc + static_cast<size_t>(row0 + q0) * dt + h * HD + quarter * 32;
       WAIT(dq_full, i & 1, 45);
+      if (quarter == 0) ATTN_TRACE(14, i);
       ptx::tc_fence_after();
 #pragma unroll
       for (int hq = 0; hq < 2; ++hq) {
@@ -1087,8 +1114,9 @@ __global__ void __launch_bounds__(512, 1)
           if (lane == 0) ptx::mbar_arrive(dq_free);
         }
 #pragma unroll
-        for (int e = 0; e < 32; ++e) atomicAdd(dst + static_cast<size_t>(hq * 32 + e) * dt, __uint_as_float(v[e]));
+        for (int e = 0; e < 32; ++e) atomicAdd(dst + static_cast<size_t>(hq * 32 + e) * dt + lane, __uint_as_float(v[e]));
       }
+      if (quarter == 0) ATTN_TRACE(15, i);
     }
   } else if (wg == 1 || wg == 2) {
     ptx::setmaxnreg_inc<192>();
@@ -1099,7 +1127,10 @@ __global__ void __launch_bounds__(512, 1)
     for (int j = 0; j < n_it; ++j) {
       const int bb = j & 1, sq = j % QST;
       const int q0 = (qt_first + j) * 64;
+      const bool tw = warp == 4;  // traced compute warp (half 0, quarter 0)
+      if (tw) ATTN_TRACE(8, j);
       WAIT(&s_full[bb], (j >> 1) & 1, 46);
+      if (tw) ATTN_TRACE(9, j);
       WAIT(&qdo_full[sq], (j / QST) & 1, 49);  // LSE / D rows of this tile (already complete)
       ptx::tc_fence_after();
       const int qc = half * 32;
@@ -1110,6 +1141,7 @@ __global__ void __launch_bounds__(512, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&st_free[bb]);  // S^T / dP^T of this tile consumed
+      if (tw) ATTN_TRACE(10, j);
       const float4* L4 = reinterpret_cast<const float4*>(sL + sq * 64 + qc);
       const float4* D4 = reinterpret_cast<const float4*>(sD + sq * 64 + qc);
       uint32_t pk[16], dk[16];
@@ -1136,7 +1168,9 @@ __global__ void __launch_bounds__(512, 1)
             dk[e / 2] &= (e & 1) ? 0x0000FFFFu : 0xFFFF0000u;
           }
       }
+      if (tw) ATTN_TRACE(11, j);
       WAIT(&pds_free[bb], ((j >> 1) & 1) ^ 1, 47);  // stage 2 of tile j-2 is done with buffer bb
+      if (tw) ATTN_TRACE(12, j);
       uint8_t* prow = sPT + bb * Cfg::kPBytes + r * 128;
       uint8_t* drow = sdST + bb * Cfg::kPBytes + r * 128;
 #pragma unroll
@@ -1149,6 +1183,7 @@ __global__ void __launch_bounds__(512, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&pds_full[bb]);
+      if (tw) ATTN_TRACE(13, j);
     }
     // dK (scaled) and dV rows of this KV block
     WAIT(kdv_full, 0, 48);
@@ -1380,7 +1415,7 @@ __global__ void __launch_bounds__(512, 1)
       const Item it = item(kidx);
       for (int i = 0; i < it.n_it; ++i, ++gt) {
         const int q0 = (it.qt_first + i) * 64;
-        float* dst = dq_acc + static_cast<size_t>(it.row0 + q0) * dt + it.h * HD + quarter * 32 + lane;
+        float* dst = dq_acc + static_cast<size_t>(it.row0 + q0) * dt + it.h * HD + quarter * 32;
         WAIT(dq_full, gt & 1, 45);
         ptx::tc_fence_after();
 #pragma unroll
@@ -1394,7 +1429,7 @@ __global__ void __launch_bounds__(512, 1)
             if (lane == 0) ptx::mbar_arrive(dq_free);
           }
 #pragma unroll
-          for (int e = 0; e < 32; ++e) atomicAdd(dst + static_cast<size_t>(hq * 32 + e) * dt, __uint_as_float(v[e]));
+          for (int e = 0; e < 32; ++e) atomicAdd(dst + static_cast<size_t>(hq * 32 + e) * dt + lane, __uint_as_float(v[e]));
         }
       }
     }
@@ -1682,13 +1717,13 @@ __global__ void __launch_bounds__(512, 1)
     stage2(n_it - 1);
     ptx::mma_commit_w(kdv_full);
   } else if (wg == 3) {
-    // dQ^T (lane = head dim, column = query) -> fp32 reductions into dq_acc; the head dims
-    // 128..159 (lanes 0..31 of the second half) are flushed by the quarter-0 warp.
+    // dQ^T (lane = head dim, column = query) -> fp32 reductions into dq_acc (one coalesced
+    // 128-byte request per query and 32 head dims); head dims 128..159 by the quarter-0 warp.
     const int quarter = warp & 3;
     const uint32_t lb = static_cast<uint32_t>(quarter * 32) << 16;
     for (int i = 0; i < n_it; ++i) {
       const int q0 = (qt_first + i) * QT;
-      float* dst = dq_acc + static_cast<size_t>(row0 + q0) * dt + h * HD + quarter * 32 + lane;
+      float* dst = dq_acc + static_cast<size_t>(row0 + q0) * dt + h * HD + quarter * 32;
       WAIT(dq_full, i & 1, 66);
       ptx::tc_fence_after();
       uint32_t va[32], vb[32];
@@ -1699,13 +1734,13 @@ __global__ void __launch_bounds__(512, 1)
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(dq_free);
 #pragma unroll
-      for (int e = 0; e < QT; ++e) atomicAdd(dst + static_cast<size_t>(e) * dt, __uint_as_float(va[e]));
+      for (int e = 0; e < QT; ++e) atomicAdd(dst + static_cast<size_t>(e) * dt + lane, __uint_as_float(va[e]));
       if (quarter == 0) {
-        float* dst_b = dst + 128;
 #pragma unroll
-        for (int e = 0; e < QT; ++e) atomicAdd(dst_b + static_cast<size_t>(e) * dt, __uint_as_float(vb[e]));
+        for (int e = 0; e < QT; ++e) atomicAdd(dst + static_cast<size_t>(e) * dt + 128 + lane, __uint_as_float(vb[e]));
       }
     }
+
   } else if (wg == 1 || wg == 2) {  // P^T, dS^T of the even / odd query tiles (warps 2-3 idle)
     const int bb = wg - 1;
     const int quarter = warp & 3;
@@ -1875,8 +1910,33 @@ int bwd_tc2(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* d
   if (!make_tmap_bf16(&tdo, dout, static_cast<uint64_t>(dt), M, dt, 64, 64)) return 3;
   dim3 grid(a.seq / 128, a.batch * a.heads);
   const float scale = 1.f / sqrtf(static_cast<float>(HD));
+#ifdef GPTB200_ATTN_TRACE
+  unsigned long long* tbuf = nullptr;
+  const char* tpath = std::getenv("GPTB200_ATTN_TRACE");
+  if (tpath) {
+    cudaMalloc(&tbuf, kTraceTiles * kTraceEv * 8);
+    cudaMemset(tbuf, 0, kTraceTiles * kTraceEv * 8);
+    cudaMemcpyToSymbol(g_attn_trace, &tbuf, sizeof(tbuf));
+  }
+#endif
   launch_pdl(fa_bwd_tc2_kernel<HD>, grid, dim3(512), Cfg::kSmem, st, tkv, tq, tdo, lse, D, dq_acc, dqkv, a.seq,
              a.heads, scale * kLog2e, scale);
+#ifdef GPTB200_ATTN_TRACE
+  if (tbuf) {
+    cudaStreamSynchronize(st);
+    std::vector<unsigned long long> h(kTraceTiles * kTraceEv);
+    cudaMemcpy(h.data(), tbuf, h.size() * 8, cudaMemcpyDeviceToHost);
+    if (FILE* f = std::fopen(tpath, "w")) {
+      for (int t = 0; t < kTraceTiles; ++t) {
+        for (int e = 0; e < kTraceEv; ++e) std::fprintf(f, "%llu%c", h[t * kTraceEv + e], e + 1 < kTraceEv ? ',' : '\n');
+      }
+      std::fclose(f);
+    }
+    unsigned long long* null = nullptr;
+    cudaMemcpyToSymbol(g_attn_trace, &null, sizeof(null));
+    cudaFree(tbuf);
+  }
+#endif
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
