@@ -250,6 +250,9 @@ int tp_session_debug_tp_allreduce(tp_session* s, const uint16_t* in, uint16_t* o
 /* Average device ms per allreduce over `iters` (ctas 0 = default grid); *nvls = 1 if the
  * session's TP group uses the NVLS kernel. */
 int tp_session_bench_tp_allreduce(tp_session* s, int iters, int mode, int ctas, float* ms, int* nvls);
+/* Average device ms of one sequence-parallel LayerNorm kernel (mode 0: NVLS reduce-scatter + LN +
+ * allgather forward, 1: backward) on the session's buffers, back to back (TP > 1 with SP only). */
+int tp_session_bench_sp(tp_session* s, int iters, int mode, float* ms);
 
 #ifdef __cplusplus
 }

@@ -108,6 +108,7 @@ SIGNATURES: dict[str, tuple] = {
     "tp_session_allreduce_max": (_i, [_vp, C.POINTER(_f)]),
     "tp_session_debug_tp_allreduce": (_i, [_vp, _vp, _vp, _i]),
     "tp_session_bench_tp_allreduce": (_i, [_vp, _i, _i, _i, C.POINTER(_f), C.POINTER(_i)]),
+    "tp_session_bench_sp": (_i, [_vp, _i, _i, C.POINTER(_f)]),
     "tp_session_set_timeout": (_i, [_vp, C.c_double]),
     "tp_session_memory": (_i, [_vp, _vp]),
     "tp_variant_counts": (_i, [C.POINTER(_i64)]),
@@ -378,6 +379,11 @@ class Session:
         out = np.empty_like(x)
         check(self._lib.tp_session_debug_tp_allreduce(self.h, x.ctypes.data, out.ctypes.data, mode))
         return out
+
+    def bench_sp(self, iters: int = 20, mode: int = 0) -> float:
+        ms = _f()
+        check(self._lib.tp_session_bench_sp(self.h, iters, mode, C.byref(ms)))
+        return ms.value
 
     def bench_tp_allreduce(self, iters: int = 20, mode: int = 0, ctas: int = 0):
         ms, nv = _f(), _i()

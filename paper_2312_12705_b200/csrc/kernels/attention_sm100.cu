@@ -2068,13 +2068,10 @@ int flash_attn_bwd(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bflo
 
 int flash_attn_fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, cudaStream_t st) {
   if (a.seq % kBM != 0) return 1;
-  // persistent CTAs win when (q block, head) items per SM are few (the snake assignment beats the
-  // block scheduler's tail and prologues overlap); with many items the per-block grid's dynamic
-  // scheduling wins (measured, microbench: 1x12 heads 523 vs 407 TF/s, 1x24 641 vs 524,
-  // 32x16 heads (1.4B MBS 32) 670 vs 766)
-  static const char* forced = std::getenv("GPTB200_ATTN_FWD_PER_BLOCK");  // A/B switch: 1 / 0
-  const int items = (a.seq / kBM) * a.batch * a.heads;
-  const bool per_block = forced ? forced[0] == '1' : items > 6 * device_sm_count();
+  // persistent CTAs for hd <= 128. In isolation the per-block grid wins at many items (1.4B MBS 32:
+  // 766 vs 670 TF/s) but inside the step it loses (530 vs 610 TF/s, same build and box class: the
+  // persistent CTAs' prologue overlap matters more behind the QKV GEMM), so it stays an A/B switch.
+  static const bool per_block = std::getenv("GPTB200_ATTN_FWD_PER_BLOCK") != nullptr;
   switch (a.head_dim) {
     case 64: return per_block ? fwd_tc<64>(a, qkv, out, lse, st) : fwd_tc_persistent<64>(a, qkv, out, lse, st);
     case 128: return per_block ? fwd_tc<128>(a, qkv, out, lse, st) : fwd_tc_persistent<128>(a, qkv, out, lse, st);

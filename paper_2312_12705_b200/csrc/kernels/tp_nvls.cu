@@ -88,6 +88,20 @@ __global__ void __launch_bounds__(kSpThreads) sp_ln_fwd_kernel(ncclDevComm dev, 
     const int R = a.row0 + i;
     const size_t goff = static_cast<size_t>(R) * d, loff = static_cast<size_t>(i) * d;
     const bf16* rsrc = a.resid_pos_table ? a.resid + static_cast<size_t>(R % a.seq) * d : a.resid + loff;
+    // issue every load of the row (the in-switch reductions take microseconds) before using any
+    uint4 yraw[VPT], rraw[VPT];
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+      const int c0 = (v * kSpThreads + threadIdx.x) * 8;
+      if (c0 >= d) break;
+      if (ymc) yraw[v] = mc_ld_reduce_bf16x8(reinterpret_cast<const uint4*>(ymc + goff + c0));
+    }
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+      const int c0 = (v * kSpThreads + threadIdx.x) * 8;
+      if (c0 >= d) break;
+      rraw[v] = *reinterpret_cast<const uint4*>(rsrc + c0);
+    }
     float h[VPT][8];
     float sum = 0.f;
 #pragma unroll
@@ -95,10 +109,10 @@ __global__ void __launch_bounds__(kSpThreads) sp_ln_fwd_kernel(ncclDevComm dev, 
       const int c0 = (v * kSpThreads + threadIdx.x) * 8;
       if (c0 >= d) break;
       float r[8];
-      unpack8(*reinterpret_cast<const uint4*>(rsrc + c0), r);
+      unpack8(rraw[v], r);
       if (ymc) {
         float y[8];
-        unpack8(mc_ld_reduce_bf16x8(reinterpret_cast<const uint4*>(ymc + goff + c0)), y);
+        unpack8(yraw[v], y);
         if (a.bias) {
           float b[8];
           unpack8(*reinterpret_cast<const uint4*>(a.bias + c0), b);
@@ -183,11 +197,18 @@ __global__ void __launch_bounds__(kSpThreads) sp_ln_bwd_kernel(ncclDevComm dev, 
     if (dymc) {
       const float mu = a.mean[i], rs = a.rstd[i];
       float s[2] = {0.f, 0.f};
+      uint4 dyraw[VPT];  // every in-switch reduction of the row in flight before the first use
 #pragma unroll
       for (int v = 0; v < VPT; ++v) {
         const int c0 = (v * kSpThreads + threadIdx.x) * 8;
         if (c0 >= d) break;
-        const uint4 dyv = mc_ld_reduce_bf16x8(reinterpret_cast<const uint4*>(dymc + goff + c0));
+        dyraw[v] = mc_ld_reduce_bf16x8(reinterpret_cast<const uint4*>(dymc + goff + c0));
+      }
+#pragma unroll
+      for (int v = 0; v < VPT; ++v) {
+        const int c0 = (v * kSpThreads + threadIdx.x) * 8;
+        if (c0 >= d) break;
+        const uint4 dyv = dyraw[v];
         *reinterpret_cast<uint4*>(dyloc + goff + c0) = dyv;  // reduced row kept for the column sums
         float x[8], dy[8], g[8];
         unpack8(dyv, dy);

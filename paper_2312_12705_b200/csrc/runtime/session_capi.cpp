@@ -228,6 +228,10 @@ int tp_session_debug_tp_allreduce(tp_session* s, const uint16_t* in, uint16_t* o
   return run("tp_session_debug_tp_allreduce", [&] { s->stage->debug_tp_allreduce(in, out, mode); });
 }
 
+int tp_session_bench_sp(tp_session* s, int iters, int mode, float* ms) {
+  return run("tp_session_bench_sp", [&] { *ms = s->stage->bench_sp(iters, mode); });
+}
+
 int tp_session_bench_tp_allreduce(tp_session* s, int iters, int mode, int ctas, float* ms, int* nvls) {
   return run("tp_session_bench_tp_allreduce", [&] {
     *ms = s->stage->bench_tp_allreduce(iters, mode, ctas);

@@ -1242,6 +1242,43 @@ float Stage::bench_tp_allreduce(int iters, int mode, int ctas) {
   return ms / std::max(iters, 1);
 }
 
+float Stage::bench_sp(int iters, int mode) {
+  if (!sp_) throw StepError{TP_ERR_UNSUPPORTED, "bench_sp: the session does not run sequence parallelism"};
+  LayerActs& A = acts_for(0, 0);
+  const LayerW W = w(0);
+  auto launch = [&] {
+    if (mode == 0) {
+      SpLnFwdArgs f;
+      f.nrows = Ms_, f.row0 = row0_, f.d = d_, f.seq = s_;
+      f.y_off = woff(tmp_md_), f.bias = W.bo, f.resid = slots_act_[0].h[0];
+      f.drop = drop_key(opts_, 1, 0, 0, 0, s_, d_);
+      f.h_out = A.hmid, f.gamma = W.ln2g, f.beta = W.ln2b, f.ln_off = woff(A.m2), f.mean = A.mu2, f.rstd = A.rs2;
+      sp_fwd(f);
+    } else {
+      SpLnBwdArgs g;
+      g.nrows = Ms_, g.row0 = row0_, g.d = d_, g.workspace = ws_;
+      g.dy_off = woff(dm_), g.x = A.hmid, g.gamma = W.ln2g, g.mean = A.mu2, g.rstd = A.rs2;
+      g.resid_grad = dh_[0], g.dx = dh_[0];
+      g.drop = drop_key(opts_, 1, 0, 0, 0, s_, d_);
+      g.dxd_off = woff(dy_), g.dgamma = gr(0).ln2g, g.dbeta = gr(0).ln2b, g.dbias = gr(0).bo;
+      sp_bwd(g);
+    }
+  };
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int i = 0; i < 3; ++i) launch();
+  cudaEventRecord(a, st_);
+  for (int i = 0; i < iters; ++i) launch();
+  cudaEventRecord(b, st_);
+  sync();
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return ms / std::max(iters, 1);
+}
+
 float Stage::allreduce_max(float v) {
   if (comms_.world == 1) return v;
   float* d = ws_;

@@ -124,6 +124,9 @@ class Stage {
   // mode 0 = automatic (NVLS when available), 1 = ncclAllReduce. in/out: M*d bf16 bit patterns.
   void debug_tp_allreduce(const uint16_t* in, uint16_t* out, int mode);
   float bench_tp_allreduce(int iters, int mode, int ctas);
+  // Average device ms of one sequence-parallel LayerNorm kernel on this session's buffers
+  // (mode 0: forward reduce-scatter + LN + allgather, 1: backward), back to back (microbenchmark).
+  float bench_sp(int iters, int mode);
   bool tp_uses_nvls() const { return comms_.tp_nvls != nullptr; }
   // 0: no TP; 1: ncclAllReduce; 2: NVLS allreduce kernel; 3: sequence parallel (fused NVLS norms)
   int tp_mode() const { return cfg_.tp == 1 ? 0 : (sp_ ? 3 : (comms_.tp_nvls ? 2 : 1)); }
