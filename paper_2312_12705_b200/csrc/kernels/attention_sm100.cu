@@ -1855,473 +1855,6 @@ int bwd_tc3(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* d
   return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
-// ---------------------------------------------------------------- backward, split form (hd 128)
-// K6 as two atomic-free passes with the stationary operands resident in TMEM as tcgen05 A
-// operands (so the tensor cores read only the streamed operand from shared memory):
-//   fa_bwd_dq_kernel  (Q-stationary) CTA = (128-row query block, head); Q and dO rows in TMEM;
-//     loops over 64-row KV tiles at or before the diagonal: S = Q K^T, dP = dO V^T (TMEM), the
-//     compute warps write dS = P (dP - D) back into TMEM (bf16 over S), dQ += dS K accumulates in
-//     TMEM and is written once as bf16 — no fp32 accumulator, no atomics, no conversion pass.
-//   fa_bwd_kv_kernel  (KV-stationary) CTA = (128-row KV block, head); K and V rows in TMEM; loops
-//     over 32-row query tiles at or after the diagonal: S^T = K Q^T, dP^T = V dO^T, P^T / dS^T
-//     written back into TMEM, dV += P^T dO and dK += dS^T Q from TMEM.
-// dQ costs a recompute of S and dP (7 GEMM passes instead of 5), in exchange every MMA streams one
-// operand from shared memory (<= 96 B/clk instead of ~200) and the L2 fp32 reduction of dQ goes.
-template <int HD>
-struct TcBwdQCfg {
-  static constexpr int NC = HD / 64;
-  static constexpr int KT = 64;                  // kv rows per tile
-  static constexpr int kTileBytes = KT * 128;    // [64 kv][64] bf16 chunk
-  static constexpr int kKVBytes = NC * kTileBytes;
-  static constexpr int ST = 3;                   // K / V ring depth
-  static constexpr int kSmem = 2 * ST * kKVBytes + 1024 + 256;
-};
-
-template <int HD>
-__global__ void __launch_bounds__(384, 1)
-    fa_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_kv, const __nv_bfloat16* __restrict__ qkv,
-                     const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse,
-                     const float* __restrict__ Dg, __nv_bfloat16* __restrict__ dqkv, int s, int ht,
-                     float scale_log2, float scale) {
-  using Cfg = TcBwdQCfg<HD>;
-  static_assert(HD == 128, "TMEM map: Q | dO | S x2 | dP x2 | dQ");
-  constexpr int NC = Cfg::NC, KT = Cfg::KT, ST = Cfg::ST, TB = Cfg::kTileBytes;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = ptx::smem_align1024(smem_raw);
-  uint8_t* sK = smem;                       // [ST][NC][64][64]
-  uint8_t* sV = sK + ST * Cfg::kKVBytes;    // [ST][NC][64][64]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + ST * Cfg::kKVBytes);
-  uint64_t* kv_full = bars;               // [ST]
-  uint64_t* kv_empty = kv_full + ST;      // [ST]
-  uint64_t* s_full = kv_empty + ST;       // [2] S_j, dP_j in TMEM
-  uint64_t* ds_full = s_full + 2;         // [2] dS_j written back (8 compute warps)
-  uint64_t* s_free = ds_full + 2;         // [2] dQ MMA consumed dS_j
-  uint64_t* ops_ready = s_free + 2;       // Q / dO rows in TMEM (8 warps)
-  uint64_t* dq_done = ops_ready + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
-
-  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
-  const int qb = gridDim.x - 1 - blockIdx.x;  // heaviest query blocks first
-  const int b = blockIdx.y / ht, h = blockIdx.y % ht;
-  const int dt = ht * HD;
-  const int row0 = b * s;
-  const int q0 = qb * 128;
-  const int n_kv = (q0 + 128) / KT;  // kv tiles at or before the diagonal
-
-  if (warp == 0 && lane == 0) {
-    ptx::tma_prefetch_desc(&tm_kv);
-    for (int i = 0; i < ST; ++i) {
-      ptx::mbar_init(&kv_full[i], 1);
-      ptx::mbar_init(&kv_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&ds_full[i], 8);
-      ptx::mbar_init(&s_free[i], 1);
-    }
-    ptx::mbar_init(ops_ready, 8);
-    ptx::mbar_init(dq_done, 1);
-    ptx::fence_mbar_init();
-  }
-  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
-  pdl_trigger();
-  pdl_wait();
-  // TMEM: Q (A operand, 64 cols) | dO (64) | S x2 (64 each) | dP x2 (64 each) | dQ (128)
-  const uint32_t tQ = tmem, tdO = tmem + 64, tS = tmem + 128, tdP = tmem + 256, tdQ = tmem + 384;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j % ST;
-        WAIT(&kv_empty[st], ((j / ST) & 1) ^ 1, 80);
-        ptx::mbar_arrive_expect_tx(&kv_full[st], 2 * Cfg::kKVBytes);
-        for (int c = 0; c < NC; ++c) {
-          ptx::tma_load_2d(sK + st * Cfg::kKVBytes + c * TB, &tm_kv, &kv_full[st], dt + h * HD + 64 * c, row0 + j * KT);
-          ptx::tma_load_2d(sV + st * Cfg::kKVBytes + c * TB, &tm_kv, &kv_full[st], 2 * dt + h * HD + 64 * c,
-                           row0 + j * KT);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, KT, false, false);   // S, dP: A (TMEM) K-major, B K-major
-    constexpr uint32_t id_dq = ptx::idesc_bf16_f32(128, HD, false, true);   // dQ: B = K MN-major
-    const uint32_t u0 = (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + 1023u) & ~1023u;
-    const uint32_t aK0 = u0, aV0 = u0 + ST * Cfg::kKVBytes;
-    WAIT(ops_ready, 0, 81);
-    ptx::tc_fence_after();
-    auto stage2 = [&](int i) {  // dQ += dS_i K_i
-      const int bb = i & 1, st = i % ST;
-      WAIT(&ds_full[bb], (i >> 1) & 1, 82);
-      ptx::tc_fence_after();
-      const uint32_t aK = aK0 + st * Cfg::kKVBytes;
-#pragma unroll
-      for (int kk = 0; kk < KT / 16; ++kk) {  // dS packed by the two column parts: kv 0-31 / 32-63
-        const uint32_t acol = (kk >> 1) * 32 + (kk & 1) * 8;
-        ptx::mma_bf16_ts_w(tdQ, tS + bb * 64 + acol, ptx::smem_desc_sw128(aK + kk * 2048, TB, 1024), id_dq,
-                           (i > 0 || kk > 0) ? 1u : 0u);
-      }
-      ptx::mma_commit_w(&kv_empty[st]);
-      ptx::mma_commit_w(&s_free[bb]);
-    };
-    for (int j = 0; j < n_kv; ++j) {
-      const int bb = j & 1, st = j % ST;
-      WAIT(&kv_full[st], (j / ST) & 1, 83);
-      if (j >= 2) WAIT(&s_free[bb], ((j - 2) >> 1) & 1, 84);
-      ptx::tc_fence_after();
-      const uint32_t aK = aK0 + st * Cfg::kKVBytes, aV = aV0 + st * Cfg::kKVBytes;
-#pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
-        const uint32_t off = (kk / 4) * TB + (kk % 4) * 32;
-        ptx::mma_bf16_ts_w(tS + bb * 64, tQ + kk * 8, ptx::smem_desc_sw128(aK + off, 16, 1024), id_s, kk > 0 ? 1u : 0u);
-        ptx::mma_bf16_ts_w(tdP + bb * 64, tdO + kk * 8, ptx::smem_desc_sw128(aV + off, 16, 1024), id_s,
-                           kk > 0 ? 1u : 0u);
-      }
-      ptx::mma_commit_w(&s_full[bb]);
-      if (j > 0) stage2(j - 1);
-    }
-    stage2(n_kv - 1);
-    ptx::mma_commit_w(dq_done);
-  } else if (warp >= 4) {
-    // 8 compute warps: 2 per TMEM lane quarter (query rows), each owning 32 of the 64 kv columns
-    const int quarter = warp & 3, part = (warp - 4) >> 2;
-    const int r = quarter * 32 + lane;  // query row within the block (TMEM lane)
-    const int q = q0 + r;
-    const uint32_t lb = static_cast<uint32_t>(quarter * 32) << 16;
-    // prologue: this row's Q (part 0) or dO (part 1) into TMEM as bf16 pairs (the A-operand layout)
-    {
-      const __nv_bfloat16* src = part == 0 ? qkv + static_cast<size_t>(row0 + q) * 3 * dt + h * HD
-                                           : dout + static_cast<size_t>(row0 + q) * dt + h * HD;
-      const uint32_t dst = (part == 0 ? tQ : tdO) + lb;
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        uint32_t v[32];
-        const uint4* s4 = reinterpret_cast<const uint4*>(src + half * 64);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint4 x = s4[i];
-          v[4 * i] = x.x, v[4 * i + 1] = x.y, v[4 * i + 2] = x.z, v[4 * i + 3] = x.w;
-        }
-        ptx::tmem_st_32x32b_x32(dst + half * 32, v);
-      }
-      ptx::tmem_st_wait();
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(ops_ready);
-    }
-    const float lq = lse[(static_cast<size_t>(b) * ht + h) * s + q];
-    const float dq = Dg[(static_cast<size_t>(b) * ht + h) * s + q];
-    for (int j = 0; j < n_kv; ++j) {
-      const int bb = j & 1;
-      WAIT(&s_full[bb], (j >> 1) & 1, 85);
-      ptx::tc_fence_after();
-      uint32_t sv[32], pv[32];
-      ptx::tmem_ld_32x32b_x32(tS + lb + bb * 64 + part * 32, sv);
-      ptx::tmem_ld_32x32b_x32(tdP + lb + bb * 64 + part * 32, pv);
-      ptx::tmem_ld_wait();
-      const int kvc = j * KT + part * 32;  // first kv index of this warp's columns
-      uint32_t pk[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        float d2[2];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const int c = 2 * e + k;
-          const float pp = ex2(fmaf(__uint_as_float(sv[c]), scale_log2, -lq));
-          d2[k] = kvc + c <= q ? pp * (__uint_as_float(pv[c]) - dq) : 0.f;
-        }
-        pk[e] = ptx::pack_bf16(d2[0], d2[1]);
-      }
-      // dS (bf16 pairs) over this warp's own first 16 S columns: the A operand of dQ += dS K
-      ptx::tmem_st_32x32b_x16(tS + lb + bb * 64 + part * 32, pk);
-      ptx::tmem_st_wait();
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&ds_full[bb]);
-    }
-    // epilogue: dQ (fp32, TMEM) * scale -> bf16 into the q section of dqkv; part p writes columns
-    // [64 p, 64 p + 64) of its row
-    WAIT(dq_done, 0, 86);
-    ptx::tc_fence_after();
-    __nv_bfloat16* qrow = dqkv + static_cast<size_t>(row0 + q) * 3 * dt + h * HD + part * 64;
-#pragma unroll 1
-    for (int c = 0; c < 2; ++c) {
-      uint32_t v[32];
-      ptx::tmem_ld_32x32b_x32(tdQ + lb + part * 64 + c * 32, v);
-      ptx::tmem_ld_wait();
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        uint4 o;
-        o.x = ptx::pack_bf16(__uint_as_float(v[8 * u]) * scale, __uint_as_float(v[8 * u + 1]) * scale);
-        o.y = ptx::pack_bf16(__uint_as_float(v[8 * u + 2]) * scale, __uint_as_float(v[8 * u + 3]) * scale);
-        o.z = ptx::pack_bf16(__uint_as_float(v[8 * u + 4]) * scale, __uint_as_float(v[8 * u + 5]) * scale);
-        o.w = ptx::pack_bf16(__uint_as_float(v[8 * u + 6]) * scale, __uint_as_float(v[8 * u + 7]) * scale);
-        reinterpret_cast<uint4*>(qrow + c * 32)[u] = o;
-      }
-    }
-  }
-  __syncthreads();
-  if (warp == 1) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<512>(tmem);
-  }
-}
-
-template <int HD>
-struct TcBwdKVCfg {
-  static constexpr int NC = HD / 64;
-  static constexpr int QT = 32;                 // query rows per tile
-  static constexpr int kQChunk = QT * 128;      // [32 q][64] bf16
-  static constexpr int kQBytes = NC * kQChunk;
-  static constexpr int QST = 4;                 // Q / dO / LSE / D ring depth
-  static constexpr int kSmem = 2 * QST * kQBytes + QST * 2 * QT * 4 + 1024 + 256;
-};
-
-template <int HD>
-__global__ void __launch_bounds__(384, 1)
-    fa_bwd_kv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
-                     const __nv_bfloat16* __restrict__ qkv, const float* __restrict__ lse,
-                     const float* __restrict__ Dg, __nv_bfloat16* __restrict__ dqkv, int s, int ht, float scale_log2,
-                     float scale) {
-  using Cfg = TcBwdKVCfg<HD>;
-  static_assert(HD == 128, "TMEM map: K | V | S^T x2 | dP^T x2 | dV | dK");
-  constexpr int NC = Cfg::NC, QT = Cfg::QT, QST = Cfg::QST;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = ptx::smem_align1024(smem_raw);
-  uint8_t* sQ = smem;                        // [QST][NC][32][64]
-  uint8_t* sdO = sQ + QST * Cfg::kQBytes;    // [QST][NC][32][64]
-  float* sL = reinterpret_cast<float*>(sdO + QST * Cfg::kQBytes);  // [QST][32]
-  float* sD = sL + QST * QT;                                      // [QST][32]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + QST * QT);
-  uint64_t* qdo_full = bars;              // [QST]
-  uint64_t* qdo_empty = qdo_full + QST;   // [QST]
-  uint64_t* s_full = qdo_empty + QST;     // [2]
-  uint64_t* pds_full = s_full + 2;        // [2] P^T / dS^T written back (4 warps of the owning WG)
-  uint64_t* s_free = pds_full + 2;        // [2] dV / dK MMAs consumed them
-  uint64_t* ops_ready = s_free + 2;       // K / V rows in TMEM (8 warps)
-  uint64_t* kdv_full = ops_ready + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kdv_full + 1);
-
-  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
-  const int kvb = blockIdx.x;
-  const int b = blockIdx.y / ht, h = blockIdx.y % ht;
-  const int dt = ht * HD;
-  const int row0 = b * s;
-  const int kv0 = kvb * 128;
-  const int qt_first = kv0 / QT;
-  const int n_it = s / QT - qt_first;
-
-  if (warp == 0 && lane == 0) {
-    ptx::tma_prefetch_desc(&tm_q);
-    ptx::tma_prefetch_desc(&tm_do);
-    for (int i = 0; i < QST; ++i) {
-      ptx::mbar_init(&qdo_full[i], 1);
-      ptx::mbar_init(&qdo_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&pds_full[i], 4);
-      ptx::mbar_init(&s_free[i], 1);
-    }
-    ptx::mbar_init(ops_ready, 8);
-    ptx::mbar_init(kdv_full, 1);
-    ptx::fence_mbar_init();
-  }
-  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
-  pdl_trigger();
-  pdl_wait();
-  // TMEM: K (A operand, 64 cols) | V (64) | S^T x2 (32 each) | dP^T x2 (32 each) | dV (128) | dK (128)
-  const uint32_t tK = tmem, tV = tmem + 64, tS = tmem + 128, tdP = tmem + 192, tdV = tmem + 256, tdK = tmem + 384;
-  const int wg = warp / 4;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      const float* gLq = lse + (static_cast<size_t>(b) * ht + h) * s;
-      const float* gDq = Dg + (static_cast<size_t>(b) * ht + h) * s;
-      for (int j = 0; j < n_it; ++j) {
-        const int sq = j % QST;
-        const int q0 = (qt_first + j) * QT;
-        WAIT(&qdo_empty[sq], ((j / QST) & 1) ^ 1, 90);
-        ptx::mbar_arrive_expect_tx(&qdo_full[sq], 2 * Cfg::kQBytes + 2 * QT * 4);
-        for (int c = 0; c < NC; ++c) {
-          ptx::tma_load_2d(sQ + sq * Cfg::kQBytes + c * Cfg::kQChunk, &tm_q, &qdo_full[sq], h * HD + 64 * c, row0 + q0);
-          ptx::tma_load_2d(sdO + sq * Cfg::kQBytes + c * Cfg::kQChunk, &tm_do, &qdo_full[sq], h * HD + 64 * c,
-                           row0 + q0);
-        }
-        ptx::bulk_load(sL + sq * QT, gLq + q0, QT * 4, &qdo_full[sq]);
-        ptx::bulk_load(sD + sq * QT, gDq + q0, QT * 4, &qdo_full[sq]);
-      }
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, QT, false, false);   // S^T, dP^T
-    constexpr uint32_t id_acc = ptx::idesc_bf16_f32(128, HD, false, true);  // dV, dK: B MN-major
-    const uint32_t u0 = (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + 1023u) & ~1023u;
-    const uint32_t aQ0 = u0, adO0 = u0 + QST * Cfg::kQBytes;
-    WAIT(ops_ready, 0, 91);
-    ptx::tc_fence_after();
-    auto stage2 = [&](int i) {  // dV += P^T dO, dK += dS^T Q (A operands from TMEM)
-      const int bb = i & 1, sq = i % QST;
-      WAIT(&pds_full[bb], (i >> 1) & 1, 92);
-      ptx::tc_fence_after();
-      const uint32_t aQ = aQ0 + sq * Cfg::kQBytes, adO = adO0 + sq * Cfg::kQBytes;
-#pragma unroll
-      for (int kk = 0; kk < QT / 16; ++kk) {
-        const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-        ptx::mma_bf16_ts_w(tdV, tS + bb * QT + kk * 8, ptx::smem_desc_sw128(adO + kk * 2048, Cfg::kQChunk, 1024), id_acc,
-                           acc);
-        ptx::mma_bf16_ts_w(tdK, tdP + bb * QT + kk * 8, ptx::smem_desc_sw128(aQ + kk * 2048, Cfg::kQChunk, 1024), id_acc,
-                           acc);
-      }
-      ptx::mma_commit_w(&qdo_empty[sq]);
-      ptx::mma_commit_w(&s_free[bb]);
-    };
-    for (int j = 0; j < n_it; ++j) {
-      const int bb = j & 1, sq = j % QST;
-      WAIT(&qdo_full[sq], (j / QST) & 1, 93);
-      if (j >= 2) WAIT(&s_free[bb], ((j - 2) >> 1) & 1, 94);
-      ptx::tc_fence_after();
-      const uint32_t aQ = aQ0 + sq * Cfg::kQBytes, adO = adO0 + sq * Cfg::kQBytes;
-#pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
-        const uint32_t aq = (kk / 4) * Cfg::kQChunk + (kk % 4) * 32;
-        ptx::mma_bf16_ts_w(tS + bb * QT, tK + kk * 8, ptx::smem_desc_sw128(aQ + aq, 16, 1024), id_s, kk > 0 ? 1u : 0u);
-        ptx::mma_bf16_ts_w(tdP + bb * QT, tV + kk * 8, ptx::smem_desc_sw128(adO + aq, 16, 1024), id_s,
-                           kk > 0 ? 1u : 0u);
-      }
-      ptx::mma_commit_w(&s_full[bb]);
-      if (j > 0) stage2(j - 1);
-    }
-    stage2(n_it - 1);
-    ptx::mma_commit_w(kdv_full);
-  } else if (wg == 1 || wg == 2) {
-    const int bb = wg - 1;  // this warpgroup's tiles (even / odd) and TMEM buffers
-    const int quarter = warp & 3;
-    const int r = quarter * 32 + lane;  // kv row within the block (TMEM lane)
-    const uint32_t lb = static_cast<uint32_t>(quarter * 32) << 16;
-    {  // prologue: K (WG1) / V (WG2) rows into TMEM as bf16 pairs
-      const __nv_bfloat16* src = qkv + static_cast<size_t>(row0 + kv0 + r) * 3 * dt + (bb == 0 ? dt : 2 * dt) + h * HD;
-      const uint32_t dst = (bb == 0 ? tK : tV) + lb;
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        uint32_t v[32];
-        const uint4* s4 = reinterpret_cast<const uint4*>(src + half * 64);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint4 x = s4[i];
-          v[4 * i] = x.x, v[4 * i + 1] = x.y, v[4 * i + 2] = x.z, v[4 * i + 3] = x.w;
-        }
-        ptx::tmem_st_32x32b_x32(dst + half * 32, v);
-      }
-      ptx::tmem_st_wait();
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(ops_ready);
-    }
-    for (int j = bb; j < n_it; j += 2) {
-      const int sq = j % QST;
-      const int q0 = (qt_first + j) * QT;
-      WAIT(&s_full[bb], (j >> 1) & 1, 95);
-      WAIT(&qdo_full[sq], (j / QST) & 1, 96);  // LSE / D of this tile
-      ptx::tc_fence_after();
-      uint32_t sv[32], dv[32];
-      ptx::tmem_ld_32x32b_x32(tS + lb + bb * QT, sv);
-      ptx::tmem_ld_32x32b_x32(tdP + lb + bb * QT, dv);
-      ptx::tmem_ld_wait();
-      const float4* L4 = reinterpret_cast<const float4*>(sL + sq * QT);
-      const float4* D4 = reinterpret_cast<const float4*>(sD + sq * QT);
-      uint32_t pk[16], dk[16];
-#pragma unroll
-      for (int e4 = 0; e4 < 8; ++e4) {
-        const float4 l4 = L4[e4], d4 = D4[e4];
-        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dvv[4] = {d4.x, d4.y, d4.z, d4.w};
-        float pp[4], ds[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const bool live = q0 + 4 * e4 + k >= kv0 + r;  // causal: query at or after this kv row
-          pp[k] = live ? ex2(fmaf(__uint_as_float(sv[4 * e4 + k]), scale_log2, -lv[k])) : 0.f;
-          ds[k] = pp[k] * (__uint_as_float(dv[4 * e4 + k]) - dvv[k]);
-        }
-        pk[2 * e4] = ptx::pack_bf16(pp[0], pp[1]);
-        pk[2 * e4 + 1] = ptx::pack_bf16(pp[2], pp[3]);
-        dk[2 * e4] = ptx::pack_bf16(ds[0], ds[1]);
-        dk[2 * e4 + 1] = ptx::pack_bf16(ds[2], ds[3]);
-      }
-      // P^T over the first 16 columns of S^T, dS^T over those of dP^T: the A operands of dV / dK
-      ptx::tmem_st_32x32b_x16(tS + lb + bb * QT, pk);
-      ptx::tmem_st_32x32b_x16(tdP + lb + bb * QT, dk);
-      ptx::tmem_st_wait();
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&pds_full[bb]);
-    }
-    // dK (scaled) and dV rows of this KV block: WG1 columns [0, 64), WG2 [64, 128)
-    WAIT(kdv_full, 0, 97);
-    ptx::tc_fence_after();
-    __nv_bfloat16* krow = dqkv + static_cast<size_t>(row0 + kv0 + r) * 3 * dt + dt + h * HD;
-    __nv_bfloat16* vrow = krow + dt;
-#pragma unroll 1
-    for (int c = bb * 2; c < bb * 2 + 2; ++c) {
-      uint32_t kv[32], vv[32];
-      ptx::tmem_ld_32x32b_x32(tdK + lb + c * 32, kv);
-      ptx::tmem_ld_32x32b_x32(tdV + lb + c * 32, vv);
-      ptx::tmem_ld_wait();
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        uint4 a, v2;
-        a.x = ptx::pack_bf16(__uint_as_float(kv[8 * u]) * scale, __uint_as_float(kv[8 * u + 1]) * scale);
-        a.y = ptx::pack_bf16(__uint_as_float(kv[8 * u + 2]) * scale, __uint_as_float(kv[8 * u + 3]) * scale);
-        a.z = ptx::pack_bf16(__uint_as_float(kv[8 * u + 4]) * scale, __uint_as_float(kv[8 * u + 5]) * scale);
-        a.w = ptx::pack_bf16(__uint_as_float(kv[8 * u + 6]) * scale, __uint_as_float(kv[8 * u + 7]) * scale);
-        v2.x = ptx::pack_bf16(__uint_as_float(vv[8 * u]), __uint_as_float(vv[8 * u + 1]));
-        v2.y = ptx::pack_bf16(__uint_as_float(vv[8 * u + 2]), __uint_as_float(vv[8 * u + 3]));
-        v2.z = ptx::pack_bf16(__uint_as_float(vv[8 * u + 4]), __uint_as_float(vv[8 * u + 5]));
-        v2.w = ptx::pack_bf16(__uint_as_float(vv[8 * u + 6]), __uint_as_float(vv[8 * u + 7]));
-        reinterpret_cast<uint4*>(krow + c * 32)[u] = a;
-        reinterpret_cast<uint4*>(vrow + c * 32)[u] = v2;
-      }
-    }
-  }
-  __syncthreads();
-  if (warp == 1) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<512>(tmem);
-  }
-}
-
-// Launch both passes of the split backward (hd 128): dK / dV (KV-stationary) then dQ (Q-stationary)
-// on the same stream; D must hold rowsum(dO * O). Writes all of dqkv.
-template <int HD>
-int bwd_split(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse,
-              const float* D, __nv_bfloat16* dqkv, cudaStream_t st) {
-  using CfgKV = TcBwdKVCfg<HD>;
-  using CfgQ = TcBwdQCfg<HD>;
-  if (ensure_dynamic_smem(reinterpret_cast<const void*>(fa_bwd_kv_kernel<HD>), CfgKV::kSmem) != 0 ||
-      ensure_dynamic_smem(reinterpret_cast<const void*>(fa_bwd_dq_kernel<HD>), CfgQ::kSmem) != 0)
-    return 3;
-  count_variant(KV_ATTN_BWD_SPLIT);
-  const int dt = a.heads * HD;
-  const uint64_t M = static_cast<uint64_t>(a.batch) * a.seq;
-  CUtensorMap tq, tdo, tkv;
-  if (!make_tmap_bf16(&tq, qkv, 3 * static_cast<uint64_t>(dt), M, 3 * dt, 64, CfgKV::QT)) return 3;
-  if (!make_tmap_bf16(&tdo, dout, static_cast<uint64_t>(dt), M, dt, 64, CfgKV::QT)) return 3;
-  if (!make_tmap_bf16(&tkv, qkv, 3 * static_cast<uint64_t>(dt), M, 3 * dt, 64, CfgQ::KT)) return 3;
-  const float scale = 1.f / sqrtf(static_cast<float>(HD));
-  dim3 grid(a.seq / 128, a.batch * a.heads);
-  cudaError_t e = launch_pdl(fa_bwd_kv_kernel<HD>, grid, dim3(384), CfgKV::kSmem, st, tq, tdo, qkv, lse, D, dqkv,
-                             a.seq, a.heads, scale * kLog2e, scale);
-  if (e == cudaSuccess)
-    e = launch_pdl(fa_bwd_dq_kernel<HD>, grid, dim3(384), CfgQ::kSmem, st, tkv, qkv, dout, lse, D, dqkv, a.seq,
-                   a.heads, scale * kLog2e, scale);
-  return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : 3;
-}
-
 // Backward preprocessing when D was not produced by the W_o dgrad epilogue: D[b,h,q] =
 // sum_c dO[q,c] * O[q,c] (one warp per (row, head)) and the fp32 dQ accumulator zeroed.
 template <int HD>
@@ -2343,7 +1876,6 @@ __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, const _
 #pragma unroll
   for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if (lane == 0) D[(static_cast<size_t>(row / s) * ht + h) * s + row % s] = acc;
-  if (dq_acc == nullptr) return;  // the split backward needs no fp32 dQ accumulator
   float* dqa = dq_acc + static_cast<size_t>(row) * dt + h * HD;
   for (int c = lane; c < HD; c += 32) dqa[c] = 0.f;
 }
@@ -2511,17 +2043,6 @@ int flash_attn_bwd(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bflo
   const int hd = a.head_dim;
   if (hd != 64 && hd != 128 && hd != 160) return 1;
   const int M = a.batch * a.seq, dt = a.heads * hd;
-  // hd 128: the split, atomic-free passes (dQ written directly, no fp32 accumulator); A/B switch
-  // GPTB200_ATTN_BWD_SPLIT=0 selects the single-pass kernel with the fp32 dQ reductions
-  static const char* split_env = std::getenv("GPTB200_ATTN_BWD_SPLIT");
-  const bool split = hd == 128 && !(split_env && split_env[0] == '0');
-  if (split) {
-    if (!d_ready) {
-      const int warps = M * a.heads, grid = (warps + 7) / 8;
-      attn_bwd_pre_kernel<128><<<grid, 256, 0, st>>>(out, dout, D, nullptr, a.seq, a.heads, M);
-    }
-    return bwd_split<128>(a, qkv, dout, lse, D, dqkv, st);
-  }
   if (d_ready && hd == 128) {
     cudaMemsetAsync(dq_acc, 0, static_cast<size_t>(M) * dt * sizeof(float), st);
   } else {

@@ -45,7 +45,6 @@ enum KernelVariant {
   KV_LN_BWD_STREAM,        // persistent bulk-copy LayerNorm backward (single HBM pass)
   KV_LN_BWD_FUSED,         // 32-row fused LayerNorm backward
   KV_LN_BWD_TWO_PASS,      // warp-per-row + column-sum LayerNorm backward
-  KV_ATTN_BWD_SPLIT,       // tcgen05 backward, split dK/dV + dQ passes (hd 128, TMEM A operands)
   KV_NUM
 };
 void count_variant(int v);
