@@ -236,8 +236,9 @@ int tp_session_memory(tp_session* s, tp_memory_report* out);
  * 0 GEMM single-CTA tiles, 1 GEMM CTA-pair 256x256, 2 GEMM CTA-pair 256x512, 3 K-sliced fp32
  * GEMM, 4 attention fwd persistent, 5 attention fwd per-block, 6 attention bwd per-block,
  * 7 attention bwd persistent, 8 attention bwd hd 64, 9 attention bwd hd 160, 10 LayerNorm bwd
- * persistent bulk-copy, 11 LayerNorm bwd 32-row fused, 12 LayerNorm bwd two-pass. */
-#define TP_KERNEL_VARIANTS 13
+ * persistent bulk-copy, 11 LayerNorm bwd 32-row fused, 12 LayerNorm bwd two-pass, 13 attention
+ * fwd two query tiles per CTA. */
+#define TP_KERNEL_VARIANTS 14
 int tp_variant_counts(int64_t out[TP_KERNEL_VARIANTS]);
 int tp_variant_counts_reset(void);
 

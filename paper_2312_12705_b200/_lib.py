@@ -133,7 +133,7 @@ class MemoryReport(C.Structure):
 
 VARIANTS = ["gemm_single", "gemm_pair_256", "gemm_pair_512", "gemm_ksplit", "attn_fwd_persistent",
             "attn_fwd_per_block", "attn_bwd_per_block", "attn_bwd_persistent", "attn_bwd_hd64",
-            "attn_bwd_hd160", "ln_bwd_stream", "ln_bwd_fused", "ln_bwd_two_pass"]
+            "attn_bwd_hd160", "ln_bwd_stream", "ln_bwd_fused", "ln_bwd_two_pass", "attn_fwd_two_q"]
 
 
 def variant_counts() -> dict:

@@ -45,8 +45,10 @@ __device__ __forceinline__ void dwait(uint64_t* bar, uint32_t parity, int id) {
   }
 }
 #define WAIT(bar, par, id) dwait(bar, par, id)
-#else
+#elif defined(GPTB200_WAIT_SLEEP)
 #define WAIT(bar, par, id) ptx::mbar_wait(bar, par)
+#else
+#define WAIT(bar, par, id) ptx::mbar_wait_spin(bar, par)
 #endif
 // Timeline instrumentation of the backward kernels (debug builds only, -DGPTB200_ATTN_TRACE):
 // clock64 stamps of one CTA's role events per query tile, dumped by the launcher to
@@ -638,6 +640,344 @@ __global__ void __launch_bounds__(TcFwdCfg<HD>::kThreads, 1)
   }
 }
 
+// K5, two query tiles per CTA (hd 64 / 128). CTA = (256-row query block, sequence-head); heaviest
+// blocks launch first. The tensor core always has the other tile's work while one tile's softmax
+// runs:  per kv tile j the MMA warp issues  PV_0(j), S_0(j+1), PV_1(j), S_1(j+1), so softmax_0(j+1)
+// overlaps PV_1(j) + S_1(j+1) and softmax_1(j+1) overlaps PV_0(j+1) + S_0(j+2) (every MMA is
+// M128 x N128, at the tcgen05 issue floor; N = 64 halves of that measure 0.54 of it).
+// TMEM: S_0 | S_1 (128 fp32 columns each; P_t overwrites S_t as packed bf16, the A operand of PV_t,
+// and S_t(j+1) follows PV_t(j) in the same in-order MMA stream) | O_0 | O_1 (HD columns each).
+// Warps: 0 TMA (Q_0 + Q_1 once, K / V rings), 1 MMA issuer, 2-3 idle, 4-7 softmax of tile 0, 8-11
+// softmax of tile 1: thread = query row = TMEM lane, so the row max and sum are thread-local;
+// O_t is rescaled lazily (running max grows by > 2^8) by the tile's own softmax warps.
+// Paired fp32 (FFMA2 / FADD2) and 2^x on the FMA pipe for a pair: x = j + f with j = rint(x) (magic-number
+// rounding), 2^f by a degree-3 minimax polynomial on [-0.5, 0.5] (relative error 7.5e-5, far below the
+// bf16 rounding of P), 2^j added to the exponent field by one IMAD per element. Inputs <= 0 (scores
+// minus the running max); clamped at -126 (2^j stays a normal exponent offset) so masked (-inf) scores
+// give a denormal ~0.
+__device__ __forceinline__ uint64_t fa_pack2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 fa_unpack2(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ uint64_t fa_fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fa_add2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float2 exp2_fma2(float a, float b) {
+  constexpr float kMagic = 12582912.f;  // 1.5 * 2^23
+  const uint64_t x = fa_pack2(fmaxf(a, -126.f), fmaxf(b, -126.f));
+  const uint64_t t = fa_add2(x, fa_pack2(kMagic, kMagic));                  // low bits = rint(x)
+  const uint64_t jf = fa_add2(t, fa_pack2(-kMagic, -kMagic));               // rint(x) as float
+  const uint64_t f = fa_fma2(jf, fa_pack2(-1.f, -1.f), x);                   // x - rint(x)
+  uint64_t p = fa_fma2(f, fa_pack2(0.05517163f, 0.05517163f), fa_pack2(0.24261117f, 0.24261117f));
+  p = fa_fma2(p, f, fa_pack2(0.693261f, 0.693261f));
+  p = fa_fma2(p, f, fa_pack2(0.99992807f, 0.99992807f));
+  const float2 pv = fa_unpack2(p), tv = fa_unpack2(t);
+  return make_float2(__int_as_float(__float_as_int(pv.x) + (__float_as_int(tv.x) << 23)),
+                     __int_as_float(__float_as_int(pv.y) + (__float_as_int(tv.y) << 23)));
+}
+
+template <int HD, int CS>
+struct TcFwd2Cfg {
+  static constexpr int NC = HD / 64;
+  static constexpr int kChunk = 128 * 128;              // [128 rows][64] bf16, SW128
+  static constexpr int kTileBytes = NC * kChunk;        // [128 rows][HD]
+  static constexpr int ST = 2;                          // K ring and V ring depth
+  static constexpr int kThreads = 128 + 2 * CS * 128;   // WG0 + CS softmax warpgroups per query tile
+  static constexpr int kSmem = 2 * kTileBytes + 2 * ST * kTileBytes + 2 * CS * 128 * 4 + 256;
+  static_assert(kSmem <= 232448, "fa_fwd2 smem over the 227 KB opt-in limit");
+  // register split (setmaxnreg): the launch allocates kRegBase per thread (65536 / threads, rounded
+  // down to 8); WG0 drops to 56 and the softmax warpgroups may grow only by what it released —
+  // asking for more blocks setmaxnreg.inc forever.
+  static constexpr int kRegBase = (65536 / kThreads) / 8 * 8;
+  static constexpr int kRegSoftmaxRaw = ((kThreads * kRegBase - 128 * 56) / (kThreads - 128)) / 8 * 8;
+  static constexpr int kRegSoftmax = kRegSoftmaxRaw > 232 ? 232 : kRegSoftmaxRaw;
+  static_assert(128 * 56 + (kThreads - 128) * kRegSoftmax <= kThreads * kRegBase, "setmaxnreg budget");
+};
+
+// EMU: pairs out of every 8 (16 scores) whose 2^x runs on the FMA pipe instead of the MUFU.
+// CS: softmax warps per (query tile, TMEM lane quarter); each owns 128/CS score columns of its 32
+// rows, the CS parts exchange their row max once per kv tile through shared memory.
+template <int HD, int EMU, int CS>
+__global__ void __launch_bounds__(TcFwd2Cfg<HD, CS>::kThreads, 1)
+    fa_fwd2_kernel(const __grid_constant__ CUtensorMap tm_qkv, __nv_bfloat16* __restrict__ out,
+                   float* __restrict__ lse, int s, int ht, float scale_log2) {
+  using Cfg = TcFwd2Cfg<HD, CS>;
+  constexpr int NC = Cfg::NC, ST = Cfg::ST, CH = Cfg::kChunk, TB = Cfg::kTileBytes;
+  constexpr int CW = 128 / CS;  // score columns per softmax thread
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if ((ptx::smem_u32(smem_raw) & 1023u) != 0) __trap();  // 128B-swizzle atoms need 1 KB alignment
+  uint8_t* sQ = smem_raw;                   // [2 tiles][NC][128][64]
+  uint8_t* sK = sQ + 2 * TB;                // [ST][NC][128][64]
+  uint8_t* sV = sK + ST * TB;               // [ST][NC][128][64]
+  float* xch = reinterpret_cast<float*>(sV + ST * TB);  // [2 tiles][CS][128] row max / sum exchange
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xch + 2 * CS * 128);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;              // [ST]
+  uint64_t* k_empty = k_full + ST;          // [ST]
+  uint64_t* v_full = k_empty + ST;          // [ST]
+  uint64_t* v_empty = v_full + ST;          // [ST]
+  uint64_t* s_full = v_empty + ST;          // [2 tiles]
+  uint64_t* p_full = s_full + 2;            // [2 tiles]
+  uint64_t* pv_done = p_full + 2;           // [2 tiles]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
+  const int qb = gridDim.y - 1 - blockIdx.y;  // heaviest query blocks first (y-major launch order)
+  const int b = blockIdx.x / ht, h = blockIdx.x % ht;
+  const int dt = ht * HD;
+  const int row0 = b * s;
+  const int n = 2 * qb + 2;  // kv tiles of tile 1; tile 0 uses the first n - 1
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tm_qkv);
+    ptx::mbar_init(q_full, 1);
+    for (int i = 0; i < ST; ++i) {
+      ptx::mbar_init(&k_full[i], 1);
+      ptx::mbar_init(&k_empty[i], 1);
+      ptx::mbar_init(&v_full[i], 1);
+      ptx::mbar_init(&v_empty[i], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      ptx::mbar_init(&s_full[t], 1);
+      ptx::mbar_init(&p_full[t], 4 * CS);
+      ptx::mbar_init(&pv_done[t], 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
+  pdl_trigger();
+  pdl_wait();
+  const int wg = warp / 4;
+  if (wg == 0) {
+    ptx::setmaxnreg_dec<56>();
+    if (warp == 0) {
+      if (lane == 0) {
+        ptx::mbar_arrive_expect_tx(q_full, 2 * TB);
+        for (int t = 0; t < 2; ++t)
+          for (int c = 0; c < NC; ++c)
+            ptx::tma_load_2d(sQ + t * TB + c * CH, &tm_qkv, q_full, h * HD + 64 * c, row0 + qb * 256 + t * 128);
+        for (int j = 0; j < n; ++j) {
+          const int st = j % ST, use = j / ST;
+          WAIT(&k_empty[st], (use & 1) ^ 1, 60);
+          ptx::mbar_arrive_expect_tx(&k_full[st], TB);
+          for (int c = 0; c < NC; ++c)
+            ptx::tma_load_2d(sK + st * TB + c * CH, &tm_qkv, &k_full[st], dt + h * HD + 64 * c, row0 + j * 128);
+          WAIT(&v_empty[st], (use & 1) ^ 1, 61);
+          ptx::mbar_arrive_expect_tx(&v_full[st], TB);
+          for (int c = 0; c < NC; ++c)
+            ptx::tma_load_2d(sV + st * TB + c * CH, &tm_qkv, &v_full[st], 2 * dt + h * HD + 64 * c, row0 + j * 128);
+        }
+      }
+    } else if (warp == 1) {
+      constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 128, false, false);
+      constexpr uint32_t id_o = ptx::idesc_bf16_f32(128, HD, false, true);
+      const uint32_t aQ = ptx::smem_u32(sQ), aK0 = ptx::smem_u32(sK), aV0 = ptx::smem_u32(sV);
+      auto issue_s = [&](int t, int j) {  // S_t = Q_t K_j^T
+        const uint32_t aq = aQ + t * TB, ak = aK0 + (j % ST) * TB;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk / 4) * CH + (kk % 4) * 32;
+          ptx::mma_bf16_ss_w(tmem + t * 128, ptx::smem_desc_sw128(aq + off, 16, 1024),
+                             ptx::smem_desc_sw128(ak + off, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+        }
+        ptx::mma_commit_w(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j (P_t from TMEM)
+        const uint32_t av = aV0 + (j % ST) * TB;
+#pragma unroll
+        for (int kk = 0; kk < 128 / 16; ++kk)
+          ptx::mma_bf16_ts_w(tmem + 256 + t * HD, tmem + t * 128 + kk * 8,
+                             ptx::smem_desc_sw128(av + kk * 2048, CH, 1024), id_o, (j > 0 || kk > 0) ? 1u : 0u);
+        ptx::mma_commit_w(&pv_done[t]);
+      };
+      WAIT(q_full, 0, 62);
+      WAIT(&k_full[0], 0, 63);
+      ptx::tc_fence_after();
+      issue_s(0, 0);
+      issue_s(1, 0);
+      ptx::mma_commit_w(&k_empty[0]);
+      for (int j = 0; j < n; ++j) {
+        const int st = j % ST, st1 = (j + 1) % ST;
+        const bool next = j + 1 < n;
+        WAIT(&v_full[st], (j / ST) & 1, 64);
+        if (next) WAIT(&k_full[st1], ((j + 1) / ST) & 1, 65);
+        if (j < n - 1) {  // tile 0 (its last kv tile is n - 2)
+          WAIT(&p_full[0], j & 1, 66);
+          ATTN_TRACE(0, j);
+          ptx::tc_fence_after();
+          issue_pv(0, j);
+          if (j + 1 < n - 1) issue_s(0, j + 1);
+          ATTN_TRACE(1, j);
+        }
+        WAIT(&p_full[1], j & 1, 67);
+        ATTN_TRACE(2, j);
+        ptx::tc_fence_after();
+        issue_pv(1, j);
+        ptx::mma_commit_w(&v_empty[st]);
+        if (next) {
+          issue_s(1, j + 1);
+          ptx::mma_commit_w(&k_empty[st1]);
+        }
+        ATTN_TRACE(3, j);
+      }
+    }
+  } else {
+    ptx::setmaxnreg_inc<Cfg::kRegSoftmax>();
+    const int t = (wg - 1) / CS;           // query tile
+    const int part = (wg - 1) % CS;        // which CW score columns of the row
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;     // query row within the tile == TMEM lane
+    const uint32_t lb = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t tS = tmem + lb + t * 128, tO = tmem + lb + 256 + t * HD;
+    const int nt = n - 1 + t;              // kv tiles of this query tile; the last is the diagonal
+    float* xrow = xch + t * CS * 128;      // [CS][128]
+    const int bar_id = 1 + t * 4 + quarter;  // named barrier of the CS warps sharing these rows
+    const bool tw = quarter == 0 && part == 0;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < nt; ++j) {
+      if (tw) ATTN_TRACE(4 + 5 * t, j);
+      WAIT(&s_full[t], j & 1, 68);
+      if (tw) ATTN_TRACE(5 + 5 * t, j);
+      ptx::tc_fence_after();
+      float x[CW];
+      {
+        uint32_t v[CW / 32][32];
+#pragma unroll
+        for (int c = 0; c < CW / 32; ++c) ptx::tmem_ld_32x32b_x32(tS + part * CW + c * 32, v[c]);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < CW / 32; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) x[c * 32 + i] = __uint_as_float(v[c][i]);
+      }
+      if (j == nt - 1) {  // diagonal tile
+#pragma unroll
+        for (int i = 0; i < CW; ++i)
+          if (part * CW + i > r) x[i] = -INFINITY;
+      }
+      float pm[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pm[k] = fmaxf(x[k], x[k + 8]);
+#pragma unroll
+      for (int i = 16; i < CW; i += 8)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pm[k] = fmaxf(pm[k], x[i + k]);
+      float mt =
+          fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) *
+          scale_log2;
+      if constexpr (CS > 1) {  // row max over the parts (also orders every part's S reads before any P write)
+        xrow[part * 128 + r] = mt;
+        named_sync(bar_id, 32 * CS);
+#pragma unroll
+        for (int o = 1; o < CS; ++o) mt = fmaxf(mt, xrow[((part + o) % CS) * 128 + r]);
+        named_sync(bar_id, 32 * CS);  // exchange slots are reused next tile
+      }
+      if (tw) ATTN_TRACE(6 + 5 * t, j);
+      if (__any_sync(0xffffffffu, mt > m_used + 8.f)) {
+        const float m_new = fmaxf(m_used, mt);
+        if (j > 0) {  // O_t holds PV_t(0..j-1) once pv_done completes phase j-1
+          WAIT(&pv_done[t], (j - 1) & 1, 69);
+          const float f = exp2f(m_used - m_new);
+          l *= f;
+          ptx::tc_fence_after();
+#pragma unroll 1
+          for (int c = part * (HD / 32) / CS; c < (part + 1) * (HD / 32) / CS; ++c) {
+            uint32_t v[32];
+            ptx::tmem_ld_32x32b_x32(tO + c * 32, v);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * f);
+            ptx::tmem_st_32x32b_x32(tO + c * 32, v);
+          }
+        }
+        m_used = m_new;
+      }
+      const uint64_t sc2 = fa_pack2(scale_log2, scale_log2), nm2 = fa_pack2(-m_used, -m_used);
+      uint64_t ls[4] = {0ull, 0ull, 0ull, 0ull};  // paired partial row sums
+#pragma unroll
+      for (int c = 0; c < CW / 32; ++c) {  // 32 scores -> 16 packed bf16x2 columns of P over S
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float2 sv = fa_unpack2(fa_fma2(fa_pack2(x[c * 32 + 2 * e], x[c * 32 + 2 * e + 1]), sc2, nm2));
+          float2 pv;
+          if ((e & 7) >= 8 - EMU) {
+            pv = exp2_fma2(sv.x, sv.y);
+          } else {
+            pv.x = ex2(sv.x);
+            pv.y = ex2(sv.y);
+          }
+          ls[e & 3] = fa_add2(ls[e & 3], fa_pack2(pv.x, pv.y));
+          pk[e] = ptx::pack_bf16(pv.x, pv.y);
+        }
+        ptx::tmem_st_32x32b_x16(tS + part * (CW / 2) + c * 16, pk);
+      }
+      {
+        const float2 a0 = fa_unpack2(fa_add2(ls[0], ls[1])), a1 = fa_unpack2(fa_add2(ls[2], ls[3]));
+        l += (a0.x + a0.y) + (a1.x + a1.y);
+      }
+      if (tw) ATTN_TRACE(7 + 5 * t, j);
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&p_full[t]);
+      if (tw) ATTN_TRACE(8 + 5 * t, j);
+    }
+    float l_tot = l;
+    if constexpr (CS > 1) {
+      xrow[part * 128 + r] = l;
+      named_sync(bar_id, 32 * CS);
+#pragma unroll
+      for (int o = 1; o < CS; ++o) l_tot += xrow[((part + o) % CS) * 128 + r];
+    }
+    WAIT(&pv_done[t], (nt - 1) & 1, 70);
+    ptx::tc_fence_after();
+    const int q_row = qb * 256 + t * 128 + r;
+    const float inv = 1.f / l_tot;
+    __nv_bfloat16* orow = out + static_cast<size_t>(row0 + q_row) * dt + h * HD;
+#pragma unroll 1
+    for (int c = part * (HD / 32) / CS; c < (part + 1) * (HD / 32) / CS; ++c) {
+      uint32_t v[32];
+      ptx::tmem_ld_32x32b_x32(tO + c * 32, v);
+      ptx::tmem_ld_wait();
+      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 pkk;
+        pkk.x = ptx::pack_bf16(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
+        pkk.y = ptx::pack_bf16(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
+        pkk.z = ptx::pack_bf16(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
+        pkk.w = ptx::pack_bf16(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
+        dst[q] = pkk;
+      }
+    }
+    if (part == 0) lse[(static_cast<size_t>(b) * ht + h) * s + q_row] = m_used + log2f(l_tot);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
 // ----------------------------------------------------------------------------- backward
 // K6 on tcgen05. CTA = one (sequence, head, 128-row KV block); loops over the 128-row query tiles
 // at and after the diagonal. Per tile:  S^T = K Q^T and dP^T = V dO^T (TMEM), one thread per KV
@@ -929,7 +1269,12 @@ struct TcBwd2Cfg {
   static_assert(kSmem <= 232448, "smem over the 227 KB opt-in limit");
 };
 
-template <int HD>
+// TP (P^T / dS^T in TMEM): the compute warps write P^T and dS^T as packed bf16 over the S^T
+// columns they have just read (each half of the tile into its own 32 columns: P^T 16, dS^T 16), and
+// dV += P^T dO, dK += dS^T Q read their A operand from TMEM; only dS^T goes to shared memory (the B
+// operand of dQ^T). S^T_{j+2} overwrites those columns after stage 2 of tile j in the same in-order
+// MMA stream.
+template <int HD, bool TP>
 __global__ void __launch_bounds__(512, 1)
     fa_bwd_tc2_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
                       const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse,
@@ -1049,10 +1394,16 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {  // K = 64 query rows
           const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-          ptx::mma_bf16_ss_w(tdV, ptx::smem_desc_sw128(aP + kk * 32, 16, 1024),
-                           ptx::smem_desc_sw128(adO + kk * 2048, 8192, 1024), id_acc, acc);
-          ptx::mma_bf16_ss_w(tdK, ptx::smem_desc_sw128(adS + kk * 32, 16, 1024),
-                           ptx::smem_desc_sw128(aQ + kk * 2048, 8192, 1024), id_acc, acc);
+          if constexpr (TP) {  // 16 query rows = 8 packed columns; half h of the tile at column 32 h
+            const uint32_t ta = tS + bb * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+            ptx::mma_bf16_ts_w(tdV, ta, ptx::smem_desc_sw128(adO + kk * 2048, 8192, 1024), id_acc, acc);
+            ptx::mma_bf16_ts_w(tdK, ta + 16, ptx::smem_desc_sw128(aQ + kk * 2048, 8192, 1024), id_acc, acc);
+          } else {
+            ptx::mma_bf16_ss_w(tdV, ptx::smem_desc_sw128(aP + kk * 32, 16, 1024),
+                               ptx::smem_desc_sw128(adO + kk * 2048, 8192, 1024), id_acc, acc);
+            ptx::mma_bf16_ss_w(tdK, ptx::smem_desc_sw128(adS + kk * 32, 16, 1024),
+                               ptx::smem_desc_sw128(aQ + kk * 2048, 8192, 1024), id_acc, acc);
+          }
         }
         if (i > 0) WAIT(dq_free, (i - 1) & 1, 44);  // dQ^T_{i-1} read out of its TMEM columns
         ATTN_TRACE(5, i);
@@ -1169,6 +1520,10 @@ __global__ void __launch_bounds__(512, 1)
           }
       }
       if (tw) ATTN_TRACE(11, j);
+      if constexpr (TP) {  // over this half's own (already read) S^T columns
+        ptx::tmem_st_32x32b_x16(tS + lb + bb * 64 + qc, pk);
+        ptx::tmem_st_32x32b_x16(tS + lb + bb * 64 + qc + 16, dk);
+      }
       WAIT(&pds_free[bb], ((j >> 1) & 1) ^ 1, 47);  // stage 2 of tile j-2 is done with buffer bb
       if (tw) ATTN_TRACE(12, j);
       uint8_t* prow = sPT + bb * Cfg::kPBytes + r * 128;
@@ -1176,10 +1531,12 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int off = ((half * 4 + u) ^ (r & 7)) * 16;
-        *reinterpret_cast<uint4*>(prow + off) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        if constexpr (!TP)
+          *reinterpret_cast<uint4*>(prow + off) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         *reinterpret_cast<uint4*>(drow + off) = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
       }
       ptx::fence_proxy_async();
+      if constexpr (TP) ptx::tmem_st_wait();
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&pds_full[bb]);
@@ -1900,7 +2257,9 @@ template <int HD>
 int bwd_tc2(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* D,
             float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st) {
   using Cfg = TcBwd2Cfg<HD>;
-  if (ensure_dynamic_smem(reinterpret_cast<const void*>(fa_bwd_tc2_kernel<HD>), Cfg::kSmem) != 0) return 3;
+  static const bool tp = std::getenv("GPTB200_ATTN_BWD_SMEM_P") == nullptr;  // A/B: P^T/dS^T in smem
+  const auto kern = tp ? fa_bwd_tc2_kernel<HD, true> : fa_bwd_tc2_kernel<HD, false>;
+  if (ensure_dynamic_smem(reinterpret_cast<const void*>(kern), Cfg::kSmem) != 0) return 3;
   count_variant(KV_ATTN_BWD_PER_BLOCK);
   const int dt = a.heads * HD;
   const uint64_t M = static_cast<uint64_t>(a.batch) * a.seq;
@@ -1919,7 +2278,7 @@ int bwd_tc2(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* d
     cudaMemcpyToSymbol(g_attn_trace, &tbuf, sizeof(tbuf));
   }
 #endif
-  launch_pdl(fa_bwd_tc2_kernel<HD>, grid, dim3(512), Cfg::kSmem, st, tkv, tq, tdo, lse, D, dq_acc, dqkv, a.seq,
+  launch_pdl(kern, grid, dim3(512), Cfg::kSmem, st, tkv, tq, tdo, lse, D, dq_acc, dqkv, a.seq,
              a.heads, scale * kLog2e, scale);
 #ifdef GPTB200_ATTN_TRACE
   if (tbuf) {
@@ -1992,6 +2351,69 @@ int fwd_tc_persistent(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat1
   launch_pdl(fa_fwd_tc_persistent<HD>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, tm, out, lse, a.seq, a.heads,
              a.batch, kLog2e / sqrtf(static_cast<float>(HD)));
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+// Debug builds (-DGPTB200_ATTN_TRACE): per-tile clock64 stamps of one CTA -> $GPTB200_ATTN_TRACE.
+struct TraceDump {
+#ifdef GPTB200_ATTN_TRACE
+  unsigned long long* buf = nullptr;
+  const char* path = std::getenv("GPTB200_ATTN_TRACE");
+  TraceDump() {
+    if (!path) return;
+    cudaMalloc(&buf, kTraceTiles * kTraceEv * 8);
+    cudaMemset(buf, 0, kTraceTiles * kTraceEv * 8);
+    cudaMemcpyToSymbol(g_attn_trace, &buf, sizeof(buf));
+  }
+  void dump(cudaStream_t st) {
+    if (!buf) return;
+    cudaStreamSynchronize(st);
+    std::vector<unsigned long long> h(kTraceTiles * kTraceEv);
+    cudaMemcpy(h.data(), buf, h.size() * 8, cudaMemcpyDeviceToHost);
+    if (FILE* f = std::fopen(path, "w")) {
+      for (int t = 0; t < kTraceTiles; ++t)
+        for (int e = 0; e < kTraceEv; ++e) std::fprintf(f, "%llu%c", h[t * kTraceEv + e], e + 1 < kTraceEv ? ',' : '\n');
+      std::fclose(f);
+    }
+    unsigned long long* null = nullptr;
+    cudaMemcpyToSymbol(g_attn_trace, &null, sizeof(null));
+    cudaFree(buf);
+    buf = nullptr;
+  }
+#else
+  void dump(cudaStream_t) {}
+#endif
+};
+
+template <int HD, int CS>
+int fwd_tc2q_cs(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, cudaStream_t st, int emu) {
+  using Cfg = TcFwd2Cfg<HD, CS>;
+  const auto kern = emu <= 0 ? fa_fwd2_kernel<HD, 0, CS> : emu == 1 ? fa_fwd2_kernel<HD, 1, CS>
+                  : emu == 2 ? fa_fwd2_kernel<HD, 2, CS> : emu == 3 ? fa_fwd2_kernel<HD, 3, CS> : fa_fwd2_kernel<HD, 4, CS>;
+  if (ensure_dynamic_smem(reinterpret_cast<const void*>(kern), Cfg::kSmem) != 0) return 3;
+  count_variant(KV_ATTN_FWD_TWO_Q);
+  const int dt = a.heads * HD;
+  CUtensorMap tm;
+  if (!make_tmap_bf16(&tm, qkv, 3 * static_cast<uint64_t>(dt), static_cast<uint64_t>(a.batch) * a.seq, 3 * dt, 64, 128))
+    return 3;
+  dim3 grid(a.batch * a.heads, a.seq / 256);
+  TraceDump trace;
+  launch_pdl(kern, grid, dim3(Cfg::kThreads), Cfg::kSmem, st, tm, out, lse, a.seq, a.heads,
+             kLog2e / sqrtf(static_cast<float>(HD)));
+  trace.dump(st);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+template <int HD>
+int fwd_tc2q(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, cudaStream_t st) {
+  static const int emu = [] {
+    const char* e = std::getenv("GPTB200_ATTN_FWD_EMU");
+    return e ? std::atoi(e) : 2;  // measured best of 0..4 (1.4B shapes: 865 / 901 TF/s; 0: 855 / 883)
+  }();
+  static const int cs = [] {
+    const char* e = std::getenv("GPTB200_ATTN_FWD_CS");
+    return e ? std::atoi(e) : 1;  // 2 warps per row measured 3 % slower (more row-max exchange than gain)
+  }();
+  return cs == 1 ? fwd_tc2q_cs<HD, 1>(a, qkv, out, lse, st, emu) : fwd_tc2q_cs<HD, 2>(a, qkv, out, lse, st, emu);
 }
 
 template <int HD>
@@ -2072,6 +2494,14 @@ int flash_attn_fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat1
   // 766 vs 670 TF/s) but inside the step it loses (530 vs 610 TF/s, same build and box class: the
   // persistent CTAs' prologue overlap matters more behind the QKV GEMM), so it stays an A/B switch.
   static const bool per_block = std::getenv("GPTB200_ATTN_FWD_PER_BLOCK") != nullptr;
+  // two query tiles per CTA (fa_fwd2_kernel) when its grid of 256-row blocks fills the GPU at least
+  // twice: 1.4B MBS 32 / 8: 865 / 901 vs 703 / 766 TF/s; with fewer blocks (tensor-parallel shapes,
+  // 12 heads x 8 blocks) the persistent one-tile kernel keeps every SM busy (555 vs 351 TF/s).
+  static const char* two_q_env = std::getenv("GPTB200_ATTN_FWD_2Q");  // A/B: 1 always, 0 never
+  const int blocks256 = a.batch * a.heads * (a.seq / 256);
+  const bool two_q = two_q_env ? two_q_env[0] == '1' : blocks256 >= 2 * device_sm_count();
+  if (two_q && a.seq % 256 == 0 && (a.head_dim == 64 || a.head_dim == 128) && !per_block)
+    return a.head_dim == 64 ? fwd_tc2q<64>(a, qkv, out, lse, st) : fwd_tc2q<128>(a, qkv, out, lse, st);
   switch (a.head_dim) {
     case 64: return per_block ? fwd_tc<64>(a, qkv, out, lse, st) : fwd_tc_persistent<64>(a, qkv, out, lse, st);
     case 128: return per_block ? fwd_tc<128>(a, qkv, out, lse, st) : fwd_tc_persistent<128>(a, qkv, out, lse, st);

@@ -45,6 +45,7 @@ enum KernelVariant {
   KV_LN_BWD_STREAM,        // persistent bulk-copy LayerNorm backward (single HBM pass)
   KV_LN_BWD_FUSED,         // 32-row fused LayerNorm backward
   KV_LN_BWD_TWO_PASS,      // warp-per-row + column-sum LayerNorm backward
+  KV_ATTN_FWD_TWO_Q,       // tcgen05 forward, two query tiles per CTA (hd 64 / 128, large grids)
   KV_NUM
 };
 void count_variant(int v);

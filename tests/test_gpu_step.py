@@ -155,12 +155,12 @@ def test_invalid_config_is_reported_not_crashed():
 
 def test_step_parity_1p4b_width_headline_variants():
     # MBS 8 = 16384 rows: CTA-pair GEMMs, K-sliced weight gradients, the persistent bulk-copy
-    # LayerNorm backward, per-block attention backward, persistent attention forward
+    # LayerNorm backward, per-block attention backward, two-query-tile attention forward
     T.variant_counts_reset()
     r = run_parity(L=2, d=2048, heads=16, V=8192, s=2048, mbs=8, gbs=8, dropout=0.1)
     v = T.variant_counts()
     print(r["loss"], max(g[1] for g in r["grads"]), v)
-    for name in ("gemm_pair_256", "gemm_ksplit", "ln_bwd_stream", "attn_bwd_per_block", "attn_fwd_persistent"):
+    for name in ("gemm_pair_256", "gemm_ksplit", "ln_bwd_stream", "attn_bwd_per_block", "attn_fwd_two_q"):
         assert v[name] > 0, (name, v)
 
 

@@ -1,0 +1,5 @@
+#!/bin/bash
+GPTB200_ATTN_FWD_2Q=1 timeout 300 python -m pytest tests/test_gpu_kernels.py -q -x -k flash 2>&1 | tail -2
+GPTB200_ATTN_FWD_2Q=1 GPTB200_LIB=$PWD/paper_2312_12705_b200/lib_trace/libtrainplan_b200.so GPTB200_ATTN_TRACE=gpurun_out/trace_fwd.csv \
+  timeout 120 python tools/run_attn_shape.py 8 2048 16 128 fwd 1; echo "rc $?"
+python tools/attn_fwd_trace.py gpurun_out/trace_fwd.csv
