@@ -1535,8 +1535,11 @@ __global__ void __launch_bounds__(512, 1)
           *reinterpret_cast<uint4*>(prow + off) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         *reinterpret_cast<uint4*>(drow + off) = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
       }
+      if (tw) ATTN_TRACE(16, j);
       ptx::fence_proxy_async();
+      if (tw) ATTN_TRACE(17, j);
       if constexpr (TP) ptx::tmem_st_wait();
+      if (tw) ATTN_TRACE(18, j);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&pds_full[bb]);

@@ -79,7 +79,9 @@ void run(const char* name, int sms, unsigned long long* d) {
               floor, floor / cyc);
 }
 
+
 int main() {
+  setvbuf(stdout, nullptr, _IONBF, 0);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   unsigned long long* d;
@@ -96,3 +98,4 @@ int main() {
   std::printf("status %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
+
