@@ -45,10 +45,12 @@ __device__ __forceinline__ void dwait(uint64_t* bar, uint32_t parity, int id) {
   }
 }
 #define WAIT(bar, par, id) dwait(bar, par, id)
-#elif defined(GPTB200_WAIT_SLEEP)
-#define WAIT(bar, par, id) ptx::mbar_wait(bar, par)
+#define WAIT_SPIN(bar, par, id) dwait(bar, par, id)
 #else
-#define WAIT(bar, par, id) ptx::mbar_wait_spin(bar, par)
+#define WAIT(bar, par, id) ptx::mbar_wait(bar, par)
+// the two-query-tile forward hands off between roles every few hundred cycles: a thread parked by
+// the suspend-hinted wait resumes too late there (94 vs 798 TFLOP/s), so it spins
+#define WAIT_SPIN(bar, par, id) ptx::mbar_wait_spin(bar, par)
 #endif
 // Timeline instrumentation of the backward kernels (debug builds only, -DGPTB200_ATTN_TRACE):
 // clock64 stamps of one CTA's role events per query tile, dumped by the launcher to
@@ -775,11 +777,11 @@ __global__ void __launch_bounds__(TcFwd2Cfg<HD, CS>::kThreads, 1)
             ptx::tma_load_2d(sQ + t * TB + c * CH, &tm_qkv, q_full, h * HD + 64 * c, row0 + qb * 256 + t * 128);
         for (int j = 0; j < n; ++j) {
           const int st = j % ST, use = j / ST;
-          WAIT(&k_empty[st], (use & 1) ^ 1, 60);
+          WAIT_SPIN(&k_empty[st], (use & 1) ^ 1, 60);
           ptx::mbar_arrive_expect_tx(&k_full[st], TB);
           for (int c = 0; c < NC; ++c)
             ptx::tma_load_2d(sK + st * TB + c * CH, &tm_qkv, &k_full[st], dt + h * HD + 64 * c, row0 + j * 128);
-          WAIT(&v_empty[st], (use & 1) ^ 1, 61);
+          WAIT_SPIN(&v_empty[st], (use & 1) ^ 1, 61);
           ptx::mbar_arrive_expect_tx(&v_full[st], TB);
           for (int c = 0; c < NC; ++c)
             ptx::tma_load_2d(sV + st * TB + c * CH, &tm_qkv, &v_full[st], 2 * dt + h * HD + 64 * c, row0 + j * 128);
@@ -807,8 +809,8 @@ __global__ void __launch_bounds__(TcFwd2Cfg<HD, CS>::kThreads, 1)
                              ptx::smem_desc_sw128(av + kk * 2048, CH, 1024), id_o, (j > 0 || kk > 0) ? 1u : 0u);
         ptx::mma_commit_w(&pv_done[t]);
       };
-      WAIT(q_full, 0, 62);
-      WAIT(&k_full[0], 0, 63);
+      WAIT_SPIN(q_full, 0, 62);
+      WAIT_SPIN(&k_full[0], 0, 63);
       ptx::tc_fence_after();
       issue_s(0, 0);
       issue_s(1, 0);
@@ -816,17 +818,17 @@ __global__ void __launch_bounds__(TcFwd2Cfg<HD, CS>::kThreads, 1)
       for (int j = 0; j < n; ++j) {
         const int st = j % ST, st1 = (j + 1) % ST;
         const bool next = j + 1 < n;
-        WAIT(&v_full[st], (j / ST) & 1, 64);
-        if (next) WAIT(&k_full[st1], ((j + 1) / ST) & 1, 65);
+        WAIT_SPIN(&v_full[st], (j / ST) & 1, 64);
+        if (next) WAIT_SPIN(&k_full[st1], ((j + 1) / ST) & 1, 65);
         if (j < n - 1) {  // tile 0 (its last kv tile is n - 2)
-          WAIT(&p_full[0], j & 1, 66);
+          WAIT_SPIN(&p_full[0], j & 1, 66);
           ATTN_TRACE(0, j);
           ptx::tc_fence_after();
           issue_pv(0, j);
           if (j + 1 < n - 1) issue_s(0, j + 1);
           ATTN_TRACE(1, j);
         }
-        WAIT(&p_full[1], j & 1, 67);
+        WAIT_SPIN(&p_full[1], j & 1, 67);
         ATTN_TRACE(2, j);
         ptx::tc_fence_after();
         issue_pv(1, j);
@@ -853,7 +855,7 @@ __global__ void __launch_bounds__(TcFwd2Cfg<HD, CS>::kThreads, 1)
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < nt; ++j) {
       if (tw) ATTN_TRACE(4 + 5 * t, j);
-      WAIT(&s_full[t], j & 1, 68);
+      WAIT_SPIN(&s_full[t], j & 1, 68);
       if (tw) ATTN_TRACE(5 + 5 * t, j);
       ptx::tc_fence_after();
       float x[CW];
@@ -893,7 +895,7 @@ __global__ void __launch_bounds__(TcFwd2Cfg<HD, CS>::kThreads, 1)
       if (__any_sync(0xffffffffu, mt > m_used + 8.f)) {
         const float m_new = fmaxf(m_used, mt);
         if (j > 0) {  // O_t holds PV_t(0..j-1) once pv_done completes phase j-1
-          WAIT(&pv_done[t], (j - 1) & 1, 69);
+          WAIT_SPIN(&pv_done[t], (j - 1) & 1, 69);
           const float f = exp2f(m_used - m_new);
           l *= f;
           ptx::tc_fence_after();
@@ -947,7 +949,7 @@ __global__ void __launch_bounds__(TcFwd2Cfg<HD, CS>::kThreads, 1)
 #pragma unroll
       for (int o = 1; o < CS; ++o) l_tot += xrow[((part + o) % CS) * 128 + r];
     }
-    WAIT(&pv_done[t], (nt - 1) & 1, 70);
+    WAIT_SPIN(&pv_done[t], (nt - 1) & 1, 70);
     ptx::tc_fence_after();
     const int q_row = qb * 256 + t * 128 + r;
     const float inv = 1.f / l_tot;

@@ -22,13 +22,6 @@
 #include "sm100_ptx.cuh"
 #include "tma_host.h"
 
-// mbarrier waits: spinning try_wait (default) or the suspend-hinted form (-DGPTB200_WAIT_SLEEP, A/B)
-#ifdef GPTB200_WAIT_SLEEP
-#define GEMM_WAIT(bar, par) ptx::mbar_wait(bar, par)
-#else
-#define GEMM_WAIT(bar, par) ptx::mbar_wait_spin(bar, par)
-#endif
-
 namespace gptb200 {
 
 namespace {
@@ -173,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = mb * kTileM + rank * kBM;
         auto n0_of = [&](int ns) { return nb * BN + ns * (BN / kNsub) + rank * kNsubRows; };
         for (int kb = 0; kb < kblocks; ++kb) {
-          GEMM_WAIT(&empty[stage], phase ^ 1);
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::kStageBytes;
           uint8_t* sb = sa + Cfg::kABytes;
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], CG * Cfg::kStageBytes);
@@ -217,11 +210,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kblocks = slice_begin(kslice + 1) - slice_begin(kslice);
         const int acc = kAccBufs == 2 ? (it & 1) : 0;
         const int use = kAccBufs == 2 ? (it >> 1) : it;
-        GEMM_WAIT(&tempty[acc], (use & 1) ^ 1);
+        ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < kblocks; ++kb) {
-          GEMM_WAIT(&full[stage], phase);
+          ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint32_t sa = ptx::smem_u32(smem + stage * Cfg::kStageBytes);
           const uint32_t sb = sa + Cfg::kABytes;
@@ -271,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int mb, nb;
       tile_coords(tile, num_m, num_n, mb, nb);
       const int acc = kAccBufs == 2 ? (it & 1) : 0;
-      GEMM_WAIT(&tfull[acc], ((kAccBufs == 2 ? (it >> 1) : it)) & 1);
+      ptx::mbar_wait(&tfull[acc], ((kAccBufs == 2 ? (it >> 1) : it)) & 1);
       ptx::tc_fence_after();
       const int row_base = mb * kTileM + rank * kBM + 32 * q;
       const int row = row_base + lane;
