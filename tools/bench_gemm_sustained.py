@@ -67,6 +67,10 @@ def main():
     if os.environ.get("SHAPES") == "mbs16":  # 1.4B step shapes at M = 32768 tokens
         shapes = [(32768, 6144, 2048, 0, 0, 0), (32768, 8192, 2048, 0, 0, 1), (32768, 2048, 2048, 0, 1, 0),
                   (32768, 2048, 8192, 0, 1, 0), (32768, 8192, 2048, 0, 1, 3)]
+    if os.environ.get("SHAPES") == "mbs32":  # 1.4B step shapes at M = 65536 tokens (the bench default)
+        shapes = [(65536, 6144, 2048, 0, 0, 0), (65536, 8192, 2048, 0, 0, 1), (65536, 2048, 2048, 0, 1, 0),
+                  (65536, 2048, 8192, 0, 1, 0), (2048, 8192, 65536, 1, 1, 2),
+                  (8192, 2048, 65536, 1, 1, 2)]
     if os.environ.get("SHAPES") == "longk":
         shapes = [(8192, 8192, 8192, 0, 0, 0), (16384, 2048, 8192, 0, 1, 0), (8192, 2048, 16384, 1, 1, 2)]
     ldaux = int(os.environ.get("LDAUX", "0"))  # experiment hook (no effect in the product build)
