@@ -25,13 +25,15 @@ int flash_attn_fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat1
 // (D must already hold rowsum(dO*O)).
 int flash_attn_bwd_tc_main(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout,
                            const float* lse, const float* D, float* dq_acc, __nv_bfloat16* dqkv,
-                           cudaStream_t st);
+                           cudaStream_t st, float* dbqkv = nullptr);
 
 // Writes dqkv[M, 3*heads*hd]. Workspaces: D[batch*heads*seq] fp32, dq_acc[M*heads*hd] fp32.
 // d_ready: D = rowsum(dO * O) was already produced (fused into the dO GEMM epilogue); only the
 // dQ accumulator is cleared before the main kernel.
+// dbqkv (fp32, 3*heads*hd, accumulated +=): the qkv bias gradient (column sums of dqkv) for hd 128,
+// folded into the kernels; returns with it untouched for other head dims (the caller sums dqkv).
 int flash_attn_bwd(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* out,
                    const __nv_bfloat16* dout, const float* lse, float* D, float* dq_acc,
-                   __nv_bfloat16* dqkv, cudaStream_t st, bool d_ready = false);
+                   __nv_bfloat16* dqkv, cudaStream_t st, bool d_ready = false, float* dbqkv = nullptr);
 
 }  // namespace gptb200

@@ -1259,6 +1259,23 @@ __global__ void __launch_bounds__(320, 1)
 // issuer (warp 1); WG1-2 = P/dS compute (TMEM lane quarter x 32-query half); WG3 = dQ flush, one
 // warp per 32 head dims, each staging its own [64 q][32 hd] box and issuing its own TMA
 // reduce-add, so the flush of tile j-1 runs concurrently with the P/dS math of tile j.
+// Column sums over a warp's 32 rows (lane = row) of 32 columns (x[e] = column e of this lane's row):
+// a butterfly in which every level halves the columns a lane carries; lane l ends with column l.
+// 31 shuffles for 32 columns. Used to fold the qkv bias gradient into the backward's dK / dV epilogue.
+__device__ __forceinline__ float warp_colsum32(float (&x)[32], int lane) {
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const bool up = (lane & w) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = up ? x[i] : x[i + w];
+      const float keep = up ? x[i + w] : x[i];
+      x[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+    }
+  }
+  return x[0];
+}
+
 template <int HD>
 struct TcBwd2Cfg {
   static constexpr int NC = HD / 64;
@@ -1281,7 +1298,7 @@ __global__ void __launch_bounds__(512, 1)
     fa_bwd_tc2_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
                       const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse,
                       const float* __restrict__ Dg, float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv,
-                      int s, int ht, float scale_log2, float scale) {
+                      float* __restrict__ dbqkv, int s, int ht, float scale_log2, float scale) {
   using Cfg = TcBwd2Cfg<HD>;
   constexpr int NC = Cfg::NC, TB = Cfg::kTileBytes;
   extern __shared__ uint8_t smem_raw[];
@@ -1573,6 +1590,15 @@ __global__ void __launch_bounds__(512, 1)
         reinterpret_cast<uint4*>(krow + c * 32)[q] = a;
         reinterpret_cast<uint4*>(vrow + c * 32)[q] = bb2;
       }
+      if (dbqkv) {  // qkv bias gradient, k and v parts: this warp's 32 kv rows of columns c*32..+31
+        float x[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(kv[e]) * scale;
+        atomicAdd(dbqkv + dt + h * HD + c * 32 + lane, warp_colsum32(x, lane));
+#pragma unroll
+        for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(vv[e]);
+        atomicAdd(dbqkv + 2 * dt + h * HD + c * 32 + lane, warp_colsum32(x, lane));
+      }
     }
   }
   __syncthreads();
@@ -1587,7 +1613,7 @@ __global__ void __launch_bounds__(512, 1)
     fa_bwd_tc2_persistent(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
                       const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse,
                       const float* __restrict__ Dg, float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv,
-                      int s, int ht, int batch, float scale_log2, float scale) {
+                      float* __restrict__ dbqkv, int s, int ht, int batch, float scale_log2, float scale) {
   using Cfg = TcBwd2Cfg<HD>;
   constexpr int NC = Cfg::NC, TB = Cfg::kTileBytes;
   extern __shared__ uint8_t smem_raw[];
@@ -1884,6 +1910,15 @@ __global__ void __launch_bounds__(512, 1)
         bb2.w = ptx::pack_bf16(__uint_as_float(vv[8 * q + 6]), __uint_as_float(vv[8 * q + 7]));
         reinterpret_cast<uint4*>(krow + c * 32)[q] = a;
         reinterpret_cast<uint4*>(vrow + c * 32)[q] = bb2;
+      }
+      if (dbqkv) {  // qkv bias gradient, k and v parts: this warp's 32 kv rows of columns c*32..+31
+        float x[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(kv[e]) * scale;
+        atomicAdd(dbqkv + dt + h * HD + c * 32 + lane, warp_colsum32(x, lane));
+#pragma unroll
+        for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(vv[e]);
+        atomicAdd(dbqkv + 2 * dt + h * HD + c * 32 + lane, warp_colsum32(x, lane));
       }
     }
     ptx::tc_fence_before();
@@ -2258,9 +2293,47 @@ __global__ void attn_dq_convert_kernel(const float* __restrict__ dq_acc, __nv_bf
   }
 }
 
+// dQ = scale * dq_acc -> bf16 (as attn_dq_convert_kernel) plus the q part of the qkv bias gradient:
+// a block covers 64 rows x 128 columns (8 warps x 8 rows, a lane 4 columns) and adds its column sums
+// into dbq with one fp32 reduction per column.
+__global__ void __launch_bounds__(256) attn_dq_convert_colsum_kernel(const float* __restrict__ dq_acc,
+                                                                     __nv_bfloat16* __restrict__ dqkv, int dt,
+                                                                     float scale, float* __restrict__ dbq) {
+  __shared__ float4 part[8][32];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int col = blockIdx.x * 128 + lane * 4;
+  const size_t r0 = static_cast<size_t>(blockIdx.y) * 64 + warp * 8;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const size_t row = r0 + i;
+    float4 v = reinterpret_cast<const float4*>(dq_acc + row * dt + col)[0];
+    v.x *= scale, v.y *= scale, v.z *= scale, v.w *= scale;
+    acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
+    uint2 pk;
+    pk.x = ptx::pack_bf16(v.x, v.y);
+    pk.y = ptx::pack_bf16(v.z, v.w);
+    *reinterpret_cast<uint2*>(dqkv + row * 3 * dt + col) = pk;
+  }
+  part[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    float4 t = part[0][lane];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+      const float4 u = part[w][lane];
+      t.x += u.x, t.y += u.y, t.z += u.z, t.w += u.w;
+    }
+    atomicAdd(dbq + col, t.x);
+    atomicAdd(dbq + col + 1, t.y);
+    atomicAdd(dbq + col + 2, t.z);
+    atomicAdd(dbq + col + 3, t.w);
+  }
+}
+
 template <int HD>
 int bwd_tc2(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* D,
-            float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st) {
+            float* dq_acc, __nv_bfloat16* dqkv, float* dbqkv, cudaStream_t st) {
   using Cfg = TcBwd2Cfg<HD>;
   static const bool tp = std::getenv("GPTB200_ATTN_BWD_SMEM_P") == nullptr;  // A/B: P^T/dS^T in smem
   const auto kern = tp ? fa_bwd_tc2_kernel<HD, true> : fa_bwd_tc2_kernel<HD, false>;
@@ -2283,7 +2356,7 @@ int bwd_tc2(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* d
     cudaMemcpyToSymbol(g_attn_trace, &tbuf, sizeof(tbuf));
   }
 #endif
-  launch_pdl(kern, grid, dim3(512), Cfg::kSmem, st, tkv, tq, tdo, lse, D, dq_acc, dqkv, a.seq,
+  launch_pdl(kern, grid, dim3(512), Cfg::kSmem, st, tkv, tq, tdo, lse, D, dq_acc, dqkv, dbqkv, a.seq,
              a.heads, scale * kLog2e, scale);
 #ifdef GPTB200_ATTN_TRACE
   if (tbuf) {
@@ -2306,7 +2379,7 @@ int bwd_tc2(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* d
 
 template <int HD>
 int bwd_tc2_persistent(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse,
-                       const float* D, float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st) {
+                       const float* D, float* dq_acc, __nv_bfloat16* dqkv, float* dbqkv, cudaStream_t st) {
   using Cfg = TcBwd2Cfg<HD>;
   if (ensure_dynamic_smem(reinterpret_cast<const void*>(fa_bwd_tc2_persistent<HD>), Cfg::kSmem) != 0) return 3;
   count_variant(KV_ATTN_BWD_PERSISTENT);
@@ -2320,7 +2393,7 @@ int bwd_tc2_persistent(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_
   const int grid = items < device_sm_count() ? items : device_sm_count();
   const float scale = 1.f / sqrtf(static_cast<float>(HD));
   launch_pdl(fa_bwd_tc2_persistent<HD>, dim3(grid), dim3(512), Cfg::kSmem, st, tkv, tq, tdo, lse, D, dq_acc, dqkv,
-             a.seq, a.heads, a.batch, scale * kLog2e, scale);
+             dbqkv, a.seq, a.heads, a.batch, scale * kLog2e, scale);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
@@ -2441,7 +2514,7 @@ int fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, flo
 }  // namespace
 
 int flash_attn_bwd_tc_main(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse,
-                           const float* D, float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st) {
+                           const float* D, float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st, float* dbqkv) {
   if (a.seq % 128 != 0) return 1;
   switch (a.head_dim) {
     case 64: return bwd_tc<64>(a, qkv, dout, lse, D, dq_acc, dqkv, st);
@@ -2452,8 +2525,8 @@ int flash_attn_bwd_tc_main(const AttnShape& a, const __nv_bfloat16* qkv, const _
       static const char* forced = std::getenv("GPTB200_ATTN_BWD_PER_BLOCK");  // A/B switch: 1 / 0
       const int items = (a.seq / 128) * a.batch * a.heads;
       const bool per_block = forced ? forced[0] == '1' : items > 6 * device_sm_count();
-      return per_block ? bwd_tc2<128>(a, qkv, dout, lse, D, dq_acc, dqkv, st)
-                       : bwd_tc2_persistent<128>(a, qkv, dout, lse, D, dq_acc, dqkv, st);
+      return per_block ? bwd_tc2<128>(a, qkv, dout, lse, D, dq_acc, dqkv, dbqkv, st)
+                       : bwd_tc2_persistent<128>(a, qkv, dout, lse, D, dq_acc, dqkv, dbqkv, st);
     }
     case 160: return bwd_tc3<160>(a, qkv, dout, lse, D, dq_acc, dqkv, st);
     default: return 1;
@@ -2465,7 +2538,8 @@ int flash_attn_fwd(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* 
 }
 
 int flash_attn_bwd(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout,
-                   const float* lse, float* D, float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st, bool d_ready) {
+                   const float* lse, float* D, float* dq_acc, __nv_bfloat16* dqkv, cudaStream_t st, bool d_ready,
+                   float* dbqkv) {
   if (a.seq % 128 != 0) return 1;
   const int hd = a.head_dim;
   if (hd != 64 && hd != 128 && hd != 160) return 1;
@@ -2483,13 +2557,21 @@ int flash_attn_bwd(const AttnShape& a, const __nv_bfloat16* qkv, const __nv_bflo
     std::fprintf(stderr, "attention bwd: preprocessing failed: %s\n", cudaGetErrorString(cudaGetLastError()));
     return 3;
   }
-  const int r = flash_attn_bwd_tc_main(a, qkv, dout, lse, D, dq_acc, dqkv, st);
+  // qkv bias gradient folded in (hd 128): k / v column sums in the main kernel's dK / dV epilogue,
+  // q column sums in the dQ conversion; other head dims leave dbqkv to the caller
+  float* dbias = hd == 128 ? dbqkv : nullptr;
+  const int r = flash_attn_bwd_tc_main(a, qkv, dout, lse, D, dq_acc, dqkv, st, dbias);
   if (r != 0) return r;
   if (dbg && cudaStreamSynchronize(st) != cudaSuccess) {
     std::fprintf(stderr, "attention bwd: main kernel failed: %s\n", cudaGetErrorString(cudaGetLastError()));
     return 3;
   }
-  attn_dq_convert_kernel<<<8 * device_sm_count(), 256, 0, st>>>(dq_acc, dqkv, M, dt, 1.f / sqrtf(static_cast<float>(hd)));
+  if (dbias)
+    attn_dq_convert_colsum_kernel<<<dim3(dt / 128, M / 64), 256, 0, st>>>(dq_acc, dqkv, dt,
+                                                                          1.f / sqrtf(static_cast<float>(hd)), dbias);
+  else
+    attn_dq_convert_kernel<<<8 * device_sm_count(), 256, 0, st>>>(dq_acc, dqkv, M, dt,
+                                                                  1.f / sqrtf(static_cast<float>(hd)));
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 

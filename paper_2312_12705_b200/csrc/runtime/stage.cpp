@@ -719,9 +719,11 @@ void Stage::layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2)
     gemm_wgrad(dy_, A.o, G.wo, M_, d_, dt_);
     {
       KScope prof(this, K_ATTN_BWD, 5.0 * mbs_ * ht_ * static_cast<double>(s_) * s_ * hd_);
-      ck(flash_attn_bwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, do_, A.lse, attn_D_, dq_acc_, dqkv_, st_, fuse_d), "flash bwd");
+      // hd 128: the qkv bias gradient is folded into the attention backward kernels
+      ck(flash_attn_bwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, do_, A.lse, attn_D_, dq_acc_, dqkv_, st_, fuse_d, G.bqkv),
+         "flash bwd");
     }
-    {
+    if (hd_ != 128) {
       KScope prof(this, K_ELEM);
       ck(colsum_bf16(dqkv_, M_, 3 * dt_, G.bqkv, ws_, st_), "dbqkv");
     }
@@ -759,9 +761,10 @@ void Stage::layer_bwd(int l, LayerActs& A, const bf16* hin, bf16* dh, bf16* dy2)
   gemm_wgrad(dya, A.o, G.wo, M_, d_, dt_);
   {
     KScope prof(this, K_ATTN_BWD, 5.0 * mbs_ * ht_ * static_cast<double>(s_) * s_ * hd_);
-    ck(flash_attn_bwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, do_, A.lse, attn_D_, dq_acc_, dqkv_, st_, fuse_d), "flash bwd");
+    ck(flash_attn_bwd({mbs_, s_, ht_, hd_}, A.qkv, A.o, do_, A.lse, attn_D_, dq_acc_, dqkv_, st_, fuse_d, G.bqkv),
+       "flash bwd");
   }
-  {
+  if (hd_ != 128) {
     KScope prof(this, K_ELEM);
     ck(colsum_bf16(dqkv_, M_, 3 * dt_, G.bqkv, ws_, st_), "dbqkv");
   }

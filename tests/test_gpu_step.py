@@ -205,5 +205,8 @@ def test_step_is_reproducible():
     assert _rel(g1, g0) < 1e-6, _rel(g1, g0)
     assert np.abs(g1 - g0).max() <= 1e-5 * np.abs(g0).max()
     # Adam normalises each element by its own history, so a reassociation-level gradient change
-    # moves the update by at most a few ulps of the parameter
-    assert np.abs(w1 - w0).max() <= 1e-6
+    # moves the update by at most a few ulps of the parameter — except where the gradient itself is
+    # at the scale of Adam's eps (m / (sqrt(v) + eps) then swings with it; bounded by lr)
+    live = np.abs(g0) > 1e-4 * np.abs(g0).max()
+    assert np.abs(w1 - w0)[live].max() <= 1e-6
+    assert np.abs(w1 - w0).max() <= 1e-3
