@@ -299,6 +299,8 @@ def main():
     clocks = ClockSampler(list(range(world))) if rank == 0 else None
     ms, _ = sess.time_steps(args.steps, profile=False)
     ms_max = sess.allreduce_max(ms)
+    # per-step device times of the same timed region (events between steps), max over ranks per step
+    per_step = [sess.allreduce_max(t) for t in sess.step_times(args.steps)]
     sess.barrier()
     clk = clocks.stop() if clocks else None
     info = sess.info()
@@ -335,6 +337,9 @@ def main():
                           "of_measured_sustained": tflops_gpu / peaks["bf16_tflops_sustained"],
                           "peaks_source": peak_src},
         "tokens_per_s_per_gpu": tok_s / world,
+        # spread of the K timed steps: per-step device ms, max over ranks per step
+        "step_ms": {"median": float(np.median(per_step)), "p10": float(np.percentile(per_step, 10)),
+                    "p90": float(np.percentile(per_step, 90)), "min": min(per_step), "max": max(per_step)},
         "loss": loss,
         "e2e": {"value": e2e_tok_s, "unit": "tokens/s", "h2d_bytes_per_step": int(tokens.nbytes),
                 "d2h_bytes_per_step": 4},

@@ -213,6 +213,9 @@ typedef struct tp_kernel_times {
 /* Runs `steps` iterations on the uploaded tokens between two CUDA events on the session stream;
  * *ms = device time. With profile != 0 every launch is bracketed by events into *kt. */
 int tp_session_time_steps(tp_session* s, int steps, int profile, float* ms, tp_kernel_times* kt);
+/* Device ms of each step of the last tp_session_time_steps call (CUDA events recorded between
+ * consecutive steps on the step stream, no host sync in between): out[0..min(n, steps)). */
+int tp_session_step_times(tp_session* s, float* out, int n);
 /* Watchdog for every host wait of the session (sync, loss read, timed steps): after `seconds`
  * without progress the session aborts its NCCL communicators (ncclCommAbort) and the call returns
  * TP_ERR_TIMEOUT (trainplan::FailureKind::Timeout, search.hpp:59); the session is unusable

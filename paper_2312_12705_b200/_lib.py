@@ -105,6 +105,7 @@ SIGNATURES: dict[str, tuple] = {
     "tp_session_read_flat": (_i, [_vp, _i, _i64, _i64, _vp]),
     "tp_session_buckets": (_i, [_vp, C.POINTER(_i64), _i, C.POINTER(_i)]),
     "tp_session_time_steps": (_i, [_vp, _i, _i, C.POINTER(_f), C.POINTER(KernelTimes)]),
+    "tp_session_step_times": (_i, [_vp, C.POINTER(_f), _i]),
     "tp_session_allreduce_max": (_i, [_vp, C.POINTER(_f)]),
     "tp_session_debug_tp_allreduce": (_i, [_vp, _vp, _vp, _i]),
     "tp_session_bench_tp_allreduce": (_i, [_vp, _i, _i, _i, C.POINTER(_f), C.POINTER(_i)]),
@@ -366,6 +367,12 @@ class Session:
         kt = KernelTimes()
         check(self._lib.tp_session_time_steps(self.h, steps, int(profile), C.byref(ms), C.byref(kt)))
         return ms.value, (kt.as_dict() if profile else None)
+
+    def step_times(self, steps: int) -> list:
+        """Device ms of each step of the last time_steps call."""
+        out = (_f * steps)()
+        check(self._lib.tp_session_step_times(self.h, out, steps))
+        return list(out)
 
     def allreduce_max(self, v: float) -> float:
         x = _f(v)

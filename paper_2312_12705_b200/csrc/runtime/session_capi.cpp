@@ -177,6 +177,13 @@ int tp_session_info(tp_session* s, int64_t out[8]) {
   });
 }
 
+int tp_session_step_times(tp_session* s, float* out, int n) {
+  return run("tp_session_step_times", [&] {
+    const std::vector<float>& t = s->stage->step_times();
+    for (int i = 0; i < n && i < static_cast<int>(t.size()); ++i) out[i] = t[i];
+  });
+}
+
 int tp_session_time_steps(tp_session* s, int steps, int profile, float* ms, tp_kernel_times* kt) {
   return run("tp_session_time_steps", [&] {
     KernelTimes k;

@@ -1175,25 +1175,32 @@ void Stage::read_tensor(int which, int tid, float* host) const {
 namespace gptb200 {
 
 float Stage::time_steps(int steps, bool profile, KernelTimes* kt) {
-  cudaEvent_t a, b;
-  cudaEventCreate(&a);
-  cudaEventCreate(&b);
+  // one event between consecutive steps (no host sync inside the timed region): the total and the
+  // per-step device times (step_ms_) for the spread
+  std::vector<cudaEvent_t> ev(static_cast<size_t>(steps) + 1);
+  for (auto& e : ev) cudaEventCreate(&e);
+  auto destroy = [&] {
+    for (auto& e : ev) cudaEventDestroy(e);
+  };
   profile_ = profile;
   ev_used_ = 0;
   prof_acc_ = KernelTimes{};
-  cudaEventRecord(a, st_);
+  cudaEventRecord(ev[0], st_);
   try {
-    for (int i = 0; i < steps; ++i) step();
+    for (int i = 0; i < steps; ++i) {
+      step();
+      cudaEventRecord(ev[i + 1], st_);
+    }
   } catch (...) {
     profile_ = false;
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
+    destroy();
     throw;
   }
-  cudaEventRecord(b, st_);
   sync();
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, a, b);
+  cudaEventElapsedTime(&ms, ev[0], ev[steps]);
+  step_ms_.assign(steps, 0.f);
+  for (int i = 0; i < steps; ++i) cudaEventElapsedTime(&step_ms_[i], ev[i], ev[i + 1]);
   if (profile && kt) {
     *kt = prof_acc_;
     for (int k = 0; k < K_NUM; ++k) kt->ms[k] = 0;
@@ -1204,8 +1211,7 @@ float Stage::time_steps(int steps, bool profile, KernelTimes* kt) {
     }
   }
   profile_ = false;
-  cudaEventDestroy(a);
-  cudaEventDestroy(b);
+  destroy();
   return ms;
 }
 

@@ -119,6 +119,8 @@ class Stage {
   // Runs `steps` iterations bracketed by CUDA events on the step stream; returns device ms.
   // With profile, every launch is bracketed too and summed per KernelClass into *kt.
   float time_steps(int steps, bool profile, KernelTimes* kt);
+  // Device ms of each step of the last time_steps call (events between consecutive steps).
+  const std::vector<float>& step_times() const { return step_ms_; }
   float allreduce_max(float v);
   // TP allreduce of the [M, d] bf16 activation buffer (test / microbenchmark hooks).
   // mode 0 = automatic (NVLS when available), 1 = ncclAllReduce. in/out: M*d bf16 bit patterns.
@@ -279,6 +281,7 @@ class Stage {
   bf16* logits_ = nullptr;
   float *xstats_ = nullptr, *xall_ = nullptr, *row_loss_ = nullptr, *loss_acc_ = nullptr;
   StepTimes times_;
+  std::vector<float> step_ms_;
 };
 
 }  // namespace gptb200
