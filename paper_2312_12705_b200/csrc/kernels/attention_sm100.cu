@@ -2465,8 +2465,9 @@ struct TraceDump {
 template <int HD, int CS>
 int fwd_tc2q_cs(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, cudaStream_t st, int emu) {
   using Cfg = TcFwd2Cfg<HD, CS>;
-  const auto kern = emu <= 0 ? fa_fwd2_kernel<HD, 0, CS> : emu == 1 ? fa_fwd2_kernel<HD, 1, CS>
-                  : emu == 2 ? fa_fwd2_kernel<HD, 2, CS> : emu == 3 ? fa_fwd2_kernel<HD, 3, CS> : fa_fwd2_kernel<HD, 4, CS>;
+  // EMU 2 (2 of every 8 exponent pairs on the FMA pipe) is the measured best of 0..4; 0 (all on the
+  // MUFU) stays instantiated as the A/B reference
+  const auto kern = emu == 0 ? fa_fwd2_kernel<HD, 0, CS> : fa_fwd2_kernel<HD, 2, CS>;
   if (ensure_dynamic_smem(reinterpret_cast<const void*>(kern), Cfg::kSmem) != 0) return 3;
   count_variant(KV_ATTN_FWD_TWO_Q);
   const int dt = a.heads * HD;
@@ -2487,11 +2488,9 @@ int fwd_tc2q(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat16* out, f
     const char* e = std::getenv("GPTB200_ATTN_FWD_EMU");
     return e ? std::atoi(e) : 2;  // measured best of 0..4 (1.4B shapes: 865 / 901 TF/s; 0: 855 / 883)
   }();
-  static const int cs = [] {
-    const char* e = std::getenv("GPTB200_ATTN_FWD_CS");
-    return e ? std::atoi(e) : 1;  // 2 warps per row measured 3 % slower (more row-max exchange than gain)
-  }();
-  return cs == 1 ? fwd_tc2q_cs<HD, 1>(a, qkv, out, lse, st, emu) : fwd_tc2q_cs<HD, 2>(a, qkv, out, lse, st, emu);
+  // one softmax warp per 32 rows (CS = 1): 2 warps per row measured 3 % slower (more row-max exchange
+  // than gain); the CS template parameter keeps that variant available for experiments
+  return fwd_tc2q_cs<HD, 1>(a, qkv, out, lse, st, emu);
 }
 
 template <int HD>
@@ -2582,11 +2581,12 @@ int flash_attn_fwd_tc(const AttnShape& a, const __nv_bfloat16* qkv, __nv_bfloat1
   // persistent CTAs' prologue overlap matters more behind the QKV GEMM), so it stays an A/B switch.
   static const bool per_block = std::getenv("GPTB200_ATTN_FWD_PER_BLOCK") != nullptr;
   // two query tiles per CTA (fa_fwd2_kernel) when its grid of 256-row blocks fills the GPU at least
-  // twice: 1.4B MBS 32 / 8: 865 / 901 vs 703 / 766 TF/s; with fewer blocks (tensor-parallel shapes,
-  // 12 heads x 8 blocks) the persistent one-tile kernel keeps every SM busy (555 vs 351 TF/s).
+  // once: 1.4B MBS 32 / 8: 865 / 901 vs 703 / 766 TF/s; tensor-parallel shapes with 192 blocks (24 heads
+  // x 8 or 2 x 12 x 8): 758 / 751 vs 672 / 659; with fewer blocks (12 heads x 8) the persistent one-tile
+  // kernel keeps every SM busy (555 vs 386 TF/s). `profiles/r02_attn_fwd_tp_shapes.txt`.
   static const char* two_q_env = std::getenv("GPTB200_ATTN_FWD_2Q");  // A/B: 1 always, 0 never
   const int blocks256 = a.batch * a.heads * (a.seq / 256);
-  const bool two_q = two_q_env ? two_q_env[0] == '1' : blocks256 >= 2 * device_sm_count();
+  const bool two_q = two_q_env ? two_q_env[0] == '1' : blocks256 >= device_sm_count();
   if (two_q && a.seq % 256 == 0 && (a.head_dim == 64 || a.head_dim == 128) && !per_block)
     return a.head_dim == 64 ? fwd_tc2q<64>(a, qkv, out, lse, st) : fwd_tc2q<128>(a, qkv, out, lse, st);
   switch (a.head_dim) {
