@@ -210,3 +210,19 @@ def test_step_is_reproducible():
     live = np.abs(g0) > 1e-4 * np.abs(g0).max()
     assert np.abs(w1 - w0)[live].max() <= 1e-6
     assert np.abs(w1 - w0).max() <= 1e-3
+
+
+def test_timed_steps_and_per_step_spread():
+    """tp_session_time_steps times K back-to-back steps with CUDA events; tp_session_step_times returns
+    each step's device time from events recorded between the steps (the bench's spread): positive,
+    and they add up to the total."""
+    spec = T.ModelSpec(2, 512, 4, 2048, 256)
+    cfg = T.ParallelConfig(tp=1, pp=1, dp=1, mbs=2, gbs=4, zero_stage=1)
+    tokens = O.gen_tokens(1234, 4 * 257, 2048).reshape(4, 257)
+    with T.Session(spec, cfg, T.TrainOptions(seed=7, lr=1e-3)) as sess:
+        sess.init_params()
+        sess.upload_tokens(tokens)
+        total, _ = sess.time_steps(4)
+        per = sess.step_times(4)
+    assert all(t > 0 for t in per), per
+    assert abs(sum(per) - total) <= 1e-3 * total + 0.05, (per, total)
