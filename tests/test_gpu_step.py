@@ -178,9 +178,10 @@ def test_step_parity_1p4b_width_pair_512_tiles():
 
 
 def test_step_parity_1p4b_width_checkpointing_small_batch():
-    # MBS 2: two-pass LayerNorm backward, persistent attention forward and backward, recompute
+    # MBS 1 (128 query blocks of 256 rows, under one wave: the one-tile persistent forward), two-pass
+    # LayerNorm backward, persistent attention backward, recompute
     T.variant_counts_reset()
-    run_parity(L=2, d=2048, heads=16, V=8192, s=2048, mbs=2, gbs=4, ckpt=True)
+    run_parity(L=2, d=2048, heads=16, V=8192, s=2048, mbs=1, gbs=2, ckpt=True)
     v = T.variant_counts()
     assert v["attn_bwd_persistent"] > 0 and v["attn_fwd_persistent"] > 0 and v["ln_bwd_two_pass"] > 0, v
 
