@@ -691,6 +691,8 @@ __device__ __forceinline__ float2 exp2_fma2(float a, float b) {
                      __int_as_float(__float_as_int(pv.y) + (__float_as_int(tv.y) << 23)));
 }
 
+constexpr int kFwd2HeadGroup = 32;  // (sequence, head) pairs per L2-resident launch group of fa_fwd2
+
 template <int HD, int CS>
 struct TcFwd2Cfg {
   static constexpr int NC = HD / 64;
@@ -737,8 +739,16 @@ __global__ void __launch_bounds__(TcFwd2Cfg<HD, CS>::kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
-  const int qb = gridDim.y - 1 - blockIdx.y;  // heaviest query blocks first (y-major launch order)
-  const int b = blockIdx.x / ht, h = blockIdx.x % ht;
+  // Launch order: groups of kFwd2HeadGroup (sequence, head) pairs, heaviest query blocks of the group
+  // first. A group's K/V (1 MB per head at s 2048) stays in L2 while its blocks run, instead of every
+  // head's K/V being re-read from HBM once per query block (heaviest-first over all heads).
+  const int nqb = gridDim.y, BH = gridDim.x;
+  const int t = blockIdx.y * BH + blockIdx.x;
+  const int grp = t / (nqb * kFwd2HeadGroup), rem = t % (nqb * kFwd2HeadGroup);
+  const int gsz = min(kFwd2HeadGroup, BH - grp * kFwd2HeadGroup);
+  const int qb = nqb - 1 - rem / gsz;
+  const int bh = grp * kFwd2HeadGroup + rem % gsz;
+  const int b = bh / ht, h = bh % ht;
   const int dt = ht * HD;
   const int row0 = b * s;
   const int n = 2 * qb + 2;  // kv tiles of tile 1; tile 0 uses the first n - 1
