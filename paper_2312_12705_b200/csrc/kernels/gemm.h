@@ -35,6 +35,8 @@ struct GemmParams {
   // vector atomics, which squares up the wave count of the few-tile, long-K weight-gradient GEMMs.
   // 0 = automatic, 1 = off.
   int split_k = 0;
+  // Tile raster: groups of group_m M-blocks sweep all N-blocks (0 = automatic; see gemm_bf16).
+  int group_m = 0;
   // Optional fused row-dot (EPI_BF16 only): rowdot_out[(m / seq * heads + n / hd) * seq + m % seq]
   // += sum over a head's hd columns of bf16(C[m, n]) * rowdot_b[m * ldc + n] (hd = 128; rowdot_out
   // zeroed by the caller). Used for the attention-backward D = rowsum(dO * O) on the dO GEMM.

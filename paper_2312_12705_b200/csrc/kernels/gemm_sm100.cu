@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "gemm.h"
 #include "pdl.cuh"
@@ -67,10 +68,10 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
 }
 
-// Tile order: groups of 8 M-blocks sweep all N-blocks so concurrently running CTAs share
+// Tile order: groups of kGroup M-blocks sweep all N-blocks so concurrently running CTAs share
 // both operand panels in L2.
-__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
-  constexpr int kGroup = 8;
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int kGroup, int& mb, int& nb) {
+  if (kGroup <= 0) kGroup = 8;
   int group = tile / (kGroup * num_n);
   int first_m = group * kGroup;
   int gsize = min(kGroup, num_m - first_m);
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int tile = unit % num_tiles, kslice = unit / num_tiles;
         const int kb0 = slice_begin(kslice), kblocks = slice_begin(kslice + 1) - kb0;
         int mb, nb;
-        tile_coords(tile, num_m, num_n, mb, nb);
+        tile_coords(tile, num_m, num_n, p.group_m, mb, nb);
         const int m0 = mb * kTileM + rank * kBM;
         auto n0_of = [&](int ns) { return nb * BN + ns * (BN / kNsub) + rank * kNsubRows; };
         for (int kb = 0; kb < kblocks; ++kb) {
@@ -262,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int unit = cluster_id; unit < num_units; unit += num_clusters, ++it) {
       const int tile = unit % num_tiles;
       int mb, nb;
-      tile_coords(tile, num_m, num_n, mb, nb);
+      tile_coords(tile, num_m, num_n, p.group_m, mb, nb);
       const int acc = kAccBufs == 2 ? (it & 1) : 0;
       ptx::mbar_wait(&tfull[acc], ((kAccBufs == 2 ? (it >> 1) : it)) & 1);
       ptx::tc_fence_after();
@@ -602,6 +603,22 @@ int g_force_cg = 0;  // test hook: 1 or 2 forces the CTA-group choice (0 = autom
 // K-slice count for an accumulating fp32 GEMM: the S (slices >= 1024 deep) that best fills the
 // last wave of `slots` concurrent tiles, charging each extra slice for its fp32 reduction traffic
 // (measured: ~3% of the GEMM per extra slice at K = 16384, i.e. ~500/K).
+// Raster group: 8 M-blocks by default. Weight-gradient GEMMs (fp32 accumulate, few output tiles,
+// K = tokens) stream both operands from HBM: the raster runs fastest along the shorter tile dimension
+// of C, so the co-resident tiles share the long operand panels (measured at the 1.4B MBS-32 shapes,
+// DRAM bytes per launch: QKV wgrad 2.71 -> 2.23 GB, fc1 3.64 -> 3.17 GB with group 1; fc2 best at
+// group >= num_m; `profiles/r02_gemm_group.txt`).
+int choose_group(const GemmParams& p, int num_m, int num_n, int slots) {
+  static const int forced = [] {
+    const char* e = std::getenv("GPTB200_GEMM_GROUP");  // A/B switch: fixed group for every GEMM
+    return e ? std::atoi(e) : 0;
+  }();
+  (void)slots;
+  if (forced > 0) return forced;
+  if (p.epi == EPI_F32 && p.accumulate) return num_m >= num_n ? 1 : num_m;
+  return 8;
+}
+
 int choose_split(const GemmParams& p, int tiles, int slots) {
   if (p.split_k > 0) return p.split_k;
   if (p.epi != EPI_F32 || !p.accumulate) return 1;
@@ -650,14 +667,17 @@ int gemm_bf16(const GemmParams& p, cudaStream_t stream) {
                          static_cast<double>(t512) / (((t512 + slots - 1) / slots) * slots) >= 0.97;
   if ((g_force_cg == 3 && p512_ok) || (g_force_cg == 0 && p512_auto)) {
     q.split_k = choose_split(p, (p.M / 256) * (p.N / 512), num_sms() / 2);
+    q.group_m = choose_group(p, p.M / 256, p.N / 512, num_sms() / 2);
     return dispatch_epi<512, 2>(q, stream);
   }
   if (g_force_cg == 2 ? pair_ok : (g_force_cg == 0 && pair_wave)) {
     q.split_k = choose_split(p, (p.M / 256) * (p.N / 256), num_sms() / 2);
+    q.group_m = choose_group(p, p.M / 256, p.N / 256, num_sms() / 2);
     return dispatch_epi<256, 2>(q, stream);
   }
   const int bn = (p.N % 256 == 0) && (p.M / kBM) * (p.N / 256) >= num_sms() ? 256 : (p.N % 128 == 0 ? 128 : 64);
   q.split_k = choose_split(p, (p.M / kBM) * (p.N / bn), num_sms());
+  q.group_m = choose_group(p, p.M / kBM, p.N / bn, num_sms());
   if (bn == 256) return dispatch_epi<256, 1>(q, stream);
   if (bn == 128) return dispatch_epi<128, 1>(q, stream);
   return dispatch_epi<64, 1>(q, stream);
