@@ -615,7 +615,9 @@ int choose_group(const GemmParams& p, int num_m, int num_n, int slots) {
   }();
   (void)slots;
   if (forced > 0) return forced;
-  if (p.epi == EPI_F32 && p.accumulate) return num_m >= num_n ? 1 : num_m;
+  // measured on the long-K (K = tokens >= 16384) weight gradients of the data-parallel shapes; the
+  // tensor-parallel ones (K = 2048..8192 tokens, large C) keep the group of 8
+  if (p.epi == EPI_F32 && p.accumulate && p.K >= 16384) return num_m >= num_n ? 1 : num_m;
   return 8;
 }
 
