@@ -44,6 +44,10 @@ struct GemmParams {
   // colsum_part[(m / 32) * N + n] = sum of C[m', n] over the 32-row block of m (deterministic;
   // reduce over the M/32 blocks afterwards). Used for the fc1 bias gradient from dGeLU(dgrad).
   float* colsum_part = nullptr;
+  // Optional per-row softmax statistics of the stored bf16 C (EPI_BF16, N % 128 == 0): rowstat_part
+  // [m * (N / 64) + n / 64] = (max, sum exp(x - max)) over the 64 columns [n, n + 64) of row m. The LM
+  // head uses them so the cross-entropy statistics need not re-read the [M, V] logits.
+  float2* rowstat_part = nullptr;
   float* rowdot_out = nullptr;
   const __nv_bfloat16* rowdot_b = nullptr;
   int rowdot_seq = 0, rowdot_heads = 0;

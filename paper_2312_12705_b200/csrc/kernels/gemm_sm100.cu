@@ -15,6 +15,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 
@@ -307,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c2 = ehalf * (BN / 128); c2 < (ehalf + 1) * (BN / 128); ++c2) {  // 64-column units
             uint32_t g[2][16];
             float rowdot = 0.f;
+            float rs_m = -INFINITY, rs_s = 0.f;  // online (max, sum exp) of this row's 64 stored values
             // dGeLU: this row's 64 pre-activation values are loaded before the TMEM reads so the
             // two latencies overlap (the epilogue bounds the dgrad GEMM's tensor-pipe activity)
             uint4 auxv[2][4];
@@ -380,12 +382,35 @@ __global__ void __launch_bounds__(kThreads, 1)
                   g[hh][j] = ptx::pack_bf16(gelu_tanh(f.x), gelu_tanh(f.y));
                 }
               }
+              if constexpr (EPI == EPI_BF16) {
+                if (p.rowstat_part != nullptr) {
+                  constexpr float kL2e = 1.4426950408889634f;
+                  float mx = rs_m;
+#pragma unroll
+                  for (int j = 0; j < 16; ++j) {
+                    const float2 f = ptx::unpack_bf16(packed[j]);
+                    mx = fmaxf(mx, fmaxf(f.x, f.y));
+                  }
+                  float acc = rs_s * exp2f((rs_m - mx) * kL2e);
+#pragma unroll
+                  for (int j = 0; j < 16; ++j) {
+                    const float2 f = ptx::unpack_bf16(packed[j]);
+                    acc += exp2f((f.x - mx) * kL2e) + exp2f((f.y - mx) * kL2e);
+                  }
+                  rs_m = mx;
+                  rs_s = acc;
+                }
+              }
               if (hh == 0) box_free();
 #pragma unroll
               for (int j = 0; j < 4; ++j)
                 put(4 * hh + j, make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]));
             }
             flush(&tmC, nb * BN + c2 * 64, false);
+            if constexpr (EPI == EPI_BF16) {
+              if (p.rowstat_part != nullptr)
+                p.rowstat_part[static_cast<size_t>(row) * (p.N / 64) + (nb * BN + c2 * 64) / 64] = make_float2(rs_m, rs_s);
+            }
             if constexpr (EPI == EPI_BF16 || EPI == EPI_DGELU) {
               if (p.colsum_part != nullptr) {  // this warp's 32 rows x 64 columns, from the staged box
                 float s0 = 0.f, s1 = 0.f;
@@ -652,6 +677,7 @@ int gemm_bf16(const GemmParams& p, cudaStream_t stream) {
   if (p.epi == EPI_DGELU && p.aux == nullptr) return kGemmErrShape;
   if (p.split_k > 1 && (p.epi != EPI_F32 || !p.accumulate || p.K / kBK < p.split_k)) return kGemmErrShape;
   if (p.colsum_part && ((p.epi != EPI_BF16 && p.epi != EPI_DGELU) || p.N % 128 != 0)) return kGemmErrShape;
+  if (p.rowstat_part && (p.epi != EPI_BF16 || p.N % 128 != 0)) return kGemmErrShape;
   if (p.rowdot_out && (p.epi != EPI_BF16 || p.N % 128 != 0 || p.rowdot_seq <= 0 || p.M % p.rowdot_seq != 0))
     return kGemmErrShape;
   // CTA pairs (256 x 256 tiles) when the problem yields at least one full wave of pairs;

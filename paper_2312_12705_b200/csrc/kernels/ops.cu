@@ -854,6 +854,48 @@ __global__ void xent_stats_kernel(const bf16* __restrict__ logits, int vcols, co
   }
 }
 
+// Row statistics from the LM-head GEMM's (max, sum exp) partials per 64 columns (GemmParams::
+// rowstat_part): the same (max, sum exp(x - max), target logit) as xent_stats_kernel without re-reading
+// the [rows, vcols] logits (only the target logit of each row).
+__global__ void xent_stats_parts_kernel(const bf16* __restrict__ logits, const float2* __restrict__ parts, int vcols,
+                                        const int32_t* __restrict__ labels, int vstart, float* __restrict__ stats) {
+  __shared__ float redm[32], reds[32];
+  const int row = blockIdx.x;
+  const int np = vcols / 64;
+  const float2* pr = parts + static_cast<size_t>(row) * np;
+  auto combine = [](float& m, float& s, float om, float os) {
+    const float nm = fmaxf(m, om);
+    s = (m == -INFINITY ? 0.f : s * exp2f((m - nm) * kLog2eF)) + (om == -INFINITY ? 0.f : os * exp2f((om - nm) * kLog2eF));
+    m = nm;
+  };
+  float m = -INFINITY, s = 0.f;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    const float2 v = pr[i];
+    combine(m, s, v.x, v.y);
+  }
+  for (int off = 16; off; off >>= 1)
+    combine(m, s, __shfl_xor_sync(0xffffffff, m, off), __shfl_xor_sync(0xffffffff, s, off));
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  if (lane == 0) {
+    redm[warp] = m;
+    reds[warp] = s;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    m = lane < nw ? redm[lane] : -INFINITY;
+    s = lane < nw ? reds[lane] : 0.f;
+    for (int off = 16; off; off >>= 1)
+      combine(m, s, __shfl_xor_sync(0xffffffff, m, off), __shfl_xor_sync(0xffffffff, s, off));
+    if (lane == 0) {
+      const int t = labels[row] - vstart;
+      stats[static_cast<size_t>(row) * 3 + 0] = m;
+      stats[static_cast<size_t>(row) * 3 + 1] = s;
+      stats[static_cast<size_t>(row) * 3 + 2] =
+          (t >= 0 && t < vcols) ? __bfloat162float(logits[static_cast<size_t>(row) * vcols + t]) : 0.f;
+    }
+  }
+}
+
 __global__ void xent_finish_kernel(bf16* __restrict__ logits, int rows, int vcols, const int32_t* __restrict__ labels,
                                    int vstart, const float* __restrict__ all_stats, int tp, float scale,
                                    float* __restrict__ row_loss) {
@@ -1135,6 +1177,13 @@ int xent_stats(const bf16* logits, int rows, int vcols, const int32_t* labels, i
                cudaStream_t st) {
   if (vcols % 8) return 1;
   xent_stats_kernel<<<rows, 512, 0, st>>>(logits, vcols, labels, vstart, stats);
+  return status();
+}
+
+int xent_stats_from_parts(const bf16* logits, const float2* parts, int rows, int vcols, const int32_t* labels,
+                          int vstart, float* stats, cudaStream_t st) {
+  if (vcols % 64) return 1;
+  xent_stats_parts_kernel<<<rows, 256, 0, st>>>(logits, parts, vcols, labels, vstart, stats);
   return status();
 }
 

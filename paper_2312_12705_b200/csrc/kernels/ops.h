@@ -96,6 +96,10 @@ int embed_bwd(const int32_t* tokens, int rows, const bf16* g, int vstart, int vr
 //   scale * (softmax - onehot) (bf16).
 int xent_stats(const bf16* logits, int rows, int vcols, const int32_t* labels, int vstart,
                float* stats, cudaStream_t st);
+// The same statistics from the LM-head GEMM's per-64-column (max, sum exp) partials
+// (GemmParams::rowstat_part, [rows][vcols / 64]); reads only the target logit of each row.
+int xent_stats_from_parts(const bf16* logits, const float2* parts, int rows, int vcols, const int32_t* labels,
+                          int vstart, float* stats, cudaStream_t st);
 int xent_finish(bf16* logits, int rows, int vcols, const int32_t* labels, int vstart,
                 const float* all_stats, int tp, float scale, float* row_loss, cudaStream_t st);
 

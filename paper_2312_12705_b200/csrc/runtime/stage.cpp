@@ -315,6 +315,8 @@ void Stage::allocate() {
     rsf_ = static_cast<float*>(alloc(Ms * 4, ACT));
     logits_ = static_cast<bf16*>(alloc(M * static_cast<size_t>(Vt_) * 2, ACT));
     xstats_ = static_cast<float*>(alloc(M * 3 * 4));
+    // (max, sum exp) per row and 64 logits, written by the LM-head GEMM epilogue
+    if (Vt_ % 128 == 0) rowstat_ = static_cast<float2*>(alloc(M * static_cast<size_t>(Vt_ / 64) * 8));
     xall_ = static_cast<float*>(alloc(M * 3 * 4 * cfg_.tp));
     row_loss_ = static_cast<float*>(alloc(M * 4));
   }
@@ -669,8 +671,22 @@ void Stage::final_ln(const bf16* h) {
 // the loss-scaled softmax - onehot for head_bwd.
 void Stage::head_and_loss(int slot) {
   Slot& S = slots_act_[slot];
-  gemm_fwd(hf_, params_ + slot_offset(0), nullptr, logits_, M_, Vt_, d_);
-  ck(xent_stats(logits_, M_, Vt_, S.labels, comms_.me.t * Vt_, xstats_, st_), "xent stats");
+  if (rowstat_) {  // LM head with the softmax statistics in its epilogue: no extra pass over the logits
+    {
+      KScope prof(this, K_GEMM, 2.0 * M_ * Vt_ * d_);
+      GemmParams p;
+      p.M = M_, p.N = Vt_, p.K = d_;
+      p.A = hf_, p.lda = d_;
+      p.B = params_ + slot_offset(0), p.ldb = d_;
+      p.C = logits_, p.ldc = Vt_, p.epi = EPI_BF16;
+      p.rowstat_part = rowstat_;
+      ck(gemm_bf16(p, st_), "lm head");
+    }
+    ck(xent_stats_from_parts(logits_, rowstat_, M_, Vt_, S.labels, comms_.me.t * Vt_, xstats_, st_), "xent stats");
+  } else {
+    gemm_fwd(hf_, params_ + slot_offset(0), nullptr, logits_, M_, Vt_, d_);
+    ck(xent_stats(logits_, M_, Vt_, S.labels, comms_.me.t * Vt_, xstats_, st_), "xent stats");
+  }
   try {
     comms_.tp_allgather_f32(xstats_, xall_, static_cast<size_t>(M_) * 3, st_);
   } catch (const CommError& e) {

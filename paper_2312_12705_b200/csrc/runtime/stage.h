@@ -279,6 +279,7 @@ class Stage {
   bf16* hf_ = nullptr;
   float *muf_ = nullptr, *rsf_ = nullptr;
   bf16* logits_ = nullptr;
+  float2* rowstat_ = nullptr;  // [M][Vt/64] (max, sum exp) partials of the LM-head epilogue
   float *xstats_ = nullptr, *xall_ = nullptr, *row_loss_ = nullptr, *loss_acc_ = nullptr;
   StepTimes times_;
   std::vector<float> step_ms_;
